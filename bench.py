@@ -1,0 +1,353 @@
+#!/usr/bin/env python
+"""Benchmark of the fused data-parallel optimizer step (BASELINE.json metric:
+"fused AR+Adam/LAMB step time & NVLink-roofline fraction, 1/2/4/8 B200").
+
+Workload (BASELINE.json configs[1]): the BERT-large 336M gradient set — 398
+tensors, 336,232,258 elements — as a tensor list (no flatten), fp16 gradients,
+fp32 master weights and LAMB state; one step = ONE fused
+ReduceScatter + LAMB + AllGather launch over the whole list. Synthetic values
+are generated on the device (gen_decl_values semantics). The per-step traffic
+(~13 GB at N=1) is 100x the 126 MB L2, so no L2 flush is needed between steps.
+
+N=1: one GPU (one rank). N>1: torchrun, one process per GPU, peers mapped
+over NVLink (DISTRIBUTED mode), weak scaling (every rank holds a full gradient
+set, as in data parallelism). value = gradient elements reduced and applied
+per second over the whole job = N * 336,232,258 / step time.
+
+--impl reference times the reference's own CPU implementation (the UNMODIFIED
+ccopt Engine compiled in place, oracle/_ref) on the same workload definition:
+the authored LAMB fused program (tests/golden/lamb_fused_program.json) over a
+bounded sample, on every host core (one Engine per core).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "fused AR+Adam/LAMB step time & NVLink-roofline fraction, 1/2/4/8 B200"
+UNIT = "Gelem/s"
+NVLINK_GBS = 770.0  # measured peer copy per direction (B200_PROFILING.md)
+
+
+def peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d["hbm_gbs"]), float(d["bf16_tflops"]), "measured"
+    return 6650.0, 1590.0, "fallback"
+
+
+# ---------------------------------------------------------------------------
+# clocks sampled during the timed region (B200_PROFILING.md recipe)
+
+class ClockSampler:
+    def __init__(self, device: int):
+        self.device = device
+        self.samples = []
+        self.proc = None
+        self.thread = None
+
+    def start(self):
+        cmd = ["nvidia-smi", "-i", str(self.device),
+               "--query-gpu=clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+               "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+               "clocks_event_reasons.sw_power_cap", "--format=csv,noheader,nounits", "-lms", "100"]
+        try:
+            self.proc = subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except FileNotFoundError:
+            return
+
+        def rd():
+            for line in self.proc.stdout:
+                self.samples.append([x.strip() for x in line.split(",")])
+
+        self.thread = threading.Thread(target=rd, daemon=True)
+        self.thread.start()
+
+    def stop(self):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+        if self.thread:
+            self.thread.join(timeout=1)
+        rows = [s for s in self.samples if len(s) >= 7]
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
+        reasons = set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in rows:
+            for n, v in zip(names, r[3:7]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": float(rows[0][1]) if rows[0][1].replace(".", "").isdigit() else None,
+                "samples": len(rows), "reasons": sorted(reasons)}
+
+
+# ---------------------------------------------------------------------------
+# reference CPU path (oracle/_ref): the reference Engine on the LAMB program
+
+def reference_cpu(sample_elems: int, threads: int, steps: int = 1):
+    """Runs `threads` independent reference Engines concurrently (one per host
+    core; the reference's own Threaded mode only spawns one thread per rank,
+    runtime.hpp:287-296, i.e. one thread at W=1), each on an N=sample_elems
+    instance of the authored fused LAMB program at W=1. Returns (elem/s, wall)."""
+    from oracle import ref
+
+    base = (ROOT / "tests" / "golden" / "lamb_program.json").read_text()
+    fused = (ROOT / "tests" / "golden" / "lamb_fused_program.json").read_text()
+    sessions = []
+    for i in range(threads):
+        s = ref.RefSession(base, None, {"N": sample_elems, "W": 1}, sched_program=fused)
+        s.gen(1 + i)
+        sessions.append(s)
+    times = [0.0] * threads
+
+    def work(i):
+        t = 0.0
+        for _ in range(steps):
+            t += sessions[i].time_engine(1 + i, ref.ENGINE_SCHED)
+        times[i] = t
+
+    t0 = time.perf_counter()
+    ths = [threading.Thread(target=work, args=(i,)) for i in range(threads)]
+    for t in ths:
+        t.start()
+    for t in ths:
+        t.join()
+    wall = time.perf_counter() - t0
+    return threads * steps * sample_elems / wall, wall
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    from oracle import ref
+
+    if not ref.available():
+        print(json.dumps({"impl": "reference", "metric": METRIC,
+                          "unavailable": "oracle/_ref/libccopt_ref.so not built (needs /root/reference at build time)"}))
+        return
+    cores = os.cpu_count() or 1
+    sample = 1 << 18
+    # warmup steps, then timed steps; each step is a bounded sample per core
+    for _ in range(max(0, min(args.warmup, 1))):
+        reference_cpu(sample, cores, 1)
+    rate, wall = reference_cpu(sample, cores, args.steps)
+    value = rate / 1e9
+    from paper_2105_05720_b200.workloads import BERT_LARGE_PARAMS
+    ms = BERT_LARGE_PARAMS / rate * 1e3
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (gen_decl_values, seed per core)",
+        "config": {"workload": "BERT-336M LAMB step (398 tensors, 336,232,258 params), "
+                               "reference Engine on tests/golden/lamb_fused_program.json",
+                   "sample": f"{cores} concurrent Engines x N={sample} elements x {args.steps} steps, W=1",
+                   "ms_per_step_is": "extrapolated to 336,232,258 elements at the measured rate"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "reference",
+                         "sample": f"{cores} x {sample} elements x {args.steps} steps in {wall:.1f} s"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+
+
+# ---------------------------------------------------------------------------
+# the CUDA path
+
+def run_coconet(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2105_05720_b200 import _lib
+    from paper_2105_05720_b200.collectives import LambHParams, TensorList, fused_rs_lamb_ag, gen_values
+    from paper_2105_05720_b200.runtime import Context
+    from paper_2105_05720_b200.workloads import BERT_LARGE_PARAMS, bert_large_counts
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    assert world == args.gpus, f"--gpus {args.gpus} but WORLD_SIZE={world}"
+    torch.cuda.set_device(local_rank)
+    distributed = world > 1
+    if distributed:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    counts = bert_large_counts()
+    padded = [(n + 63) // 64 * 64 for n in counts]
+    W = world
+    need = sum(padded) * (2 + 4) + 2 * (sum(counts) // W + 64 * len(counts) + 4096) * 4 + (256 << 20)
+    ctx = Context(W, mode="distributed" if distributed else "virtual", rank=rank, device=local_rank,
+                  heap_bytes=need)
+    tl = TensorList(ctx, counts)
+    grads = [ctx.alloc([n], torch.float16) for n in counts]
+    params = [ctx.alloc([n], torch.float32) for n in counts]
+    m = ctx.alloc([tl.shard_elems], torch.float32)
+    v = ctx.alloc([tl.shard_elems], torch.float32)
+    my_ranks = ctx.local_ranks()
+    for r in my_ranks:
+        for i, n in enumerate(counts):
+            gen_values(ctx, ctx.view(grads[i], r), 1, f"g{i}", "local", r, [n], group_size=W)
+            gen_values(ctx, ctx.view(params[i], r), 1, f"p{i}", "replicated", r, [n], group_size=W)
+        ctx.view(m, r).uniform_(-1e-3, 1e-3)
+        ctx.view(v, r).uniform_(1e-4, 1e-3)
+    hp = LambHParams(lr=1e-3, beta1=0.9, beta2=0.999, t=1.0, eps=1e-6, wd=0.01)
+    stream = torch.cuda.current_stream()
+    torch.cuda.synchronize()
+
+    def step():
+        fused_rs_lamb_ag(ctx, tl, grads, params, m, v, hp)
+
+    def barrier():
+        torch.cuda.synchronize()
+        if distributed:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        step()
+    ctx.check()
+    barrier()
+    sampler = ClockSampler(local_rank)
+    sampler.start()
+    launches0 = ctx.launch_count()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        step()
+    e1.record(stream)
+    barrier()
+    clocks = sampler.stop()
+    ctx.check()
+    launches = ctx.launch_count() - launches0
+    ms = e0.elapsed_time(e1) / args.steps
+    if distributed:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    N = BERT_LARGE_PARAMS
+    value = W * N / (ms * 1e-3) / 1e9
+
+    # -- e2e: through the public API with HOST buffers (pinned), H2D of the
+    # step's gradients and D2H of the updated parameters inside the timed region
+    h_grads = [torch.empty(n, dtype=torch.float16, pin_memory=True) for n in counts]
+    h_params = [torch.empty(n, dtype=torch.float32, pin_memory=True) for n in counts]
+    me = my_ranks[0]
+    for i in range(len(counts)):
+        h_grads[i].copy_(ctx.view(grads[i], me))
+    barrier()
+    e2e_steps = max(2, min(args.steps, 5))
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        for i in range(len(counts)):
+            ctx.view(grads[i], me).copy_(h_grads[i], non_blocking=True)
+        step()
+        for i in range(len(counts)):
+            h_params[i].copy_(ctx.view(params[i], me), non_blocking=True)
+        torch.cuda.synchronize()
+    barrier()
+    e2e_s = (time.perf_counter() - t0) / e2e_steps
+    if distributed:
+        t = torch.tensor([e2e_s], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    h2d = sum(counts) * 2
+    d2h = sum(counts) * 4
+
+    # -- roofline of the dominant (only) kernel
+    hbm_peak, tc_peak, peak_kind = peaks()
+    shard = N / W
+    # per-rank HBM bytes: W=1 two-pass LAMB = 38 B/elem; W>1 the
+    # shard's 38 B minus its g read / p write (served by the peers' HBM) plus this
+    # rank's whole g read by its owners (2N) and whole p written by them (4N)
+    hbm_bytes = 38.0 * shard if W == 1 else 32.0 * shard + 6.0 * N
+    nvl_bytes = (W - 1) / W * N * (2 + 4)
+    if W == 1:
+        achieved = hbm_bytes / (ms * 1e-3) / 1e9
+        roof = {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+                "frac": achieved / hbm_peak, "peak_kind": peak_kind,
+                "algorithmic_bytes_per_launch": hbm_bytes}
+    else:
+        achieved = nvl_bytes / (ms * 1e-3) / 1e9
+        roof = {"bound": "nvlink", "achieved": achieved, "peak": NVLINK_GBS, "unit": "GB/s",
+                "frac": achieved / NVLINK_GBS, "peak_kind": "measured peer copy (B200_PROFILING.md)",
+                "algorithmic_bytes_per_launch": nvl_bytes}
+    prof = ROOT / "profiles" / "ncu_traffic.json"
+    roof["traffic"] = None
+    if prof.exists():
+        try:
+            roof["traffic"] = json.loads(prof.read_text()).get("lamb_kernel", {}).get("dram_bytes_per_launch")
+        except Exception:
+            pass
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            from oracle import ref
+            if ref.available():
+                cores = os.cpu_count() or 1
+                rate, wall = reference_cpu(1 << 18, cores, 1)
+                cpu = {"value": rate / 1e9, "unit": UNIT, "cores": cores, "kind": "reference",
+                       "sample": f"{cores} concurrent reference Engines x 262144-element LAMB "
+                                 f"(tests/golden/lamb_fused_program.json, W=1) in {wall:.1f} s"}
+        except Exception as e:  # the baseline is reported, not required
+            cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "reference", "sample": f"failed: {e}"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (device-generated, gen_decl_values semantics)",
+            "config": {"workload": "BERT-336M LAMB step: 398-tensor list, 336,232,258 params, fp16 grads, "
+                                   "fp32 master weights + m/v, fused ReduceScatter+LAMB+AllGather",
+                       "global_batch": None, "seq_len": None, "parallelism": f"dp{world}",
+                       "l2": "per-step traffic ~13 GB >> 126 MB L2 (no flush needed)",
+                       "math": "FAST (fp32 element math, fp64 norms)"},
+            "roofline": roof, "cpu_baseline": cpu,
+            "e2e": {"value": W * N / e2e_s / 1e9, "unit": UNIT, "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": d2h,
+                    "what": "pinned H2D of this rank's fp16 grads + fused step + D2H of updated fp32 params"},
+            "gpu_launches": launches, "clocks": clocks,
+            "kernel_ms": ms,
+        }
+        print(json.dumps(line))
+    ctx.close()
+    if distributed:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="coconet", choices=["coconet", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_coconet(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,105 @@
+"""Generates tests/golden/*.json from the UNMODIFIED reference (oracle/_ref).
+
+Run here (where /root/reference exists):  python -m oracle.make_golden
+The GPU box has no /root/reference; the tests there use these committed
+fixtures plus the numpy restatement (oracle/coconet_oracle.py).
+
+For every case it records, at concrete sizes: the base and scheduled programs
+as the reference serialises them (program_to_json, json_io.hpp:359-401), the
+reference Engine's digest on the scheduled program (exact-mode target), the
+oracle's digest on the base program, their deviation, the Engine's
+RunReport counters, and per-result-key digests.
+"""
+from __future__ import annotations
+
+import json
+import sys
+from pathlib import Path
+
+import numpy as np
+
+from oracle import coconet_oracle as co
+from oracle import ref
+
+ROOT = Path(__file__).resolve().parent.parent
+REF = Path("/root/reference/proj")
+OUT = ROOT / "tests" / "golden"
+
+ADAM_CASES = [(w, n) for w in (1, 2, 4, 8) for n in (1024, 4096)] + [(4, 1 << 20), (8, 1 << 16)]
+MP_CASES = [(w, dims) for w in (1, 2, 4) for dims in ({"B": 2, "S": 8, "H": 64},)] + [
+    (8, {"B": 2, "S": 16, "H": 128})]
+PP_CASES = [(w, n) for w in (2, 4, 8) for n in (1024, 4096)]
+
+
+def key_digests(sess, which):
+    return {k: "%016x" % co.digest_results({k: v}) for k, v in sess.results(which).items()}
+
+
+def run_case(name, program, schedule, dims, seed=1, sched_program=None):
+    s = ref.RefSession(program, schedule, dims, sched_program=sched_program)
+    s.gen(seed)
+    s.run(seed, ref.ORACLE)
+    s.run(seed, ref.ENGINE_SCHED)
+    s.run(seed, ref.ENGINE_BASE)
+    rec = {
+        "name": name, "dims": dims, "seed": seed,
+        "base_program": s.program_json(0), "sched_program": s.program_json(1),
+        "engine_sched_digest": "%016x" % s.digest(ref.ENGINE_SCHED),
+        "engine_base_digest": "%016x" % s.digest(ref.ENGINE_BASE),
+        "oracle_digest": "%016x" % s.digest(ref.ORACLE),
+        "deviation_sched_vs_oracle": s.compare(ref.ORACLE, ref.ENGINE_SCHED),
+        "report_sched": s.report(ref.ENGINE_SCHED),
+        "report_base": s.report(ref.ENGINE_BASE),
+        "key_digests_sched": key_digests(s, ref.ENGINE_SCHED),
+        "key_digests_oracle": key_digests(s, ref.ORACLE),
+    }
+    for r in (rec["report_sched"], rec["report_base"]):
+        r.pop("wall_s", None)
+    return rec
+
+
+def main():
+    if not ref.available():
+        sys.exit("oracle/_ref/libccopt_ref.so missing: make -C oracle ref")
+    OUT.mkdir(parents=True, exist_ok=True)
+    adam = REF / "goldens" / "adam.json"
+    adam_s = REF / "schedules" / "adam_fused.json"
+    recs = []
+    for w, n in ADAM_CASES:
+        dims = {"N": n, "W": w, "B": 2, "S": 8, "H": 64}
+        recs.append(run_case(f"adam_W{w}_N{n}", adam.read_text(), adam_s.read_text(), dims))
+    (OUT / "adam_cases.json").write_text(json.dumps(recs, indent=1))
+    mp = REF / "goldens" / "model_parallel.json"
+    mp_s = REF / "schedules" / "mp_overlap.json"
+    recs = []
+    for w, d in MP_CASES:
+        dims = dict(d, N=1024, W=w)
+        recs.append(run_case(f"mp_W{w}_B{d['B']}_S{d['S']}_H{d['H']}", mp.read_text(), mp_s.read_text(), dims))
+    (OUT / "mp_cases.json").write_text(json.dumps(recs, indent=1))
+    pp = REF / "goldens" / "pipeline.json"
+    pp_s = REF / "schedules" / "pipeline_overlap.json"
+    recs = []
+    for w, n in PP_CASES:
+        dims = {"N": n, "W": w, "B": 2, "S": 8, "H": 64}
+        recs.append(run_case(f"pp_W{w}_N{n}", pp.read_text(), pp_s.read_text(), dims))
+    (OUT / "pp_cases.json").write_text(json.dumps(recs, indent=1))
+    # KAT: AdamScalarChainFrozenValues (test_oracle.cpp:24-48), through the reference
+    # N=4 (not 1): the fused schedule needs N % W == 0 (as_slice, transform.hpp:553)
+    s = ref.RefSession(adam.read_text(), adam_s.read_text(), {"N": 4, "W": 4, "B": 2, "S": 8, "H": 64})
+    s.gen(1)
+    consts = {"p": 1.0, "m": 0.0, "v": 0.0, "lr": 0.01, "beta1": 0.9, "beta2": 0.999, "t": 1.0}
+    for r in range(4):
+        s.set("g", r, np.ones(4, np.float32))
+        for k, val in consts.items():
+            s.set(k, r, np.full(4 if k in ("p", "m", "v") else 1, val, np.float32))
+    s.run(1, ref.ORACLE)
+    s.run(1, ref.ENGINE_SCHED)
+    kat = {"inputs": dict(consts, g=1.0, W=4),
+           "oracle": {k: s.value(k, 0, 4).tolist()[0] for k in ("avg", "m_", "v_", "m1", "v1", "p_", "p", "m")},
+           "engine_sched": {k: v[0].tolist() for k, v in s.results(ref.ENGINE_SCHED).items()}}
+    (OUT / "adam_kat.json").write_text(json.dumps(kat, indent=1))
+    print("wrote", sorted(p.name for p in OUT.glob("*.json")))
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,218 @@
+"""Python wrappers of the fused compute/communication entry points.
+
+Every function is collective over its group and asynchronous on the current
+torch stream; buffers are `SymmBuffer`s of the context (same offset on every
+rank). See include/coconet_cuda.h for the reference routine each one replaces.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._lib import check, i64_array, ptr_array
+from .runtime import Context, SymmBuffer, elem_of
+
+FNV_OFFSET = 0xcbf29ce484222325
+FNV_PRIME = 0x100000001b3
+
+
+def fnv1a(s: str | bytes, h: int = FNV_OFFSET) -> int:
+    """ccopt::fnv1a (types.hpp:161-170) — decl keys, dropout keys."""
+    data = s.encode() if isinstance(s, str) else s
+    for b in data:
+        h ^= b
+        h = (h * FNV_PRIME) & 0xFFFFFFFFFFFFFFFF
+    return h
+
+
+class TensorList:
+    """Device bucket table (BucketTable, runtime.hpp:575-614) for a list of
+    tensors with element counts `counts`, on group `group`."""
+
+    def __init__(self, ctx: Context, counts, group: int = 0, bucket_cap: int = 1024):
+        self.ctx = ctx
+        self.counts = [int(c) for c in counts]
+        self.group = group
+        h = C.c_void_p()
+        check(ctx.lib.coconet_tlist_create(ctx.handle, group, len(self.counts),
+                                           i64_array(self.counts), bucket_cap, C.byref(h)))
+        self.handle = h
+        lib = ctx.lib
+        self.total = int(lib.coconet_tlist_total(h))
+        self.shard_elems = int(lib.coconet_tlist_shard_elems(h))
+        self.state_elems = int(lib.coconet_tlist_state_elems(h))
+        self.n_buckets = int(lib.coconet_tlist_buckets(h))
+        self.metadata_bytes = int(lib.coconet_tlist_metadata_bytes(h))
+
+    def chunk(self, r: int) -> tuple[int, int]:
+        lo, hi = C.c_int64(), C.c_int64()
+        check(self.ctx.lib.coconet_tlist_chunk(self.handle, r, C.byref(lo), C.byref(hi)))
+        return lo.value, hi.value
+
+    def segments(self, r: int) -> np.ndarray:
+        """[n, 4] int64 (tensor, toff, len, state index) of rank r's segments
+        (r = -1: the ONE_SHOT table)."""
+        n = self.n_buckets + 16
+        bufs = [(C.c_int64 * n)() for _ in range(4)]
+        got = int(self.ctx.lib.coconet_tlist_segments(self.handle, r, *bufs, n))
+        check(0 if got >= 0 else 3)
+        return np.stack([np.frombuffer(b, dtype=np.int64)[:got] for b in bufs], axis=1)
+
+    def state_index_map(self, r: int):
+        """(tensor, element, state index) arrays of every element rank r owns."""
+        segs = self.segments(r)
+        if len(segs) == 0:
+            z = np.zeros(0, np.int64)
+            return z, z, z
+        lens = segs[:, 2]
+        rep = np.repeat(np.arange(len(segs)), lens)
+        within = np.arange(int(lens.sum())) - np.repeat(np.cumsum(lens) - lens, lens)
+        return segs[rep, 0], segs[rep, 1] + within, segs[rep, 3] + within
+
+    def shard_index(self, pos: int) -> int:
+        return int(self.ctx.lib.coconet_tlist_shard_index(self.handle, pos))
+
+    def close(self):
+        if self.handle:
+            self.ctx.lib.coconet_tlist_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def _ptrs(ctx: Context, bufs):
+    return ptr_array([ctx.ptr(b) for b in bufs])
+
+
+@dataclass
+class AdamHParams:
+    lr: float
+    beta1: float
+    beta2: float
+    t: float
+    eps: float = 0.0
+    cv_beta1: bool = True   # the golden's (1-beta1) second-moment coefficient
+    math: int = _lib.MATH_EXACT
+    algo: int = _lib.ALGO_AUTO
+
+
+@dataclass
+class LambHParams:
+    lr: float
+    beta1: float
+    beta2: float
+    t: float
+    eps: float = 1e-6
+    wd: float = 0.01
+    math: int = _lib.MATH_FAST
+
+
+def fused_rs_adam_ag(ctx: Context, tl: TensorList, grads, params, m: SymmBuffer, v: SymmBuffer,
+                     hp: AdamHParams, stream=None) -> None:
+    """ReduceScatter + Adam + AllGather (FusedAllReduce, runtime.hpp:471-516)."""
+    g_elem = elem_of(grads[0].dtype)
+    p = _lib.AdamParams(hp.lr, hp.beta1, hp.beta2, hp.t, hp.eps, int(hp.cv_beta1), hp.math, hp.algo)
+    check(ctx.lib.coconet_fused_rs_adam_ag(
+        ctx.handle, tl.handle, _ptrs(ctx, grads), g_elem, _ptrs(ctx, params), ctx.ptr(m), ctx.ptr(v),
+        C.byref(p), ctx.stream_ptr(stream)))
+
+
+def fused_rs_lamb_ag(ctx: Context, tl: TensorList, grads, params, m: SymmBuffer, v: SymmBuffer,
+                     hp: LambHParams, stream=None) -> None:
+    g_elem = elem_of(grads[0].dtype)
+    p = _lib.LambParams(hp.lr, hp.beta1, hp.beta2, hp.t, hp.eps, hp.wd, hp.math)
+    check(ctx.lib.coconet_fused_rs_lamb_ag(
+        ctx.handle, tl.handle, _ptrs(ctx, grads), g_elem, _ptrs(ctx, params), ctx.ptr(m), ctx.ptr(v),
+        C.byref(p), ctx.stream_ptr(stream)))
+
+
+def allreduce(ctx: Context, tl: TensorList, xs, outs, reducer: int = _lib.SUM,
+              algo: int = _lib.ALGO_AUTO, stream=None) -> None:
+    """Tensor-list AllReduce (runtime.hpp:384-395; scattered_collective :624-675)."""
+    check(ctx.lib.coconet_allreduce(ctx.handle, tl.handle, _ptrs(ctx, xs), _ptrs(ctx, outs),
+                                    elem_of(xs[0].dtype), reducer, algo, ctx.stream_ptr(stream)))
+
+
+def reduce_scatter(ctx: Context, x: SymmBuffer, out: SymmBuffer, axis: int = -1, group: int = 0,
+                   reducer: int = _lib.SUM, stream=None) -> None:
+    shape = i64_array(x.shape)
+    check(ctx.lib.coconet_reduce_scatter(ctx.handle, group, ctx.ptr(x), ctx.ptr(out),
+                                         elem_of(x.dtype), reducer, len(x.shape), shape,
+                                         axis if axis >= 0 else len(x.shape) - 1,
+                                         ctx.stream_ptr(stream)))
+
+
+def all_gather(ctx: Context, x: SymmBuffer | None, out: SymmBuffer, axis: int = -1, group: int = 0,
+               stream=None) -> None:
+    shape = i64_array(out.shape)
+    check(ctx.lib.coconet_all_gather(ctx.handle, group, ctx.ptr(x) if x is not None else None,
+                                     ctx.ptr(out), elem_of(out.dtype), len(out.shape), shape,
+                                     axis if axis >= 0 else len(out.shape) - 1,
+                                     ctx.stream_ptr(stream)))
+
+
+def gen_values(ctx: Context, dst: torch.Tensor, seed: int, name: str, layout: str, rank: int,
+               global_shape, sliced_dim: int = -1, group_size: int = 1, stream=None) -> None:
+    """gen_decl_values (state.hpp:55-74) for one decl on one rank, on device."""
+    shape = i64_array(global_shape)
+    check(ctx.lib.coconet_gen_values(ctx.handle, C.c_void_p(dst.data_ptr()), elem_of(dst.dtype),
+                                     seed & 0xFFFFFFFFFFFFFFFF, fnv1a(name), int(layout == "local"),
+                                     rank, len(global_shape), shape, sliced_dim, group_size,
+                                     ctx.stream_ptr(stream)))
+
+
+@dataclass
+class BdrHParams:
+    rate: float
+    seed: int
+    key: int
+    math: int = _lib.MATH_EXACT
+
+    def c(self):
+        return _lib.BdrParams(self.rate, self.seed, self.key, self.math)
+
+
+def fused_rs_bdr_ag(ctx: Context, x: SymmBuffer, b: SymmBuffer, r: SymmBuffer, out: SymmBuffer,
+                    hp: BdrHParams, group: int = 0, stream=None) -> None:
+    rows = int(np.prod(x.shape[:-1])) if len(x.shape) > 1 else 1
+    p = hp.c()
+    check(ctx.lib.coconet_fused_rs_bdr_ag(ctx.handle, group, ctx.ptr(x), ctx.ptr(b), ctx.ptr(r),
+                                          ctx.ptr(out), elem_of(x.dtype), rows, x.shape[-1],
+                                          C.byref(p), ctx.stream_ptr(stream)))
+
+
+def rs_fused_send_ag(ctx: Context, src_group: int, dst_group: int, x: SymmBuffer, b: SymmBuffer,
+                     r: SymmBuffer, out: SymmBuffer, hp: BdrHParams, stream=None) -> None:
+    p = hp.c()
+    check(ctx.lib.coconet_rs_fused_send_ag(ctx.handle, src_group, dst_group, ctx.ptr(x), ctx.ptr(b),
+                                           ctx.ptr(r), ctx.ptr(out), elem_of(x.dtype), x.numel,
+                                           C.byref(p), ctx.stream_ptr(stream)))
+
+
+def matmul(ctx: Context, a: SymmBuffer, b: SymmBuffer, c: SymmBuffer, math: int = _lib.MATH_FAST,
+           group: int = 0, stream=None) -> None:
+    m = int(np.prod(a.shape[:-1]))
+    k = a.shape[-1]
+    n = b.shape[-1]
+    check(ctx.lib.coconet_matmul(ctx.handle, group, ctx.ptr(a), ctx.ptr(b), ctx.ptr(c),
+                                 elem_of(a.dtype), elem_of(c.dtype), m, n, k, math,
+                                 ctx.stream_ptr(stream)))
+
+
+def mm_overlap_fused_ar(ctx: Context, a: SymmBuffer, w: SymmBuffer, b: SymmBuffer, r: SymmBuffer,
+                        partial: SymmBuffer, out: SymmBuffer, hp: BdrHParams, group: int = 0,
+                        stream=None) -> None:
+    rows = int(np.prod(a.shape[:-1]))
+    p = hp.c()
+    check(ctx.lib.coconet_mm_overlap_fused_ar(ctx.handle, group, ctx.ptr(a), ctx.ptr(w), ctx.ptr(b),
+                                              ctx.ptr(r), ctx.ptr(partial), ctx.ptr(out),
+                                              elem_of(a.dtype), rows, w.shape[-1], a.shape[-1],
+                                              C.byref(p), ctx.stream_ptr(stream)))

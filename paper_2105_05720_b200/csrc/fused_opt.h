@@ -1,0 +1,56 @@
+// Tensor-list structures shared by the fused optimizer and AllReduce kernels.
+#pragma once
+
+#include <vector>
+
+#include "internal.h"
+
+namespace coconet {
+
+// One unit of work: a bucket (or the part of a bucket inside one flat chunk)
+// of one tensor. 24 bytes; read once per segment by a whole warp (broadcast).
+struct Seg {
+  int64_t toff;  // element offset inside the tensor
+  int64_t sidx;  // index of the first element in shard/state storage (== toff mod 4)
+  int64_t meta;  // tensor (32 bits) | len (24 bits) | owner rank (8 bits)
+};
+
+__host__ __device__ __forceinline__ int64_t pack_meta(int tensor, int len, int owner) {
+  return (int64_t(tensor) << 32) | (int64_t(len & 0xffffff) << 8) | int64_t(owner & 0xff);
+}
+__host__ __device__ __forceinline__ int meta_tensor(int64_t m) { return int(m >> 32); }
+__host__ __device__ __forceinline__ int meta_len(int64_t m) { return int((m >> 8) & 0xffffff); }
+__host__ __device__ __forceinline__ int meta_owner(int64_t m) { return int(m & 0xff); }
+
+}  // namespace coconet
+
+struct coconet_tlist {
+  coconet_ctx* ctx = nullptr;
+  int group = 0;
+  int n_tensors = 0;
+  int64_t bucket_cap = 1024;
+  std::vector<int64_t> counts;
+  int64_t total = 0;
+  int64_t n_buckets = 0;
+  int64_t n_segs = 0;
+  int64_t chunk_lo[coconet::kMaxRanks + 1] = {};
+  int64_t seg_begin[coconet::kMaxRanks + 1] = {};  // TWO_SHOT table of rank r
+  int64_t csr_begin[coconet::kMaxRanks] = {};      // per-rank per-tensor segment lists
+  int64_t os_begin = 0, os_end = 0;                // ONE_SHOT table
+  int64_t shard_elems = 0;
+  int64_t full_state_elems = 0;
+  int64_t metadata_bytes = 0;
+  std::vector<int64_t> host_flat, host_sidx;  // TWO_SHOT segments, flat order
+  std::vector<int64_t> last_offs;
+  void* dev_mem = nullptr;
+  coconet::Seg* d_segs = nullptr;
+  int64_t* d_csr_ptr = nullptr;
+  int64_t* d_csr_idx = nullptr;
+  int64_t* d_offs = nullptr;       // [2][n_tensors] heap offsets bound per call
+  double* d_seg_part = nullptr;    // per-segment partial sums (LAMB)
+};
+
+namespace coconet {
+int tlist_bind(coconet_tlist* tl, const void* const* a, const void* const* b, int a_elem_bytes,
+               int b_elem_bytes, cudaStream_t stream);
+}

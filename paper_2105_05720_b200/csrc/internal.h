@@ -1,0 +1,68 @@
+// Host-side internals of libcoconet_cuda (context, groups, errors, launches).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+#include "coconet_cuda.h"
+
+struct coconet_group_s {
+  int first = 0;
+  int size = 1;
+  uint32_t epoch = 0;  // calls issued on this group (flag value)
+};
+
+struct coconet_ctx {
+  int mode = COCONET_MODE_VIRTUAL;
+  int world = 1;
+  int rank = 0;  // distributed: this process; virtual: 0
+  int device = 0;
+  int sm_count = 148;
+  size_t heap_bytes = 0;  // per rank, including the reserved pad
+  char* heap[coconet::kMaxRanks] = {};
+  bool peer_mapped[coconet::kMaxRanks] = {};
+  cudaIpcMemHandle_t my_handle{};
+  size_t heap_used = coconet::kReservedBytes;
+  int* status_host = nullptr;  // host-mapped watchdog word
+  int* status_dev = nullptr;
+  uint64_t timeout_ns = 20ull * 1000 * 1000 * 1000;
+  uint64_t launches = 0;
+  std::vector<coconet_group_s> groups;
+};
+
+namespace coconet {
+
+int set_error(int status, const std::string& msg);
+int cuda_fail(cudaError_t e, const char* what);
+
+#define CN_CUDA(call)                                            \
+  do {                                                           \
+    cudaError_t _e = (call);                                     \
+    if (_e != cudaSuccess) return ::coconet::cuda_fail(_e, #call); \
+  } while (0)
+
+// Ranks resident on this device for a launch over `group`.
+inline int local_ranks(const coconet_ctx* c, int group) {
+  return c->mode == COCONET_MODE_VIRTUAL ? c->groups[size_t(group)].size : 1;
+}
+
+// Builds the RankSet for one collective launch on `group` and bumps its epoch.
+int make_rankset(coconet_ctx* c, int group, RankSet* rs);
+
+// Heap offset of a caller pointer (own rank's heap; virtual: rank 0's).
+int heap_offset(const coconet_ctx* c, const void* p, int64_t* off);
+
+// Blocks per rank for a cooperative launch of `func`.
+int coop_blocks(coconet_ctx* c, const void* func, int threads, size_t smem, int group,
+                int64_t want, int* blocks);
+
+int coop_launch(coconet_ctx* c, const void* func, dim3 grid, dim3 block, void** args,
+                size_t smem, cudaStream_t stream);
+
+bool valid_group(const coconet_ctx* c, int group);
+
+}  // namespace coconet

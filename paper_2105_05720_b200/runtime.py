@@ -1,0 +1,161 @@
+"""Context and symmetric memory (Python side of include/coconet_cuda.h).
+
+A `Context` owns one symmetric heap per rank. `SymmBuffer` is an allocation
+with the same offset on every rank; `ctx.view(buf, r)` is rank r's copy as a
+torch tensor (zero-copy, via __cuda_array_interface__).
+
+VIRTUAL mode keeps all W ranks on one device in this process — the
+reference's own in-process rank model (state.hpp:17-20) — and one call runs
+every rank. DISTRIBUTED mode is one process per GPU: heap handles are
+exchanged through torch.distributed (any backend; NCCL is only bootstrap) and
+peers are mapped over NVLink.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import torch
+
+from . import _lib
+from ._lib import check, load
+
+_DTYPES = {torch.float32: _lib.F32, torch.float16: _lib.F16, torch.bfloat16: _lib.BF16}
+
+
+def elem_of(dtype: torch.dtype) -> int:
+    try:
+        return _DTYPES[dtype]
+    except KeyError:
+        raise _lib.CoconetError(3, f"unsupported dtype {dtype}") from None
+
+
+class _CAI:
+    """Minimal __cuda_array_interface__ exporter for a raw device range."""
+
+    def __init__(self, ptr: int, nbytes: int):
+        self.__cuda_array_interface__ = {
+            "shape": (nbytes,), "typestr": "|u1", "data": (ptr, False), "version": 3,
+            "strides": None,
+        }
+
+
+@dataclass(frozen=True)
+class SymmBuffer:
+    offset: int
+    shape: tuple
+    dtype: torch.dtype
+
+    @property
+    def numel(self) -> int:
+        n = 1
+        for s in self.shape:
+            n *= int(s)
+        return n
+
+    @property
+    def nbytes(self) -> int:
+        return self.numel * torch.empty((), dtype=self.dtype).element_size()
+
+
+class Context:
+    def __init__(self, world: int, mode: str = "virtual", rank: int = 0, device: int = 0,
+                 heap_bytes: int = 1 << 30, process_group=None, timeout_ms: int | None = None):
+        self.lib = load()
+        self.world = int(world)
+        self.mode = mode
+        self.rank = int(rank) if mode == "distributed" else 0
+        self.device = int(device)
+        m = _lib.MODE_VIRTUAL if mode == "virtual" else _lib.MODE_DISTRIBUTED
+        h = C.c_void_p()
+        torch.cuda.set_device(self.device)
+        torch.cuda.init()
+        check(self.lib.coconet_init(C.byref(h), m, self.rank, self.world, self.device, heap_bytes))
+        self.handle = h
+        if timeout_ms is not None:
+            check(self.lib.coconet_set_timeout_ms(h, int(timeout_ms)))
+        if mode == "distributed":
+            self._open_peers(process_group)
+        self._heap_bytes = None
+        self._heaps: dict[int, torch.Tensor] = {}
+        self.groups = {0: (0, self.world)}
+
+    # -- bootstrap -------------------------------------------------------------
+    def _open_peers(self, pg):
+        import torch.distributed as dist
+
+        n = C.c_size_t(0)
+        check(self.lib.coconet_heap_handle(self.handle, None, C.byref(n)))
+        buf = (C.c_char * n.value)()
+        check(self.lib.coconet_heap_handle(self.handle, buf, C.byref(n)))
+        mine = bytes(buf)
+        allh = [None] * self.world
+        dist.all_gather_object(allh, mine, group=pg)
+        blob = b"".join(allh)
+        check(self.lib.coconet_open_peers(self.handle, C.c_char_p(blob), n.value))
+        dist.barrier(group=pg)
+
+    def close(self):
+        if self.handle:
+            torch.cuda.synchronize(self.device)
+            self._heaps.clear()
+            self.lib.coconet_finalize(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # -- memory ------------------------------------------------------------------
+    def local_ranks(self):
+        return list(range(self.world)) if self.mode == "virtual" else [self.rank]
+
+    def _heap(self, rank: int) -> torch.Tensor:
+        t = self._heaps.get(rank)
+        if t is None:
+            base = self.lib.coconet_symm_ptr(self.handle, rank, 0)
+            if not base:
+                raise _lib.CoconetError(14, f"rank {rank}'s heap is not addressable here")
+            size = int(self.lib.coconet_heap_bytes(self.handle))
+            t = torch.as_tensor(_CAI(base, size), device=f"cuda:{self.device}")
+            self._heaps[rank] = t
+        return t
+
+    def alloc(self, shape, dtype=torch.float32) -> SymmBuffer:
+        shape = tuple(int(s) for s in (shape if isinstance(shape, (tuple, list)) else (shape,)))
+        buf = SymmBuffer(0, shape, dtype)
+        off = C.c_size_t(0)
+        check(self.lib.coconet_symm_alloc(self.handle, max(1, buf.nbytes), C.byref(off)))
+        return SymmBuffer(off.value, shape, dtype)
+
+    def reset(self):
+        check(self.lib.coconet_symm_reset(self.handle))
+
+    def view(self, buf: SymmBuffer, rank: int | None = None) -> torch.Tensor:
+        r = self.rank if rank is None else rank
+        h = self._heap(r)
+        return h[buf.offset:buf.offset + buf.nbytes].view(buf.dtype).view(buf.shape)
+
+    def ptr(self, buf: SymmBuffer, rank: int | None = None) -> int:
+        r = (0 if self.mode == "virtual" else self.rank) if rank is None else rank
+        return int(self.lib.coconet_symm_ptr(self.handle, r, buf.offset))
+
+    # -- groups / sync -------------------------------------------------------------
+    def group(self, first_rank: int, size: int) -> int:
+        g = C.c_int(0)
+        check(self.lib.coconet_group_create(self.handle, first_rank, size, C.byref(g)))
+        self.groups[g.value] = (first_rank, size)
+        return g.value
+
+    @staticmethod
+    def stream_ptr(stream=None) -> int:
+        s = stream if stream is not None else torch.cuda.current_stream()
+        return int(s.cuda_stream)
+
+    def check(self, stream=None):
+        check(self.lib.coconet_check(self.handle, C.c_void_p(self.stream_ptr(stream))))
+
+    def launch_count(self) -> int:
+        return int(self.lib.coconet_launch_count(self.handle))
