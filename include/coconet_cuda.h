@@ -131,6 +131,10 @@ int coconet_gen_values(coconet_ctx_t ctx, void* dst, int out_elem, uint64_t seed
  * c is owned by group rank c. Built once, reused every step (paper §5.4). */
 int coconet_tlist_create(coconet_ctx_t ctx, int group, int n_tensors, const int64_t* counts,
                          int64_t bucket_cap, coconet_tlist_t* out);
+/* Host-only plan of the same tables for a group of `world` ranks (no device,
+ * no context): for inspection and CPU tests; cannot be passed to kernels. */
+int coconet_tlist_plan(int world, int n_tensors, const int64_t* counts, int64_t bucket_cap,
+                       coconet_tlist_t* out);
 int coconet_tlist_destroy(coconet_tlist_t tl);
 /* Elements of shard storage each rank needs for sliced state (m, v): the
  * owned flat chunk plus alignment padding (so shard quads align with tensor

@@ -83,6 +83,7 @@ _SIGNATURES = {
     "coconet_launch_count": (_U64, [_P]),
     "coconet_gen_values": (_I, [_P, _P, _I, _U64, _U64, _I, _I, _I, _PI64, _I, _I, _P]),
     "coconet_tlist_create": (_I, [_P, _I, _I, _PI64, _I64, C.POINTER(_P)]),
+    "coconet_tlist_plan": (_I, [_I, _I, _PI64, _I64, C.POINTER(_P)]),
     "coconet_tlist_destroy": (_I, [_P]),
     "coconet_tlist_shard_elems": (_I64, [_P]),
     "coconet_tlist_total": (_I64, [_P]),

@@ -33,15 +33,22 @@ class TensorList:
     """Device bucket table (BucketTable, runtime.hpp:575-614) for a list of
     tensors with element counts `counts`, on group `group`."""
 
-    def __init__(self, ctx: Context, counts, group: int = 0, bucket_cap: int = 1024):
+    def __init__(self, ctx: Context | None, counts, group: int = 0, bucket_cap: int = 1024,
+                 world: int | None = None):
+        """ctx=None builds a host-only plan for `world` ranks (no device)."""
         self.ctx = ctx
         self.counts = [int(c) for c in counts]
         self.group = group
         h = C.c_void_p()
-        check(ctx.lib.coconet_tlist_create(ctx.handle, group, len(self.counts),
+        lib = ctx.lib if ctx is not None else _lib.load()
+        self.lib = lib
+        if ctx is None:
+            check(lib.coconet_tlist_plan(int(world), len(self.counts), i64_array(self.counts),
+                                         bucket_cap, C.byref(h)))
+        else:
+            check(lib.coconet_tlist_create(ctx.handle, group, len(self.counts),
                                            i64_array(self.counts), bucket_cap, C.byref(h)))
         self.handle = h
-        lib = ctx.lib
         self.total = int(lib.coconet_tlist_total(h))
         self.shard_elems = int(lib.coconet_tlist_shard_elems(h))
         self.state_elems = int(lib.coconet_tlist_state_elems(h))
@@ -50,7 +57,7 @@ class TensorList:
 
     def chunk(self, r: int) -> tuple[int, int]:
         lo, hi = C.c_int64(), C.c_int64()
-        check(self.ctx.lib.coconet_tlist_chunk(self.handle, r, C.byref(lo), C.byref(hi)))
+        check(self.lib.coconet_tlist_chunk(self.handle, r, C.byref(lo), C.byref(hi)))
         return lo.value, hi.value
 
     def segments(self, r: int) -> np.ndarray:
@@ -58,7 +65,7 @@ class TensorList:
         (r = -1: the ONE_SHOT table)."""
         n = self.n_buckets + 16
         bufs = [(C.c_int64 * n)() for _ in range(4)]
-        got = int(self.ctx.lib.coconet_tlist_segments(self.handle, r, *bufs, n))
+        got = int(self.lib.coconet_tlist_segments(self.handle, r, *bufs, n))
         check(0 if got >= 0 else 3)
         return np.stack([np.frombuffer(b, dtype=np.int64)[:got] for b in bufs], axis=1)
 
@@ -74,11 +81,11 @@ class TensorList:
         return segs[rep, 0], segs[rep, 1] + within, segs[rep, 3] + within
 
     def shard_index(self, pos: int) -> int:
-        return int(self.ctx.lib.coconet_tlist_shard_index(self.handle, pos))
+        return int(self.lib.coconet_tlist_shard_index(self.handle, pos))
 
     def close(self):
         if self.handle:
-            self.ctx.lib.coconet_tlist_destroy(self.handle)
+            self.lib.coconet_tlist_destroy(self.handle)
             self.handle = None
 
     def __del__(self):

@@ -25,8 +25,9 @@ __host__ __device__ __forceinline__ int meta_owner(int64_t m) { return int(m & 0
 }  // namespace coconet
 
 struct coconet_tlist {
-  coconet_ctx* ctx = nullptr;
+  coconet_ctx* ctx = nullptr;  // null for a plan-only list (coconet_tlist_plan)
   int group = 0;
+  int world = 1;
   int n_tensors = 0;
   int64_t bucket_cap = 1024;
   std::vector<int64_t> counts;
@@ -40,6 +41,8 @@ struct coconet_tlist {
   int64_t shard_elems = 0;
   int64_t full_state_elems = 0;
   int64_t metadata_bytes = 0;
+  std::vector<coconet::Seg> table;             // TWO_SHOT tables, then the ONE_SHOT table
+  std::vector<int64_t> csr_ptr, csr_idx;
   std::vector<int64_t> host_flat, host_sidx;  // TWO_SHOT segments, flat order
   std::vector<int64_t> last_offs;
   void* dev_mem = nullptr;

@@ -8,7 +8,7 @@
 // the part of it inside one rank's flat chunk) and read/write the caller's
 // tensors in place, so there is no flatten copy.
 //
-// Segment tables built once on the host:
+// Segment tables built once on the host (plan_tlist, no device needed):
 //   TWO_SHOT : per rank r, the segments of flat chunk [total*r/W,
 //              total*(r+1)/W) (runtime.hpp:63-66); `sidx` indexes the rank's
 //              padded shard storage for sliced state (m, v).
@@ -26,42 +26,30 @@ using namespace coconet;
 namespace {
 
 struct HostSeg {
-  int64_t toff, sidx;
+  int64_t toff;
   int32_t tensor, len, owner;
   int64_t flat;
 };
 
-}  // namespace
-
-extern "C" {
-
-int coconet_tlist_create(coconet_ctx_t c, int group, int n_tensors, const int64_t* counts,
-                         int64_t bucket_cap, coconet_tlist_t* out) {
-  if (!c || !out || !counts) return set_error(COCONET_ERR_INVALID_INPUT, "null argument");
-  *out = nullptr;
-  if (!valid_group(c, group)) return set_error(COCONET_ERR_NO_SUCH_RANK, "no such group");
+int plan_tlist(coconet_tlist* tl, int W, int n_tensors, const int64_t* counts, int64_t bucket_cap) {
+  if (!counts) return set_error(COCONET_ERR_INVALID_INPUT, "null counts");
   if (n_tensors < 1) return set_error(COCONET_ERR_INVALID_INPUT, "empty tensor list");
+  if (W < 1 || W > kMaxRanks) return set_error(COCONET_ERR_NO_SUCH_RANK, "bad group size");
   if (bucket_cap < 4 || bucket_cap > (1 << 20) || (bucket_cap & 3))
     return set_error(COCONET_ERR_INVALID_INPUT, "bucket capacity must be a multiple of 4 in [4, 2^20]");
-  const int W = c->groups[size_t(group)].size;
-  auto* tl = new coconet_tlist();
-  tl->ctx = c;
-  tl->group = group;
+  tl->world = W;
   tl->n_tensors = n_tensors;
   tl->bucket_cap = bucket_cap;
   tl->counts.assign(counts, counts + n_tensors);
+  tl->total = 0;
   for (int i = 0; i < n_tensors; ++i) {
-    if (counts[i] <= 0) {
-      delete tl;
-      // build_bucket_table: "tensor has no elements" (runtime.hpp:596)
+    // build_bucket_table: "tensor has no elements" (runtime.hpp:596)
+    if (counts[i] <= 0)
       return set_error(COCONET_ERR_INVALID_INPUT, "tensor " + std::to_string(i) + " has no elements");
-    }
     tl->total += counts[i];
   }
-  if (tl->total < W) {
-    delete tl;
-    return set_error(COCONET_ERR_DIVISIBILITY, "fewer bucketed elements than ranks");
-  }
+  // scattered_collective: "fewer bucketed elements than ranks" (runtime.hpp:630)
+  if (tl->total < W) return set_error(COCONET_ERR_DIVISIBILITY, "fewer bucketed elements than ranks");
   // round-robin bucket order (runtime.hpp:604-613)
   std::vector<int64_t> cursor(static_cast<size_t>(n_tensors), 0);
   std::vector<HostSeg> buckets;
@@ -103,8 +91,11 @@ int coconet_tlist_create(coconet_ctx_t c, int group, int n_tensors, const int64_
     }
   }
   // TWO_SHOT tables: pieces grouped by owner (already ordered by flat position)
-  std::vector<Seg> table;
+  std::vector<Seg>& table = tl->table;
+  table.clear();
   table.reserve(pieces.size() * 2);
+  tl->host_flat.clear();
+  tl->host_sidx.clear();
   int64_t shard_max = 0;
   tl->seg_begin[0] = 0;
   size_t pi = 0;
@@ -113,11 +104,7 @@ int coconet_tlist_create(coconet_ctx_t c, int group, int n_tensors, const int64_
     while (pi < pieces.size() && pieces[pi].owner == r) {
       HostSeg& p = pieces[pi++];
       cur += ((p.toff & 3) - (cur & 3) + 4) & 3;
-      Seg s;
-      s.toff = p.toff;
-      s.sidx = cur;
-      s.meta = pack_meta(p.tensor, p.len, r);
-      table.push_back(s);
+      table.push_back(Seg{p.toff, cur, pack_meta(p.tensor, p.len, r)});
       tl->host_flat.push_back(p.flat);
       tl->host_sidx.push_back(cur);
       cur += p.len;
@@ -131,43 +118,42 @@ int coconet_tlist_create(coconet_ctx_t c, int group, int n_tensors, const int64_
   int64_t cur = 0;
   for (auto& p : pieces) {
     cur += ((p.toff & 3) - (cur & 3) + 4) & 3;
-    Seg s;
-    s.toff = p.toff;
-    s.sidx = cur;
-    s.meta = pack_meta(p.tensor, p.len, p.owner);
-    table.push_back(s);
+    table.push_back(Seg{p.toff, cur, pack_meta(p.tensor, p.len, p.owner)});
     cur += p.len;
   }
   tl->os_end = int64_t(table.size());
   tl->full_state_elems = (cur + 3) & ~int64_t(3);
   // per-tensor segment lists of each rank (TWO_SHOT), for deterministic
   // per-tensor reductions (LAMB): CSR over [seg_begin[r], seg_begin[r+1])
-  std::vector<int64_t> csr_ptr, csr_idx;
+  tl->csr_ptr.clear();
+  tl->csr_idx.clear();
   for (int r = 0; r < W; ++r) {
     std::vector<std::vector<int64_t>> per(static_cast<size_t>(n_tensors));
     for (int64_t s = tl->seg_begin[r]; s < tl->seg_begin[r + 1]; ++s)
       per[size_t(meta_tensor(table[size_t(s)].meta))].push_back(s);
-    tl->csr_begin[r] = int64_t(csr_ptr.size());
-    int64_t acc = int64_t(csr_idx.size());
+    tl->csr_begin[r] = int64_t(tl->csr_ptr.size());
+    int64_t acc = int64_t(tl->csr_idx.size());
     for (int t = 0; t < n_tensors; ++t) {
-      csr_ptr.push_back(acc);
-      for (auto s : per[size_t(t)]) csr_idx.push_back(s);
-      acc = int64_t(csr_idx.size());
+      tl->csr_ptr.push_back(acc);
+      for (auto s : per[size_t(t)]) tl->csr_idx.push_back(s);
+      acc = int64_t(tl->csr_idx.size());
     }
-    csr_ptr.push_back(acc);
+    tl->csr_ptr.push_back(acc);
   }
   tl->n_segs = int64_t(table.size());
+  tl->metadata_bytes = int64_t(table.size() * sizeof(Seg));
+  return COCONET_OK;
+}
+
+int upload_tlist(coconet_tlist* tl) {
+  const auto& table = tl->table;
   size_t bytes_segs = table.size() * sizeof(Seg);
-  size_t bytes_ptr = csr_ptr.size() * sizeof(int64_t);
-  size_t bytes_idx = std::max<size_t>(1, csr_idx.size()) * sizeof(int64_t);
-  size_t bytes_offs = size_t(n_tensors) * 2 * sizeof(int64_t);
+  size_t bytes_ptr = tl->csr_ptr.size() * sizeof(int64_t);
+  size_t bytes_idx = std::max<size_t>(1, tl->csr_idx.size()) * sizeof(int64_t);
+  size_t bytes_offs = size_t(tl->n_tensors) * 2 * sizeof(int64_t);
   size_t bytes_part = size_t(table.size()) * 2 * sizeof(double);
   size_t total = bytes_segs + bytes_ptr + bytes_idx + bytes_offs + bytes_part + 5 * 256;
-  cudaError_t e = cudaMalloc(&tl->dev_mem, total);
-  if (e != cudaSuccess) {
-    delete tl;
-    return cuda_fail(e, "tlist cudaMalloc");
-  }
+  CN_CUDA(cudaMalloc(&tl->dev_mem, total));
   char* p = static_cast<char*>(tl->dev_mem);
   auto carve = [&](size_t n) {
     char* q = p;
@@ -179,16 +165,47 @@ int coconet_tlist_create(coconet_ctx_t c, int group, int n_tensors, const int64_
   tl->d_csr_idx = reinterpret_cast<int64_t*>(carve(bytes_idx));
   tl->d_offs = reinterpret_cast<int64_t*>(carve(bytes_offs));
   tl->d_seg_part = reinterpret_cast<double*>(carve(bytes_part));
-  tl->metadata_bytes = int64_t(bytes_segs);
-  e = cudaMemcpy(tl->d_segs, table.data(), bytes_segs, cudaMemcpyHostToDevice);
-  if (e == cudaSuccess) e = cudaMemcpy(tl->d_csr_ptr, csr_ptr.data(), bytes_ptr, cudaMemcpyHostToDevice);
-  if (e == cudaSuccess && !csr_idx.empty())
-    e = cudaMemcpy(tl->d_csr_idx, csr_idx.data(), csr_idx.size() * sizeof(int64_t), cudaMemcpyHostToDevice);
-  if (e != cudaSuccess) {
+  CN_CUDA(cudaMemcpy(tl->d_segs, table.data(), bytes_segs, cudaMemcpyHostToDevice));
+  CN_CUDA(cudaMemcpy(tl->d_csr_ptr, tl->csr_ptr.data(), bytes_ptr, cudaMemcpyHostToDevice));
+  if (!tl->csr_idx.empty())
+    CN_CUDA(cudaMemcpy(tl->d_csr_idx, tl->csr_idx.data(), tl->csr_idx.size() * sizeof(int64_t),
+                       cudaMemcpyHostToDevice));
+  tl->last_offs.assign(size_t(tl->n_tensors) * 2, -1);
+  return COCONET_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int coconet_tlist_create(coconet_ctx_t c, int group, int n_tensors, const int64_t* counts,
+                         int64_t bucket_cap, coconet_tlist_t* out) {
+  if (!c || !out) return set_error(COCONET_ERR_INVALID_INPUT, "null argument");
+  *out = nullptr;
+  if (!valid_group(c, group)) return set_error(COCONET_ERR_NO_SUCH_RANK, "no such group");
+  auto* tl = new coconet_tlist();
+  tl->ctx = c;
+  tl->group = group;
+  int rc = plan_tlist(tl, c->groups[size_t(group)].size, n_tensors, counts, bucket_cap);
+  if (!rc) rc = upload_tlist(tl);
+  if (rc) {
     coconet_tlist_destroy(tl);
-    return cuda_fail(e, "tlist upload");
+    return rc;
   }
-  tl->last_offs.assign(size_t(n_tensors) * 2, -1);
+  *out = tl;
+  return COCONET_OK;
+}
+
+int coconet_tlist_plan(int world, int n_tensors, const int64_t* counts, int64_t bucket_cap,
+                       coconet_tlist_t* out) {
+  if (!out) return set_error(COCONET_ERR_INVALID_INPUT, "null argument");
+  *out = nullptr;
+  auto* tl = new coconet_tlist();
+  int rc = plan_tlist(tl, world, n_tensors, counts, bucket_cap);
+  if (rc) {
+    delete tl;
+    return rc;
+  }
   *out = tl;
   return COCONET_OK;
 }
@@ -211,8 +228,7 @@ int64_t coconet_tlist_metadata_bytes(coconet_tlist_t tl) { return tl ? tl->metad
 
 int coconet_tlist_chunk(coconet_tlist_t tl, int r, int64_t* lo, int64_t* hi) {
   if (!tl) return set_error(COCONET_ERR_INVALID_INPUT, "null tlist");
-  int W = tl->ctx->groups[size_t(tl->group)].size;
-  if (r < 0 || r >= W) return set_error(COCONET_ERR_NO_SUCH_RANK, "rank out of range");
+  if (r < 0 || r >= tl->world) return set_error(COCONET_ERR_NO_SUCH_RANK, "rank out of range");
   if (lo) *lo = tl->chunk_lo[r];
   if (hi) *hi = tl->chunk_lo[r + 1];
   return COCONET_OK;
@@ -220,10 +236,27 @@ int coconet_tlist_chunk(coconet_tlist_t tl, int r, int64_t* lo, int64_t* hi) {
 
 int64_t coconet_tlist_shard_index(coconet_tlist_t tl, int64_t pos) {
   if (!tl || pos < 0 || pos >= tl->total) return -1;
-  // segments are ordered by flat position across ranks
+  // TWO_SHOT segments are ordered by flat position across ranks
   auto it = std::upper_bound(tl->host_flat.begin(), tl->host_flat.end(), pos);
   size_t s = size_t(it - tl->host_flat.begin()) - 1;
   return tl->host_sidx[s] + (pos - tl->host_flat[s]);
+}
+
+int64_t coconet_tlist_segments(coconet_tlist_t tl, int r, int64_t* tensor, int64_t* toff,
+                               int64_t* len, int64_t* sidx, int64_t cap) {
+  if (!tl) return set_error(COCONET_ERR_INVALID_INPUT, "null tlist");
+  if (r < -1 || r >= tl->world) return set_error(COCONET_ERR_NO_SUCH_RANK, "rank out of range");
+  int64_t b = r < 0 ? tl->os_begin : tl->seg_begin[r];
+  int64_t e = r < 0 ? tl->os_end : tl->seg_begin[r + 1];
+  if (e - b > cap) return -(e - b);
+  for (int64_t i = 0; i < e - b; ++i) {
+    const Seg& s = tl->table[size_t(b + i)];
+    tensor[i] = meta_tensor(s.meta);
+    toff[i] = s.toff;
+    len[i] = meta_len(s.meta);
+    sidx[i] = s.sidx;
+  }
+  return e - b;
 }
 
 }  // extern "C"
@@ -236,6 +269,7 @@ namespace coconet {
 int tlist_bind(coconet_tlist* tl, const void* const* a, const void* const* b, int a_elem_bytes,
                int b_elem_bytes, cudaStream_t stream) {
   const coconet_ctx* c = tl->ctx;
+  if (!c || !tl->dev_mem) return set_error(COCONET_ERR_INVALID_INPUT, "tensor list has no device table (plan-only)");
   std::vector<int64_t> offs(size_t(tl->n_tensors) * 2);
   for (int i = 0; i < tl->n_tensors; ++i) {
     int64_t oa = 0, ob = 0;
@@ -261,25 +295,3 @@ int tlist_bind(coconet_tlist* tl, const void* const* a, const void* const* b, in
 }
 
 }  // namespace coconet
-
-extern "C" int64_t coconet_tlist_segments(coconet_tlist_t tl, int r, int64_t* tensor, int64_t* toff,
-                                          int64_t* len, int64_t* sidx, int64_t cap) {
-  if (!tl) return set_error(COCONET_ERR_INVALID_INPUT, "null tlist");
-  int W = tl->ctx->groups[size_t(tl->group)].size;
-  if (r < -1 || r >= W) return set_error(COCONET_ERR_NO_SUCH_RANK, "rank out of range");
-  int64_t b = r < 0 ? tl->os_begin : tl->seg_begin[r];
-  int64_t e = r < 0 ? tl->os_end : tl->seg_begin[r + 1];
-  if (e - b > cap) return -(e - b);
-  std::vector<Seg> h(size_t(e - b));
-  if (e > b) {
-    cudaError_t err = cudaMemcpy(h.data(), tl->d_segs + b, size_t(e - b) * sizeof(Seg), cudaMemcpyDeviceToHost);
-    if (err != cudaSuccess) return cuda_fail(err, "segments D2H");
-  }
-  for (size_t i = 0; i < h.size(); ++i) {
-    tensor[i] = meta_tensor(h[i].meta);
-    toff[i] = h[i].toff;
-    len[i] = meta_len(h[i].meta);
-    sidx[i] = h[i].sidx;
-  }
-  return e - b;
-}
