@@ -19,6 +19,12 @@
 // replicated state (the AR-Opt family). Cross-rank ordering: one flag barrier
 // at entry (peers' gradients are ready) and one at exit (peers finished
 // reading ours and writing into our parameters).
+//
+// Latency hiding (the kernels are HBM/NVLink streams): the group size is a
+// template parameter (register arrays sized exactly), segment descriptors are
+// prefetched two segments ahead (the descriptor -> tensor-offset -> data
+// chain would otherwise be exposed per segment), and each lane keeps UNROLL
+// quads' loads in flight before consuming any.
 #include <cooperative_groups.h>
 
 #include <algorithm>
@@ -33,7 +39,6 @@ namespace {
 
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
-constexpr int kUnroll = 2;
 
 struct OptArgs {
   RankSet rs;
@@ -62,28 +67,39 @@ struct LambK {
   int64_t csr_begin[kMaxRanks];
 };
 
+// Compile-time group size (WT > 0) or runtime W <= kMaxRanks (WT == 0).
+template <int WT> struct Ranks {
+  static constexpr int kMax = WT > 0 ? WT : kMaxRanks;
+  __device__ __forceinline__ static bool has(int j, int W) { return WT > 0 ? true : j < W; }
+};
+
+template <int WT>
 __device__ __forceinline__ int rot(int owner, int j, int W) {
+  const int w = WT > 0 ? WT : W;
   int q = owner + 1 + j;
-  q -= (q >= W) ? W : 0;
-  q -= (q >= W) ? W : 0;
+  q -= (q >= w) ? w : 0;
+  q -= (q >= w) ? w : 0;
   return q;
 }
 
 // Ring-order reduction of one quad over the group (runtime.hpp:302-305:
 // chunk c accumulates x[c+1], x[c+2], ..., x[c]). The loads are issued first
 // (W independent 8/16-byte requests), then folded in order.
-template <typename T, int RED>
-__device__ __forceinline__ void ring_reduce4(char* const* base, int64_t off, int owner, int W,
-                                             float acc[4]) {
-  float x[kMaxRanks][4];
+template <typename T, int RED, int WT>
+__device__ __forceinline__ void ring_load4(char* const* base, int64_t off, int owner, int W,
+                                           float x[][4]) {
 #pragma unroll
-  for (int j = 0; j < kMaxRanks; ++j)
-    if (j < W) load4(reinterpret_cast<const T*>(base[rot(owner, j, W)] + off), x[j]);
+  for (int j = 0; j < Ranks<WT>::kMax; ++j)
+    if (Ranks<WT>::has(j, W)) load4(reinterpret_cast<const T*>(base[rot<WT>(owner, j, W)] + off), x[j]);
+}
+
+template <int RED, int WT>
+__device__ __forceinline__ void ring_fold4(const float x[][4], int W, float acc[4]) {
 #pragma unroll
   for (int i = 0; i < 4; ++i) acc[i] = x[0][i];
 #pragma unroll
-  for (int j = 1; j < kMaxRanks; ++j)
-    if (j < W) {
+  for (int j = 1; j < Ranks<WT>::kMax; ++j)
+    if (Ranks<WT>::has(j, W)) {
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
         // reduce_apply(red, inbox, slot) (types.hpp:76-82): inbox = acc
@@ -109,6 +125,60 @@ __device__ __forceinline__ void st4m(T* p, const float v[4], int lo, int hi) {
     for (int i = 0; i < 4; ++i)
       if (i >= lo && i < hi) p[i] = from_f32<T>(v[i]);
   }
+}
+
+// Segment descriptor with its tensor's two heap offsets resolved.
+struct SegD {
+  int64_t toff, sidx, aoff, boff;
+  int len, owner, tensor;
+};
+
+// Iterates this warp's segments [s, se) with stride `st`, prefetching the
+// descriptor two segments ahead and the tensor offsets one ahead:
+//   for (SegIter it(...); it.valid(); it.next()) { SegD d = it.get(); ... }
+// (no lambdas: capturing kernel parameters by reference spills them).
+struct SegIter {
+  const Seg* segs;
+  const int64_t* offs;
+  int n;
+  int64_t s, se, st;
+  Seg d1, d2, d3;
+  int64_t a1, b1, a2, b2;
+
+  __device__ __forceinline__ SegIter(const Seg* segs_, const int64_t* offs_, int n_, int64_t s_, int64_t se_,
+                                     int64_t st_)
+      : segs(segs_), offs(offs_), n(n_), s(s_), se(se_), st(st_) {
+    if (s < se) {
+      d1 = segs[s];
+      d2 = s + st < se ? segs[s + st] : d1;
+      a1 = offs[meta_tensor(d1.meta)];
+      b1 = offs[n + meta_tensor(d1.meta)];
+      prefetch();
+    }
+  }
+  __device__ __forceinline__ void prefetch() {
+    d3 = s + 2 * st < se ? segs[s + 2 * st] : d2;
+    a2 = offs[meta_tensor(d2.meta)];
+    b2 = offs[n + meta_tensor(d2.meta)];
+  }
+  __device__ __forceinline__ bool valid() const { return s < se; }
+  __device__ __forceinline__ int64_t index() const { return s; }
+  __device__ __forceinline__ SegD get() const {
+    return SegD{d1.toff, d1.sidx, a1, b1, meta_len(d1.meta), meta_owner(d1.meta), meta_tensor(d1.meta)};
+  }
+  __device__ __forceinline__ void next() {
+    s += st;
+    d1 = d2;
+    d2 = d3;
+    a1 = a2;
+    b1 = b2;
+    if (s < se) prefetch();
+  }
+};
+
+__device__ __forceinline__ void quad_range(const SegD& d, int64_t e0, int& lo, int& hi) {
+  lo = int(max(int64_t(0), d.toff - e0));
+  hi = int(min(int64_t(4), d.toff + d.len - e0));
 }
 
 // Adam element (goldens/adam.json under adam_fused.json):
@@ -141,12 +211,12 @@ __device__ __forceinline__ void adam_elem(float g, float& m, float& v, float& p,
   }
 }
 
-template <typename G, int MATH, bool ONE_SHOT>
-__global__ void __launch_bounds__(kThreads) adam_kernel(OptArgs a, AdamK k) {
+template <typename G, int MATH, bool ONE_SHOT, int WT, int U>
+__global__ void __launch_bounds__(kThreads, 2) adam_kernel(OptArgs a, AdamK k) {
   __shared__ char* s_base[kMaxRanks];
   const RankSet& rs = a.rs;
   if (threadIdx.x < kMaxRanks) s_base[threadIdx.x] = threadIdx.x < rs.world ? rs.base[threadIdx.x] : nullptr;
-  const int W = rs.world;
+  const int W = WT > 0 ? WT : rs.world;
   const int me = rs.rank();
   if (!rank_barrier(rs, 0)) return;  // peers' gradients are complete
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -154,96 +224,99 @@ __global__ void __launch_bounds__(kThreads) adam_kernel(OptArgs a, AdamK k) {
   const int64_t se = ONE_SHOT ? a.os_end : a.seg_begin[me + 1];
   float* m = reinterpret_cast<float*>(s_base[me] + a.m_off);
   float* v = reinterpret_cast<float*>(s_base[me] + a.v_off);
-  for (int64_t s = sb + int64_t(blockIdx.x) * kWarps + warp; s < se;
-       s += int64_t(gridDim.x) * kWarps) {
-    const Seg sg = a.segs[s];
-    const int t = meta_tensor(sg.meta), len = meta_len(sg.meta), owner = meta_owner(sg.meta);
-    const int64_t goff = a.offs[t], poff = a.offs[a.n_tensors + t];
-    const int64_t q0 = sg.toff >> 2, q1 = (sg.toff + len + 3) >> 2;
-    for (int64_t qb = q0 + lane; qb < q1; qb += 32 * kUnroll) {
-      float g[kUnroll][4], mm[kUnroll][4], vv[kUnroll][4], pp[kUnroll][4];
+  const char* pme = s_base[me];
+  for (SegIter it(a.segs, a.offs, a.n_tensors, sb + int64_t(blockIdx.x) * kWarps + warp, se,
+                  int64_t(gridDim.x) * kWarps);
+       it.valid(); it.next()) {
+         const SegD d = it.get();
+         const int64_t q0 = d.toff >> 2, q1 = (d.toff + d.len + 3) >> 2;
+         for (int64_t qb = q0 + lane; qb < q1; qb += 32 * U) {
+           float g[U][Ranks<WT>::kMax][4], mm[U][4], vv[U][4], pp[U][4];
 #pragma unroll
-      for (int u = 0; u < kUnroll; ++u) {
-        const int64_t q = qb + 32 * u;
-        if (q < q1) {
-          const int64_t e0 = q << 2;
-          const int64_t si = sg.sidx + (e0 - sg.toff);
-          ring_reduce4<G, COCONET_SUM>(s_base, goff + e0 * int64_t(sizeof(G)), owner, W, g[u]);
-          ld4(m + si, mm[u]);
-          ld4(v + si, vv[u]);
-          ld4(reinterpret_cast<const float*>(s_base[me] + poff) + e0, pp[u]);
-        }
-      }
+           for (int u = 0; u < U; ++u) {
+             const int64_t q = qb + 32 * u;
+             if (q < q1) {
+               const int64_t e0 = q << 2;
+               const int64_t si = d.sidx + (e0 - d.toff);
+               ring_load4<G, COCONET_SUM, WT>(s_base, d.aoff + e0 * int64_t(sizeof(G)), d.owner, W, g[u]);
+               ld4(m + si, mm[u]);
+               ld4(v + si, vv[u]);
+               ld4(reinterpret_cast<const float*>(pme + d.boff) + e0, pp[u]);
+             }
+           }
 #pragma unroll
-      for (int u = 0; u < kUnroll; ++u) {
-        const int64_t q = qb + 32 * u;
-        if (q < q1) {
-          const int64_t e0 = q << 2;
-          const int lo = int(max(int64_t(0), sg.toff - e0));
-          const int hi = int(min(int64_t(4), sg.toff + len - e0));
-          const int64_t si = sg.sidx + (e0 - sg.toff);
+           for (int u = 0; u < U; ++u) {
+             const int64_t q = qb + 32 * u;
+             if (q < q1) {
+               const int64_t e0 = q << 2;
+               int lo, hi;
+               quad_range(d, e0, lo, hi);
+               const int64_t si = d.sidx + (e0 - d.toff);
+               float gs[4];
+               ring_fold4<COCONET_SUM, WT>(g[u], W, gs);
 #pragma unroll
-          for (int i = 0; i < 4; ++i) adam_elem<MATH>(g[u][i], mm[u][i], vv[u][i], pp[u][i], k);
-          st4m(m + si, mm[u], lo, hi);
-          st4m(v + si, vv[u], lo, hi);
-          if (ONE_SHOT) {
-            st4m(reinterpret_cast<float*>(s_base[me] + poff) + e0, pp[u], lo, hi);
-          } else {
+               for (int i = 0; i < 4; ++i) adam_elem<MATH>(gs[i], mm[u][i], vv[u][i], pp[u][i], k);
+               st4m(m + si, mm[u], lo, hi);
+               st4m(v + si, vv[u], lo, hi);
+               if (ONE_SHOT) {
+                 st4m(reinterpret_cast<float*>(s_base[me] + d.boff) + e0, pp[u], lo, hi);
+               } else {
 #pragma unroll
-            for (int j = 0; j < kMaxRanks; ++j)  // AG push, own copy included
-              if (j < W) st4m(reinterpret_cast<float*>(s_base[j] + poff) + e0, pp[u], lo, hi);
-          }
-        }
-      }
-    }
-  }
+                 for (int j = 0; j < Ranks<WT>::kMax; ++j)  // AG push, own copy included
+                   if (Ranks<WT>::has(j, W)) st4m(reinterpret_cast<float*>(s_base[j] + d.boff) + e0, pp[u], lo, hi);
+               }
+             }
+           }
+         }
+       }
   rank_barrier(rs, 1);  // peers done reading our g and writing our p
 }
 
 // Tensor-list AllReduce (x -> out). TWO_SHOT = pull-RS of the own chunk +
 // push-AG; ONE_SHOT = pull everything, write own copy (out != x).
-template <typename T, int RED, bool ONE_SHOT>
-__global__ void __launch_bounds__(kThreads) allreduce_kernel(OptArgs a) {
+template <typename T, int RED, bool ONE_SHOT, int WT, int U>
+__global__ void __launch_bounds__(kThreads, 2) allreduce_kernel(OptArgs a) {
   __shared__ char* s_base[kMaxRanks];
   const RankSet& rs = a.rs;
   if (threadIdx.x < kMaxRanks) s_base[threadIdx.x] = threadIdx.x < rs.world ? rs.base[threadIdx.x] : nullptr;
-  const int W = rs.world;
+  const int W = WT > 0 ? WT : rs.world;
   const int me = rs.rank();
   if (!rank_barrier(rs, 0)) return;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t sb = ONE_SHOT ? a.os_begin : a.seg_begin[me];
   const int64_t se = ONE_SHOT ? a.os_end : a.seg_begin[me + 1];
-  for (int64_t s = sb + int64_t(blockIdx.x) * kWarps + warp; s < se;
-       s += int64_t(gridDim.x) * kWarps) {
-    const Seg sg = a.segs[s];
-    const int t = meta_tensor(sg.meta), len = meta_len(sg.meta), owner = meta_owner(sg.meta);
-    const int64_t xoff = a.offs[t], ooff = a.offs[a.n_tensors + t];
-    const int64_t q0 = sg.toff >> 2, q1 = (sg.toff + len + 3) >> 2;
-    for (int64_t qb = q0 + lane; qb < q1; qb += 32 * kUnroll) {
-      float acc[kUnroll][4];
+  for (SegIter it(a.segs, a.offs, a.n_tensors, sb + int64_t(blockIdx.x) * kWarps + warp, se,
+                  int64_t(gridDim.x) * kWarps);
+       it.valid(); it.next()) {
+         const SegD d = it.get();
+         const int64_t q0 = d.toff >> 2, q1 = (d.toff + d.len + 3) >> 2;
+         for (int64_t qb = q0 + lane; qb < q1; qb += 32 * U) {
+           float x[U][Ranks<WT>::kMax][4];
 #pragma unroll
-      for (int u = 0; u < kUnroll; ++u) {
-        const int64_t q = qb + 32 * u;
-        if (q < q1) ring_reduce4<T, RED>(s_base, xoff + (q << 2) * int64_t(sizeof(T)), owner, W, acc[u]);
-      }
+           for (int u = 0; u < U; ++u) {
+             const int64_t q = qb + 32 * u;
+             if (q < q1) ring_load4<T, RED, WT>(s_base, d.aoff + (q << 2) * int64_t(sizeof(T)), d.owner, W, x[u]);
+           }
 #pragma unroll
-      for (int u = 0; u < kUnroll; ++u) {
-        const int64_t q = qb + 32 * u;
-        if (q < q1) {
-          const int64_t e0 = q << 2;
-          const int lo = int(max(int64_t(0), sg.toff - e0));
-          const int hi = int(min(int64_t(4), sg.toff + len - e0));
-          if (ONE_SHOT) {
-            st4m(reinterpret_cast<T*>(s_base[me] + ooff) + e0, acc[u], lo, hi);
-          } else {
+           for (int u = 0; u < U; ++u) {
+             const int64_t q = qb + 32 * u;
+             if (q < q1) {
+               const int64_t e0 = q << 2;
+               int lo, hi;
+               quad_range(d, e0, lo, hi);
+               float acc[4];
+               ring_fold4<RED, WT>(x[u], W, acc);
+               if (ONE_SHOT) {
+                 st4m(reinterpret_cast<T*>(s_base[me] + d.boff) + e0, acc, lo, hi);
+               } else {
 #pragma unroll
-            for (int j = 0; j < kMaxRanks; ++j)
-              if (j < W) st4m(reinterpret_cast<T*>(s_base[j] + ooff) + e0, acc[u], lo, hi);
-          }
-        }
-      }
-    }
-  }
+                 for (int j = 0; j < Ranks<WT>::kMax; ++j)
+                   if (Ranks<WT>::has(j, W)) st4m(reinterpret_cast<T*>(s_base[j] + d.boff) + e0, acc, lo, hi);
+               }
+             }
+           }
+         }
+       }
   rank_barrier(rs, 1);
 }
 
@@ -264,12 +337,12 @@ __device__ __forceinline__ float lamb_u(float m, float v, float p, const LambK& 
 //  deterministic) -> pushed into every peer's exchange area -> flag barrier
 //  -> totals combined in rank order (state.hpp:163-167)
 //  pass 2: trust ratio -> p update -> AG push.
-template <typename G>
-__global__ void __launch_bounds__(kThreads) lamb_kernel(OptArgs a, LambK k) {
+template <typename G, int WT, int U>
+__global__ void __launch_bounds__(kThreads, 2) lamb_kernel(OptArgs a, LambK k) {
   __shared__ char* s_base[kMaxRanks];
   const RankSet& rs = a.rs;
   if (threadIdx.x < kMaxRanks) s_base[threadIdx.x] = threadIdx.x < rs.world ? rs.base[threadIdx.x] : nullptr;
-  const int W = rs.world;
+  const int W = WT > 0 ? WT : rs.world;
   const int me = rs.rank();
   // No early return before the grid syncs: a CTA whose barrier timed out
   // skips its work but still arrives, so the grid cannot deadlock.
@@ -278,49 +351,54 @@ __global__ void __launch_bounds__(kThreads) lamb_kernel(OptArgs a, LambK k) {
   const int64_t sb = a.seg_begin[me], se = ok ? a.seg_begin[me + 1] : sb;
   float* m = reinterpret_cast<float*>(s_base[me] + a.m_off);
   float* v = reinterpret_cast<float*>(s_base[me] + a.v_off);
+  const char* pme = s_base[me];
   const int64_t wstride = int64_t(gridDim.x) * kWarps;
   const int64_t wid = int64_t(blockIdx.x) * kWarps + warp;
   // ---- pass 1
-  for (int64_t s = sb + wid; s < se; s += wstride) {
-    const Seg sg = a.segs[s];
-    const int t = meta_tensor(sg.meta), len = meta_len(sg.meta);
-    const int64_t goff = a.offs[t], poff = a.offs[a.n_tensors + t];
-    const int64_t q0 = sg.toff >> 2, q1 = (sg.toff + len + 3) >> 2;
+  for (SegIter it(a.segs, a.offs, a.n_tensors, sb + wid, se, wstride); it.valid(); it.next()) {
+    const SegD d = it.get();
+    const int64_t s = it.index();
+    const int64_t q0 = d.toff >> 2, q1 = (d.toff + d.len + 3) >> 2;
     double sp = 0.0, su = 0.0;
-    for (int64_t qb = q0 + lane; qb < q1; qb += 32 * kUnroll) {
-      float g[kUnroll][4], mm[kUnroll][4], vv[kUnroll][4], pp[kUnroll][4];
+    for (int64_t qb = q0 + lane; qb < q1; qb += 32 * U) {
+      float g[U][Ranks<WT>::kMax][4], mm[U][4], vv[U][4], pp[U][4];
 #pragma unroll
-      for (int u = 0; u < kUnroll; ++u) {
+      for (int u = 0; u < U; ++u) {
         const int64_t q = qb + 32 * u;
         if (q < q1) {
           const int64_t e0 = q << 2;
-          const int64_t si = sg.sidx + (e0 - sg.toff);
-          ring_reduce4<G, COCONET_SUM>(s_base, goff + e0 * int64_t(sizeof(G)), me, W, g[u]);
+          const int64_t si = d.sidx + (e0 - d.toff);
+          ring_load4<G, COCONET_SUM, WT>(s_base, d.aoff + e0 * int64_t(sizeof(G)), me, W, g[u]);
           ld4(m + si, mm[u]);
           ld4(v + si, vv[u]);
-          ld4(reinterpret_cast<const float*>(s_base[me] + poff) + e0, pp[u]);
+          ld4(reinterpret_cast<const float*>(pme + d.boff) + e0, pp[u]);
         }
       }
 #pragma unroll
-      for (int u = 0; u < kUnroll; ++u) {
+      for (int u = 0; u < U; ++u) {
         const int64_t q = qb + 32 * u;
         if (q < q1) {
           const int64_t e0 = q << 2;
-          const int lo = int(max(int64_t(0), sg.toff - e0));
-          const int hi = int(min(int64_t(4), sg.toff + len - e0));
-          const int64_t si = sg.sidx + (e0 - sg.toff);
+          int lo, hi;
+          quad_range(d, e0, lo, hi);
+          const int64_t si = d.sidx + (e0 - d.toff);
+          float gs[4];
+          ring_fold4<COCONET_SUM, WT>(g[u], W, gs);
+          float fp = 0.f, fu = 0.f;
 #pragma unroll
           for (int i = 0; i < 4; ++i) {
-            float mn = fmaf(k.fcm, g[u][i], mm[u][i] * k.fb1);
-            float vn = fmaf(k.fcv * g[u][i], g[u][i], vv[u][i] * k.fb2);
+            const float mn = fmaf(k.fcm, gs[i], mm[u][i] * k.fb1);
+            const float vn = fmaf(k.fcv * gs[i], gs[i], vv[u][i] * k.fb2);
             mm[u][i] = mn;
             vv[u][i] = vn;
             if (i >= lo && i < hi) {
-              float uu = lamb_u(mn, vn, pp[u][i], k);
-              sp += double(pp[u][i]) * double(pp[u][i]);
-              su += double(uu) * double(uu);
+              const float uu = lamb_u(mn, vn, pp[u][i], k);
+              fp = fmaf(pp[u][i], pp[u][i], fp);
+              fu = fmaf(uu, uu, fu);
             }
           }
+          sp += double(fp);
+          su += double(fu);
           st4m(m + si, mm[u], lo, hi);
           st4m(v + si, vv[u], lo, hi);
         }
@@ -359,43 +437,44 @@ __global__ void __launch_bounds__(kThreads) lamb_kernel(OptArgs a, LambK k) {
   cg::this_grid().sync();
   if (!rank_barrier(rs, 2)) return;
   // ---- pass 2
-  for (int64_t s = sb + wid; s < se; s += wstride) {
-    const Seg sg = a.segs[s];
-    const int t = meta_tensor(sg.meta), len = meta_len(sg.meta);
-    const int64_t poff = a.offs[a.n_tensors + t];
-    double P = 0.0, U = 0.0;
-    for (int q = 0; q < W; ++q) {  // rank order 0..W-1
-      P += __ldcg(xch_me + (int64_t(q) * a.n_tensors + t) * 2);
-      U += __ldcg(xch_me + (int64_t(q) * a.n_tensors + t) * 2 + 1);
-    }
-    const float ratio = float((k.lr * sqrt(P)) / sqrt(U));
-    const int64_t q0 = sg.toff >> 2, q1 = (sg.toff + len + 3) >> 2;
-    for (int64_t qb = q0 + lane; qb < q1; qb += 32 * kUnroll) {
-      float mm[kUnroll][4], vv[kUnroll][4], pp[kUnroll][4];
+  for (SegIter it(a.segs, a.offs, a.n_tensors, sb + wid, se, wstride); it.valid(); it.next()) {
+    const SegD d = it.get();
+    double P = 0.0, Uu = 0.0;
 #pragma unroll
-      for (int u = 0; u < kUnroll; ++u) {
+    for (int q = 0; q < Ranks<WT>::kMax; ++q)  // rank order 0..W-1
+      if (Ranks<WT>::has(q, W)) {
+        P += __ldcg(xch_me + (int64_t(q) * a.n_tensors + d.tensor) * 2);
+        Uu += __ldcg(xch_me + (int64_t(q) * a.n_tensors + d.tensor) * 2 + 1);
+      }
+    const float ratio = float((k.lr * sqrt(P)) / sqrt(Uu));
+    const int64_t poff = d.boff;
+    const int64_t q0 = d.toff >> 2, q1 = (d.toff + d.len + 3) >> 2;
+    for (int64_t qb = q0 + lane; qb < q1; qb += 32 * U) {
+      float mm[U][4], vv[U][4], pp[U][4];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
         const int64_t q = qb + 32 * u;
         if (q < q1) {
           const int64_t e0 = q << 2;
-          const int64_t si = sg.sidx + (e0 - sg.toff);
+          const int64_t si = d.sidx + (e0 - d.toff);
           ld4(m + si, mm[u]);
           ld4(v + si, vv[u]);
-          ld4(reinterpret_cast<const float*>(s_base[me] + poff) + e0, pp[u]);
+          ld4(reinterpret_cast<const float*>(pme + poff) + e0, pp[u]);
         }
       }
 #pragma unroll
-      for (int u = 0; u < kUnroll; ++u) {
+      for (int u = 0; u < U; ++u) {
         const int64_t q = qb + 32 * u;
         if (q < q1) {
           const int64_t e0 = q << 2;
-          const int lo = int(max(int64_t(0), sg.toff - e0));
-          const int hi = int(min(int64_t(4), sg.toff + len - e0));
+          int lo, hi;
+          quad_range(d, e0, lo, hi);
           float pn[4];
 #pragma unroll
           for (int i = 0; i < 4; ++i) pn[i] = pp[u][i] - ratio * lamb_u(mm[u][i], vv[u][i], pp[u][i], k);
 #pragma unroll
-          for (int j = 0; j < kMaxRanks; ++j)
-            if (j < W) st4m(reinterpret_cast<float*>(s_base[j] + poff) + e0, pn, lo, hi);
+          for (int j = 0; j < Ranks<WT>::kMax; ++j)
+            if (Ranks<WT>::has(j, W)) st4m(reinterpret_cast<float*>(s_base[j] + poff) + e0, pn, lo, hi);
         }
       }
     }
@@ -444,28 +523,60 @@ bool resolve_one_shot(int algo, const coconet_tlist* tl, int W) {
   return W > 1 && tl->total <= (int64_t(1) << 16);
 }
 
-template <typename G, int MATH, bool OS>
+// ---- instantiation tables: group size specialised for 1, 2, 4, 8 ranks,
+// generic (runtime W) otherwise; unroll depth by how many loads a quad needs.
+template <int WT> constexpr int unroll_for() { return WT == 1 ? 4 : (WT == 2 ? 2 : (WT == 4 ? 2 : 1)); }
+
+template <typename G, int MATH, bool OS, int WT>
 const void* adam_fn() {
-  return reinterpret_cast<const void*>(&adam_kernel<G, MATH, OS>);
+  constexpr int U = MATH == COCONET_MATH_EXACT ? (WT == 1 ? 2 : 1) : unroll_for<WT>();
+  return reinterpret_cast<const void*>(&adam_kernel<G, MATH, OS, WT, U>);
+}
+
+template <typename G, int MATH, bool OS>
+const void* adam_w(int W) {
+  switch (W) {
+    case 1: return adam_fn<G, MATH, OS, 1>();
+    case 2: return adam_fn<G, MATH, OS, 2>();
+    case 4: return adam_fn<G, MATH, OS, 4>();
+    case 8: return adam_fn<G, MATH, OS, 8>();
+    default: return adam_fn<G, MATH, OS, 0>();
+  }
 }
 
 template <typename G>
-const void* adam_pick(int math, bool os) {
-  if (math == COCONET_MATH_EXACT) return os ? adam_fn<G, COCONET_MATH_EXACT, true>() : adam_fn<G, COCONET_MATH_EXACT, false>();
-  return os ? adam_fn<G, COCONET_MATH_FAST, true>() : adam_fn<G, COCONET_MATH_FAST, false>();
+const void* adam_pick(int math, bool os, int W) {
+  if (math == COCONET_MATH_EXACT) return os ? adam_w<G, COCONET_MATH_EXACT, true>(W) : adam_w<G, COCONET_MATH_EXACT, false>(W);
+  return os ? adam_w<G, COCONET_MATH_FAST, true>(W) : adam_w<G, COCONET_MATH_FAST, false>(W);
 }
 
-template <typename T, int RED>
-const void* ar_pick(bool os) {
-  return os ? reinterpret_cast<const void*>(&allreduce_kernel<T, RED, true>)
-            : reinterpret_cast<const void*>(&allreduce_kernel<T, RED, false>);
+template <typename T, int RED, bool OS>
+const void* ar_w(int W) {
+  switch (W) {
+    case 1: return reinterpret_cast<const void*>(&allreduce_kernel<T, RED, OS, 1, 4>);
+    case 2: return reinterpret_cast<const void*>(&allreduce_kernel<T, RED, OS, 2, 4>);
+    case 4: return reinterpret_cast<const void*>(&allreduce_kernel<T, RED, OS, 4, 2>);
+    case 8: return reinterpret_cast<const void*>(&allreduce_kernel<T, RED, OS, 8, 1>);
+    default: return reinterpret_cast<const void*>(&allreduce_kernel<T, RED, OS, 0, 1>);
+  }
 }
 
 template <typename T>
-const void* ar_pick_red(int red, bool os) {
-  if (red == COCONET_MAX) return ar_pick<T, COCONET_MAX>(os);
-  if (red == COCONET_MIN) return ar_pick<T, COCONET_MIN>(os);
-  return ar_pick<T, COCONET_SUM>(os);
+const void* ar_pick(int red, bool os, int W) {
+  if (red == COCONET_MAX) return os ? ar_w<T, COCONET_MAX, true>(W) : ar_w<T, COCONET_MAX, false>(W);
+  if (red == COCONET_MIN) return os ? ar_w<T, COCONET_MIN, true>(W) : ar_w<T, COCONET_MIN, false>(W);
+  return os ? ar_w<T, COCONET_SUM, true>(W) : ar_w<T, COCONET_SUM, false>(W);
+}
+
+template <typename G>
+const void* lamb_pick(int W) {
+  switch (W) {
+    case 1: return reinterpret_cast<const void*>(&lamb_kernel<G, 1, 4>);
+    case 2: return reinterpret_cast<const void*>(&lamb_kernel<G, 2, 2>);
+    case 4: return reinterpret_cast<const void*>(&lamb_kernel<G, 4, 2>);
+    case 8: return reinterpret_cast<const void*>(&lamb_kernel<G, 8, 1>);
+    default: return reinterpret_cast<const void*>(&lamb_kernel<G, 0, 1>);
+  }
 }
 
 int check_state(coconet_ctx* c, const void* ptr, int64_t* off) {
@@ -517,9 +628,9 @@ int coconet_fused_rs_adam_ag(coconet_ctx_t c, coconet_tlist_t tl, const void* co
   if (rc) return rc;
   OptArgs a;
   fill_args(tl, &a, rs, m_off, v_off);
-  const void* fn = g_elem == COCONET_F32   ? adam_pick<float>(hp->math, os)
-                   : g_elem == COCONET_F16 ? adam_pick<__half>(hp->math, os)
-                                           : adam_pick<__nv_bfloat16>(hp->math, os);
+  const void* fn = g_elem == COCONET_F32   ? adam_pick<float>(hp->math, os, W)
+                   : g_elem == COCONET_F16 ? adam_pick<__half>(hp->math, os, W)
+                                           : adam_pick<__nv_bfloat16>(hp->math, os, W);
   void* args[] = {&a, &k};
   return launch_opt(c, tl, fn, args, os, stream);
 }
@@ -536,6 +647,7 @@ int coconet_fused_rs_lamb_ag(coconet_ctx_t c, coconet_tlist_t tl, const void* co
   if (size_t(kMaxRanks) * tl->n_tensors * 2 * sizeof(double) > kXchBytes / kMaxGroups)
     return set_error(COCONET_ERR_UNSUPPORTED, "too many tensors for the exchange area");
   cudaStream_t stream = static_cast<cudaStream_t>(stream_);
+  const int W = c->groups[size_t(tl->group)].size;
   int64_t m_off = 0, v_off = 0;
   int rc = check_state(c, m_shard, &m_off);
   if (!rc) rc = check_state(c, v_shard, &v_off);
@@ -560,9 +672,9 @@ int coconet_fused_rs_lamb_ag(coconet_ctx_t c, coconet_tlist_t tl, const void* co
   if (rc) return rc;
   OptArgs a;
   fill_args(tl, &a, rs, m_off, v_off);
-  const void* fn = g_elem == COCONET_F32   ? reinterpret_cast<const void*>(&lamb_kernel<float>)
-                   : g_elem == COCONET_F16 ? reinterpret_cast<const void*>(&lamb_kernel<__half>)
-                                           : reinterpret_cast<const void*>(&lamb_kernel<__nv_bfloat16>);
+  const void* fn = g_elem == COCONET_F32   ? lamb_pick<float>(W)
+                   : g_elem == COCONET_F16 ? lamb_pick<__half>(W)
+                                           : lamb_pick<__nv_bfloat16>(W);
   void* args[] = {&a, &k};
   return launch_opt(c, tl, fn, args, false, stream);
 }
@@ -585,9 +697,9 @@ int coconet_allreduce(coconet_ctx_t c, coconet_tlist_t tl, const void* const* x,
   if (rc) return rc;
   OptArgs a;
   fill_args(tl, &a, rs, 0, 0);
-  const void* fn = elem == COCONET_F32   ? ar_pick_red<float>(reducer, os)
-                   : elem == COCONET_F16 ? ar_pick_red<__half>(reducer, os)
-                                         : ar_pick_red<__nv_bfloat16>(reducer, os);
+  const void* fn = elem == COCONET_F32   ? ar_pick<float>(reducer, os, W)
+                   : elem == COCONET_F16 ? ar_pick<__half>(reducer, os, W)
+                                         : ar_pick<__nv_bfloat16>(reducer, os, W);
   void* args[] = {&a};
   return launch_opt(c, tl, fn, args, os, stream);
 }
