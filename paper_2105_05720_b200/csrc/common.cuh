@@ -18,9 +18,19 @@ constexpr int kFlagPhases = 8;     // distinct barrier slots per launch
 //   uint32 flags[kMaxGroups][kFlagPhases][kMaxRanks][kMaxBlocks]
 constexpr size_t kPadBytes =
     size_t(kMaxGroups) * kFlagPhases * kMaxRanks * kMaxBlocks * sizeof(uint32_t);
-// exchange area after the pad (LAMB per-tensor partials, scalar reductions)
+// per-group areas after the pad (kGroupAreaBytes each):
+//   [0, kTileFlagsOff)              LAMB per-tensor partials exchange
+//   [kTileFlagsOff, kCountersOff)   per-tile flags of the overlapped MatMul
+//   [kCountersOff, kGroupAreaBytes) arrival counters
 constexpr size_t kXchBytes = size_t(8) << 20;
+constexpr size_t kGroupAreaBytes = kXchBytes / kMaxGroups;
+constexpr size_t kTileFlagsOff = kGroupAreaBytes - (size_t(128) << 10);
+constexpr size_t kCountersOff = kGroupAreaBytes - (size_t(64) << 10);
 constexpr size_t kReservedBytes = kPadBytes + kXchBytes;
+
+__host__ __device__ constexpr size_t group_area(int group) {
+  return kPadBytes + size_t(group) * kGroupAreaBytes;
+}
 
 // Per-launch view of the ranks a kernel touches. Virtual mode: all ranks of
 // the group are on this device, blockIdx.y = group rank. Distributed: one

@@ -414,7 +414,7 @@ __global__ void __launch_bounds__(kThreads, 2) lamb_kernel(OptArgs a, LambK k) {
   __threadfence();
   cg::this_grid().sync();
   // ---- per-tensor partials of this rank -> every peer's exchange slot [me][t]
-  const int64_t xch_off = int64_t(kPadBytes) + int64_t(rs.group) * int64_t(kXchBytes / kMaxGroups);
+  const int64_t xch_off = int64_t(group_area(rs.group));
   double* xch_me = reinterpret_cast<double*>(s_base[me] + xch_off);
   for (int64_t t = ok ? wid : a.n_tensors; t < a.n_tensors; t += wstride) {
     const int64_t* ptr = k.csr_ptr + k.csr_begin[me];
@@ -644,7 +644,7 @@ int coconet_fused_rs_lamb_ag(coconet_ctx_t c, coconet_tlist_t tl, const void* co
     return set_error(COCONET_ERR_UNSUPPORTED,
                      "LAMB runs in FAST math only: its whole-tensor sums cannot reproduce the "
                      "reference's sequential double accumulation bit-for-bit");
-  if (size_t(kMaxRanks) * tl->n_tensors * 2 * sizeof(double) > kXchBytes / kMaxGroups)
+  if (size_t(kMaxRanks) * tl->n_tensors * 2 * sizeof(double) > kTileFlagsOff)
     return set_error(COCONET_ERR_UNSUPPORTED, "too many tensors for the exchange area");
   cudaStream_t stream = static_cast<cudaStream_t>(stream_);
   const int W = c->groups[size_t(tl->group)].size;
