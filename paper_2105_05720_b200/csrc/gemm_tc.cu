@@ -589,7 +589,7 @@ __global__ void __launch_bounds__(256) overlap_consumer_kernel(OvArgs a) {
 constexpr size_t kTileFlagBytes = kCountersOff - kTileFlagsOff;  // per group: up to 16384 tiles
 
 std::mutex g_mp_mu;
-uint32_t g_mp_arrivals[16][coconet::kMaxRanks] = {};
+
 cudaStream_t g_side[16] = {};
 cudaEvent_t g_ev[16][2] = {};
 
@@ -692,13 +692,9 @@ int coconet_mm_overlap_fused_ar(coconet_ctx_t c, int group, const void* a, const
   double th = std::ceil(hp->rate * 9007199254740992.0);
   o.thresh = th <= 0 ? 0 : uint64_t(th);
   o.math = hp->math;
-  {
-    // every owner adds one arrival per row tile to every rank's counter
-    std::lock_guard<std::mutex> lk(g_mp_mu);
-    uint32_t& cum = g_mp_arrivals[c->device & 15][group & 7];
-    cum += uint32_t(p.g.tiles_m) * uint32_t(W);
-    o.arrive_target = cum;
-  }
+  // every owner adds one arrival per row tile to every rank's counter
+  c->mp_arrivals[group] += uint32_t(p.g.tiles_m) * uint32_t(W);
+  o.arrive_target = c->mp_arrivals[group];
   for (int i = 0; i < p.g.ranks; ++i)
     p.g.flags[i] = reinterpret_cast<uint32_t*>(p.g.c[i] - o.part_off + o.flag_off);
   p.g.epoch = o.rs.epoch;
@@ -706,19 +702,23 @@ int coconet_mm_overlap_fused_ar(coconet_ctx_t c, int group, const void* a, const
   cudaEvent_t e0, e1;
   rc = side_stream(c->device, &side, &e0, &e1);
   if (rc) return rc;
-  // consumer first on the side stream (it waits on tile flags), GEMM on the
-  // caller's stream; at most one consumer CTA per SM so the persistent GEMM
-  // CTAs (1 per SM) always fit beside them.
+  // GEMM on the caller's stream, consumer on a side stream ordered after the
+  // caller's prior work; the caller's stream then waits for the consumer.
   CN_CUDA(cudaEventRecord(e0, s));
   CN_CUDA(cudaStreamWaitEvent(side, e0, 0));
   const int nl = local_ranks(c, group);
   int cblocks = std::max(1, std::min(p.g.tiles_m, c->sm_count / nl));
   auto cfn = in_elem == COCONET_BF16 ? overlap_consumer_kernel<__nv_bfloat16> : overlap_consumer_kernel<__half>;
+  // The GEMM is enqueued FIRST: it never waits on the consumer, so the pair is
+  // deadlock-free whatever the hardware does with the two streams (measured:
+  // a consumer enqueued first can hold the GEMM back until it times out). The
+  // consumer's CTAs (256 threads, no smem) fit beside the 1-per-SM GEMM CTAs
+  // and start polling tile flags while the GEMM is still running.
+  rc = launch_tc(c, &p, in_elem, in_elem, c->sm_count, s);
+  if (rc) return rc;
   cfn<<<dim3(unsigned(cblocks), unsigned(nl)), 256, 0, side>>>(o);
   CN_CUDA(cudaGetLastError());
   c->launches++;
-  rc = launch_tc(c, &p, in_elem, in_elem, c->sm_count, s);
-  if (rc) return rc;
   CN_CUDA(cudaEventRecord(e1, side));
   CN_CUDA(cudaStreamWaitEvent(s, e1, 0));
   return COCONET_OK;
