@@ -258,6 +258,72 @@ int coconet_mm_overlap_fused_ar(coconet_ctx_t ctx, int group, const void* a, con
                                 int in_elem, int64_t rows, int64_t cols, int64_t k_local,
                                 const coconet_bdr_params* hp, void* stream);
 
+/* ---- generic element-wise expressions (eval_pointwise, state.hpp:126-193) --
+ * Any ccopt ExprDag (expr.hpp:29-173) lowered to a node list in evaluation
+ * order (children before parents, only nodes reachable from the root without
+ * entering ReduceTensor children). Evaluated in IEEE double without
+ * contraction like eval_expr (expr.hpp:186-222); element-uniform subtrees
+ * (scalar-only, e.g. 1 - pow(beta1, t)) arrive pre-folded by the host as
+ * CONST, per rank. Used by GpuEngine for Pointwise nodes and for fused
+ * expressions no specialised kernel matches. */
+enum coconet_expr_op {
+  COCONET_OP_CONST = 0, COCONET_OP_INPUT = 1, COCONET_OP_ADD = 2, COCONET_OP_SUB = 3,
+  COCONET_OP_MUL = 4, COCONET_OP_DIV = 5, COCONET_OP_SQRT = 6, COCONET_OP_POW = 7,
+  COCONET_OP_DROPOUT = 8, COCONET_OP_REDUCED = 9, COCONET_OP_UPDATE = 10
+};
+
+#define COCONET_EXPR_MAX_NODES 160
+#define COCONET_EXPR_MAX_OPERANDS 12
+#define COCONET_EXPR_MAX_DIMS 6
+
+typedef struct {
+  int32_t op;       /* coconet_expr_op */
+  int32_t a, b;     /* operand node positions in this list */
+  int32_t slot;     /* INPUT: operand slot; UPDATE: target slot; REDUCED: reduce index;
+                       CONST: per-rank constant index (-1 = use `value`) */
+  double value;     /* CONST */
+  double rate;      /* DROPOUT */
+  uint64_t key;     /* DROPOUT */
+} coconet_expr_node;
+
+/* A tensor as the element loop sees it: its heap offset, its GLOBAL shape
+ * right-aligned to the output rank (BroadcastView, view.hpp:75-98), and its
+ * storage layout (sliced_dim >= 0: only the rank's slice is stored,
+ * DistView::to_local view.hpp:49-60). */
+typedef struct {
+  int64_t off;
+  int32_t elem;                          /* coconet_elem */
+  int32_t ndim;
+  int64_t shape[COCONET_EXPR_MAX_DIMS];  /* global shape, ndim entries */
+  int32_t sliced_dim;                    /* in this operand's own dims, -1 if not sliced */
+  int32_t pad_;
+} coconet_operand;
+
+typedef struct {
+  int32_t n_nodes, n_inputs, n_targets, n_reduce;
+  int32_t root;
+  int32_t out_sliced_dim;      /* iteration space: the output's layout */
+  int32_t out_ndim;
+  int32_t n_rank_consts;       /* per-rank constants (folded uniform subtrees) */
+  int64_t out_shape[COCONET_EXPR_MAX_DIMS];
+  uint64_t seed;
+  coconet_operand out;
+  coconet_operand inputs[COCONET_EXPR_MAX_OPERANDS];
+  coconet_operand targets[4];
+  coconet_expr_node nodes[COCONET_EXPR_MAX_NODES];
+} coconet_expr_program;
+
+/* Per-element pass: out[r] and Update targets for every local rank.
+ * rank_consts[r * n_rank_consts + i], reduced[r * n_reduce + j] (may be NULL). */
+int coconet_pointwise(coconet_ctx_t ctx, int group, const coconet_expr_program* prog,
+                      const double* rank_consts, const double* reduced, void* stream);
+/* ReduceTensor pre-pass: for reduce node `node` (sum/max/min = red) evaluates
+ * its subtree (no Update stores) over each rank's local iteration space and
+ * writes one partial per local rank into host memory partial[r] (synchronous).
+ * Deterministic (fixed-order two-level reduction). */
+int coconet_pointwise_reduce(coconet_ctx_t ctx, int group, const coconet_expr_program* prog, int node,
+                             int red, const double* rank_consts, double* partial, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -30,7 +30,7 @@ CUDA_LIB = PKG / "libcoconet_cuda.so"
 ENGINE_LIB = PKG / "libcoconet_engine.so"
 
 CU_SOURCES = ["context.cu", "tlist.cu", "fused_opt.cu", "gen.cu", "collectives.cu",
-              "fused_bdr.cu", "gemm_tc.cu"]
+              "fused_bdr.cu", "gemm_tc.cu", "pointwise.cu"]
 
 
 def _run(cmd, cwd=None):
@@ -92,7 +92,8 @@ def build_engine(force: bool = False) -> Path | None:
     cmd = ["g++", "-std=c++20", "-O2", "-fPIC", "-shared", "-pthread", "-I", str(INCLUDE),
            "-I", str(CCOPT_REF_DIR / "include"), "-I", str(NLOHMANN_DIR), "-I",
            str(CUDA_HOME / "include"), "-o", str(ENGINE_LIB)] + [str(s) for s in srcs] + [
-        "-L", str(PKG), "-Wl,-rpath,$ORIGIN", "-lcoconet_cuda"]
+        "-L", str(PKG), "-Wl,-rpath,$ORIGIN", "-lcoconet_cuda",
+        "-L", str(CUDA_HOME / "lib64"), "-Wl,-rpath," + str(CUDA_HOME / "lib64"), "-lcudart"]
     _run(cmd)
     return ENGINE_LIB
 

@@ -185,6 +185,7 @@ int coconet_finalize(coconet_ctx_t c) {
       cudaFree(c->heap[r]);
   }
   if (c->status_host) cudaFreeHost(c->status_host);
+  if (c->small_dev) cudaFree(c->small_dev);
   delete c;
   return COCONET_OK;
 }

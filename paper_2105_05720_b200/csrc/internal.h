@@ -31,6 +31,8 @@ struct coconet_ctx {
   int* status_dev = nullptr;
   uint64_t timeout_ns = 20ull * 1000 * 1000 * 1000;
   uint64_t launches = 0;
+  void* small_dev = nullptr;  // scratch for per-call constants (pointwise)
+  size_t small_bytes = 0;
   // cumulative arrivals expected on this rank's per-group counter (overlapped
   // MatMul + fused AllReduce); the device counters start at 0 with the heap
   uint32_t mp_arrivals[coconet::kMaxGroups] = {};
