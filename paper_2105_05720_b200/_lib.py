@@ -103,6 +103,10 @@ _SIGNATURES = {
     "coconet_matmul": (_I, [_P, _I, _P, _P, _P, _I, _I, _I64, _I64, _I64, _I, _P]),
     "coconet_mm_overlap_fused_ar": (_I, [_P, _I, _P, _P, _P, _P, _P, _P, _I, _I64, _I64, _I64,
                                          C.POINTER(BdrParams), _P]),
+    # generic expression programs (driven by GpuEngine; opaque here)
+    "coconet_pointwise": (_I, [_P, _I, _P, C.POINTER(C.c_double), C.POINTER(C.c_double), _P]),
+    "coconet_pointwise_reduce": (_I, [_P, _I, _P, _I, _I, C.POINTER(C.c_double),
+                                      C.POINTER(C.c_double), _P]),
 }
 
 _lib = None
