@@ -234,8 +234,9 @@ __global__ void __launch_bounds__(kThreads, 2) adam_kernel(OptArgs a, AdamK k) {
            float g[U][Ranks<WT>::kMax][4], mm[U][4], vv[U][4], pp[U][4];
 #pragma unroll
            for (int u = 0; u < U; ++u) {
-             const int64_t q = qb + 32 * u;
-             if (q < q1) {
+             // clamped, unconditional loads: the compiler can batch all U of them
+             const int64_t q = min(qb + 32 * u, q1 - 1);
+             {
                const int64_t e0 = q << 2;
                const int64_t si = d.sidx + (e0 - d.toff);
                ring_load4<G, COCONET_SUM, WT>(s_base, d.aoff + e0 * int64_t(sizeof(G)), d.owner, W, g[u]);
@@ -294,8 +295,8 @@ __global__ void __launch_bounds__(kThreads, 2) allreduce_kernel(OptArgs a) {
            float x[U][Ranks<WT>::kMax][4];
 #pragma unroll
            for (int u = 0; u < U; ++u) {
-             const int64_t q = qb + 32 * u;
-             if (q < q1) ring_load4<T, RED, WT>(s_base, d.aoff + (q << 2) * int64_t(sizeof(T)), d.owner, W, x[u]);
+             const int64_t q = min(qb + 32 * u, q1 - 1);  // clamped, unconditional loads
+             ring_load4<T, RED, WT>(s_base, d.aoff + (q << 2) * int64_t(sizeof(T)), d.owner, W, x[u]);
            }
 #pragma unroll
            for (int u = 0; u < U; ++u) {
@@ -364,8 +365,8 @@ __global__ void __launch_bounds__(kThreads, 2) lamb_kernel(OptArgs a, LambK k) {
       float g[U][Ranks<WT>::kMax][4], mm[U][4], vv[U][4], pp[U][4];
 #pragma unroll
       for (int u = 0; u < U; ++u) {
-        const int64_t q = qb + 32 * u;
-        if (q < q1) {
+        const int64_t q = min(qb + 32 * u, q1 - 1);  // clamped, unconditional loads
+        {
           const int64_t e0 = q << 2;
           const int64_t si = d.sidx + (e0 - d.toff);
           ring_load4<G, COCONET_SUM, WT>(s_base, d.aoff + e0 * int64_t(sizeof(G)), me, W, g[u]);
@@ -453,8 +454,8 @@ __global__ void __launch_bounds__(kThreads, 2) lamb_kernel(OptArgs a, LambK k) {
       float mm[U][4], vv[U][4], pp[U][4];
 #pragma unroll
       for (int u = 0; u < U; ++u) {
-        const int64_t q = qb + 32 * u;
-        if (q < q1) {
+        const int64_t q = min(qb + 32 * u, q1 - 1);  // clamped, unconditional loads
+        {
           const int64_t e0 = q << 2;
           const int64_t si = d.sidx + (e0 - d.toff);
           ld4(m + si, mm[u]);

@@ -30,6 +30,31 @@ def elem_of(dtype: torch.dtype) -> int:
         raise _lib.CoconetError(3, f"unsupported dtype {dtype}") from None
 
 
+def exchange_blobs(mine: bytes, world: int, pg=None) -> bytes:
+    """All-gathers one fixed-size blob per rank (heap handles) over any
+    torch.distributed backend and returns them concatenated in rank order —
+    the layout coconet_open_peers expects."""
+    import torch.distributed as dist
+
+    allb = [None] * world
+    dist.all_gather_object(allb, mine, group=pg)
+    if any(b is None or len(b) != len(mine) for b in allb):
+        raise _lib.CoconetError(3, "heap handles of different sizes across ranks")
+    return b"".join(allb)
+
+
+def max_over_ranks(value: float, pg=None) -> float:
+    """Timing reduction used by bench.py: the job's time is the slowest rank's."""
+    import torch.distributed as dist
+
+    if not dist.is_initialized() or dist.get_world_size(pg) == 1:
+        return float(value)
+    dev = "cuda" if dist.get_backend(pg) == "nccl" else "cpu"
+    t = torch.tensor([float(value)], device=dev, dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX, group=pg)
+    return float(t.item())
+
+
 class _CAI:
     """Minimal __cuda_array_interface__ exporter for a raw device range."""
 
@@ -88,10 +113,7 @@ class Context:
         check(self.lib.coconet_heap_handle(self.handle, None, C.byref(n)))
         buf = (C.c_char * n.value)()
         check(self.lib.coconet_heap_handle(self.handle, buf, C.byref(n)))
-        mine = bytes(buf)
-        allh = [None] * self.world
-        dist.all_gather_object(allh, mine, group=pg)
-        blob = b"".join(allh)
+        blob = exchange_blobs(bytes(buf), self.world, pg)
         check(self.lib.coconet_open_peers(self.handle, C.c_char_p(blob), n.value))
         dist.barrier(group=pg)
 

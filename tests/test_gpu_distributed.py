@@ -1,0 +1,113 @@
+"""GPU, DISTRIBUTED mode with real processes: W processes share one B200, each
+maps the others' heaps through CUDA IPC (coconet_heap_handle /
+coconet_open_peers) — the same code path as one process per GPU over NVLink,
+and the cross-process flag protocol (st.release.sys / ld.acquire.sys) runs
+between contexts that the driver time-slices. Results must equal the
+restated reference bit for bit (EXACT)."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+pytestmark = pytest.mark.gpu
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _inputs(W, counts):
+    rng = np.random.default_rng(11)
+    g = [rng.uniform(-1, 1, (W, n)).astype(np.float32) for n in counts]
+    p = [rng.uniform(0.1, 0.9, n).astype(np.float32) for n in counts]
+    m = [rng.uniform(-0.1, 0.1, n).astype(np.float32) for n in counts]
+    v = [rng.uniform(0.01, 0.2, n).astype(np.float32) for n in counts]
+    return g, p, m, v
+
+
+def _worker(rank, world, port, counts, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from oracle import coconet_oracle as co
+        from paper_2105_05720_b200 import _lib
+        from paper_2105_05720_b200.collectives import AdamHParams, TensorList, allreduce, fused_rs_adam_ag
+        from paper_2105_05720_b200.runtime import Context
+
+        torch.cuda.set_device(0)
+        ctx = Context(world, mode="distributed", rank=rank, device=0, heap_bytes=64 << 20, timeout_ms=60000)
+        tl = TensorList(ctx, counts)
+        g, p, m, v = _inputs(world, counts)
+        gb = [ctx.alloc([n]) for n in counts]
+        pb = [ctx.alloc([n]) for n in counts]
+        mb, vb = ctx.alloc([tl.shard_elems]), ctx.alloc([tl.shard_elems])
+        tens, elem, sidx = tl.state_index_map(rank)
+        ms = np.zeros(tl.shard_elems, np.float32)
+        vs = np.zeros(tl.shard_elems, np.float32)
+        for t in range(len(counts)):
+            ctx.view(gb[t]).copy_(torch.from_numpy(g[t][rank]))
+            ctx.view(pb[t]).copy_(torch.from_numpy(p[t]))
+            sel = tens == t
+            ms[sidx[sel]] = m[t][elem[sel]]
+            vs[sidx[sel]] = v[t][elem[sel]]
+        ctx.view(mb).copy_(torch.from_numpy(ms))
+        ctx.view(vb).copy_(torch.from_numpy(vs))
+        torch.cuda.synchronize()
+        dist.barrier()
+        hp = AdamHParams(0.01, 0.9, 0.999, 3.0, 0.0, True, _lib.MATH_EXACT, _lib.ALGO_TWO_SHOT)
+        for _ in range(2):  # twice: epochs advance consistently across processes
+            fused_rs_adam_ag(ctx, tl, gb, pb, mb, vb, hp)
+            ctx.check()
+        # AllReduce of the (original) gradients, out of place
+        ob = [ctx.alloc([n]) for n in counts]
+        for t in range(len(counts)):
+            ctx.view(gb[t]).copy_(torch.from_numpy(g[t][rank]))
+        torch.cuda.synchronize()
+        dist.barrier()
+        allreduce(ctx, tl, gb, ob)
+        ctx.check()
+        got_p = [ctx.view(b).cpu().numpy() for b in pb]
+        got_ar = [ctx.view(b).cpu().numpy() for b in ob]
+        # expected: two reference fused Adam steps on the same per-rank grads
+        k = co.adam_consts(0.01, 0.9, 0.999, 3.0)
+        m1, v1, p1 = co.fused_adam(g, m, v, p, k)
+        _, _, p2 = co.fused_adam(g, m1, v1, p1, k)
+        table = co.bucket_table(counts)
+        flat = co.flatten_bucket_order(g, table)
+        bounds = co.flat_chunks(flat.shape[1], world)
+        owner = np.searchsorted(np.asarray(bounds[1:]), np.arange(flat.shape[1]), side="right")
+        ar = co.unflatten_bucket_order(co.ring_reduce(flat, owner), counts, table)
+        ok_p = all(np.array_equal(got_p[t], p2[t]) for t in range(len(counts)))
+        ok_ar = all(np.array_equal(got_ar[t], ar[t]) for t in range(len(counts)))
+        dist.barrier()
+        ctx.close()
+        q.put((rank, ok_p, ok_ar, None))
+    except Exception as e:  # report, don't hang the parent
+        q.put((rank, False, False, repr(e)))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_distributed_processes_share_one_gpu(world):
+    counts = [3000, 1024, 77, 5000]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, counts, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=300) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=120)
+    for rank, ok_p, ok_ar, err in res:
+        assert err is None, err
+        assert ok_p, f"rank {rank}: fused Adam differs from the reference"
+        assert ok_ar, f"rank {rank}: allreduce differs from the reference"

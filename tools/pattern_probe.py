@@ -1,0 +1,124 @@
+"""Per-pattern timing on ONE GPU with virtual ranks (all W ranks' data in this
+device's HBM; "NVLink" traffic becomes local HBM traffic, so these are kernel
+and protocol costs, not link-bound numbers). Configs from BASELINE.json:
+  C1  Adam 2^20 fp32, W=4          (fused RS-Adam-AG, exact and fast)
+  C3  MP [8192x384]x[384x3072] bf16, W=8 (tcgen05 GEMM, fused RS-BDR-AG, overlap)
+  C4  PP N=25,165,824, 2 stages x 4 (RS -> fused send -> AG)
+Usage: python tools/pattern_probe.py [--only c1,c3,c4] [--gemm-only]"""
+import argparse
+import json
+import sys
+from pathlib import Path
+
+import torch
+
+sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
+
+from paper_2105_05720_b200 import _lib  # noqa: E402
+from paper_2105_05720_b200.collectives import (AdamHParams, BdrHParams, TensorList, fused_rs_adam_ag,  # noqa: E402
+                                               fused_rs_bdr_ag, gen_values, matmul, mm_overlap_fused_ar,
+                                               rs_fused_send_ag)
+from paper_2105_05720_b200.runtime import Context  # noqa: E402
+
+
+def timeit(fn, steps=20, warmup=3):
+    for _ in range(warmup):
+        fn()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(steps):
+        fn()
+    e1.record()
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / steps
+
+
+def c1(out):
+    W, N = 4, 1 << 20
+    ctx = Context(W, heap_bytes=64 << 20)
+    tl = TensorList(ctx, [N])
+    g, p = ctx.alloc([N]), ctx.alloc([N])
+    m, v = ctx.alloc([tl.shard_elems]), ctx.alloc([tl.shard_elems])
+    for r in range(W):
+        gen_values(ctx, ctx.view(g, r), 1, "g", "local", r, [N], group_size=W)
+        gen_values(ctx, ctx.view(p, r), 1, "p", "replicated", r, [N], group_size=W)
+        ctx.view(m, r).zero_()
+        ctx.view(v, r).fill_(1e-3)
+    for math, name in ((_lib.MATH_EXACT, "exact"), (_lib.MATH_FAST, "fast")):
+        for algo, an in ((_lib.ALGO_TWO_SHOT, "two_shot"),):
+            hp = AdamHParams(1e-3, 0.9, 0.999, 1.0, 0.0, True, math, algo)
+            ms = timeit(lambda: fused_rs_adam_ag(ctx, tl, [g], [p], m, v, hp), 50)
+            out[f"c1_adam_W4_N2^20_{name}_{an}_us"] = ms * 1e3
+    ctx.close()
+
+
+def c3(out, gemm_only=False):
+    W, rows, H = 8, 8192, 3072
+    k = H // W
+    dt = torch.bfloat16
+    ctx = Context(W, heap_bytes=(3 << 30))
+    x, w = ctx.alloc([rows, k], dt), ctx.alloc([k, H], dt)
+    part, bb, rr, o1 = ctx.alloc([rows, H], dt), ctx.alloc([H], dt), ctx.alloc([rows, H], dt), ctx.alloc([rows, H], dt)
+    for r in range(W):
+        ctx.view(x, r).normal_()
+        ctx.view(w, r).normal_(0, k ** -0.5)
+        ctx.view(bb, r).normal_(0, 0.1)
+        ctx.view(rr, r).normal_()
+    hp = BdrHParams(0.1, 1, 11617925594314093840, _lib.MATH_FAST)
+    gemm = timeit(lambda: matmul(ctx, x, w, part, math=_lib.MATH_FAST))
+    flops = 2.0 * rows * H * k * W
+    out["c3_gemm_8ranks_us"] = gemm * 1e3
+    out["c3_gemm_tflops"] = flops / (gemm * 1e-3) / 1e12
+    if gemm_only:
+        return
+    ar = timeit(lambda: fused_rs_bdr_ag(ctx, part, bb, rr, o1, hp))
+    ov = timeit(lambda: mm_overlap_fused_ar(ctx, x, w, bb, rr, part, o1, hp))
+    out["c3_fused_rs_bdr_ag_8ranks_us"] = ar * 1e3
+    out["c3_sequential_us"] = (gemm + ar) * 1e3
+    out["c3_overlap_us"] = ov * 1e3
+    # bytes the RS->epilogue->AG moves through HBM here (all 8 ranks): each rank
+    # reads its column block from 8 partials, b and r, and writes the block to 8 outs
+    blk = rows * (H // W) * 2
+    out["c3_fused_ar_GBs"] = W * (8 * blk + blk + 8 * blk) / (ar * 1e-3) / 1e9
+    ctx.close()
+
+
+def c4(out):
+    W, N = 8, 25_165_824
+    S = W // 2
+    ctx = Context(W, heap_bytes=(1 << 30))
+    g0, g1 = ctx.group(0, S), ctx.group(S, S)
+    x, bb, rr, o = (ctx.alloc([N]) for _ in range(4))
+    for r in range(S):
+        gen_values(ctx, ctx.view(x, r), 1, "in", "local", r, [N], group_size=S)
+        gen_values(ctx, ctx.view(bb, r), 1, "b", "replicated", r, [N], group_size=S)
+        gen_values(ctx, ctx.view(rr, r), 1, "r", "replicated", r, [N], group_size=S)
+    for math, name in ((_lib.MATH_EXACT, "exact"), (_lib.MATH_FAST, "fast")):
+        hp = BdrHParams(0.1, 1, 3251584743947114031, math)
+        ms = timeit(lambda: rs_fused_send_ag(ctx, g0, g1, x, bb, rr, o, hp))
+        out[f"c4_pp_2x4_N25M_fp32_{name}_us"] = ms * 1e3
+        # HBM bytes on this device: each sender reads its chunk from 4 ranks + b + r,
+        # writes it to 4 receivers: (4 + 2 + 4) * N/4 * 4B per sender, 4 senders
+        out[f"c4_pp_{name}_GBs"] = 10 * N * 4 / (ms * 1e-3) / 1e9
+    ctx.close()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--only", default="c1,c3,c4")
+    ap.add_argument("--gemm-only", action="store_true")
+    a = ap.parse_args()
+    out = {}
+    sel = a.only.split(",")
+    if "c1" in sel:
+        c1(out)
+    if "c3" in sel:
+        c3(out, a.gemm_only)
+    if "c4" in sel:
+        c4(out)
+    print(json.dumps(out, indent=1))
+
+
+if __name__ == "__main__":
+    main()
