@@ -19,10 +19,13 @@
 //  * EXACT (fp32 inputs): fp64 accumulation in k order on the FP64 pipe,
 //    bit-identical to eval_matmul (each fp32*fp32 product is exact in double,
 //    so FMA == multiply-then-add).
-//  * Overlap: the RS -> bias+dropout+residual -> AG kernel runs concurrently
-//    on a second stream, one work unit per (128-row tile, column block); a unit
-//    starts as soon as every rank has published the tiles it covers, so the
-//    all-reduce of row tile i overlaps the GEMM of row tiles > i.
+//  * Overlap (one cooperative kernel, 16 warps per CTA): warps 2, 3 and 8-15
+//    start on the all-reduce at once, warps 0/1/4-7 join when their GEMM roles
+//    finish. A unit (row tile, owner rank, 32 rows) is taken from an atomic
+//    ticket in row-tile order and starts as soon as every rank has published
+//    the tiles it covers, so the RS -> bias+dropout+residual -> AG of row tile
+//    i overlaps the MMAs of later row tiles. GEMM warps never wait on comm
+//    warps, so the kernel cannot deadlock.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -37,21 +40,27 @@ using namespace coconet;
 
 namespace {
 
-constexpr int BM = 128, BK = 64, STAGES = 4;
+constexpr int BM = 128, BK = 64;
 constexpr int kGemmThreads = 256;
 constexpr int kAccStride = 256;   // TMEM columns per accumulator buffer
 constexpr int kTmemCols = 512;
+constexpr int kFusedThreads = 512;  // overlap kernel: 16 warps (0/1/4-7 GEMM roles, the rest all-reduce)
+constexpr int kFusedWarps = kFusedThreads / 32;
+constexpr int kUnitU = 2;           // quads per lane in flight in an all-reduce unit
 
 template <int BN> struct Cfg {
+  static constexpr int STAGES = BN == 256 ? 3 : 4;
   static constexpr int A_BYTES = BM * BK * 2;
   static constexpr int B_BYTES = BN * BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 256;
+  static constexpr int EPI_BYTES = 4 * 2 * 4096;  // 4 epilogue warps x 2 staging buffers of 32 rows x 128 B
+  static constexpr int SMEM = STAGES * STAGE_BYTES + EPI_BYTES + 1024 + 256;
 };
 
 struct RankMaps {
   CUtensorMap a[kMaxRanks];
   CUtensorMap b[kMaxRanks];
+  CUtensorMap c[kMaxRanks];  // output, stored by TMA from swizzled staging tiles
 };
 
 struct GemmArgs {
@@ -105,6 +114,13 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, i
           smem_u32(dst)),
       "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
       : "memory");
+}
+
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void* src, int c0, int c1) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(c0), "r"(c1), "r"(smem_u32(src))
+               : "memory");
 }
 
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
@@ -183,19 +199,144 @@ __device__ __forceinline__ void decode_tile(const GemmArgs& g, int t, int& r, in
   r = j - nt * g.ranks;
 }
 
-template <int BN, typename TO>
-__global__ void __launch_bounds__(kGemmThreads, 1) gemm_tc_kernel(const __grid_constant__ RankMaps maps, GemmArgs g,
-                                                                  uint32_t in_fmt) {
+// ---- fused all-reduce epilogue of the overlapped MatMul (mp_overlap.json) ----
+// Work unit = (row tile mt, owner rank, 32-row group): one warp pulls that
+// block of column block `owner` from every rank's partial sums (ring-order
+// fp32 fold), applies dropout(x + b) + r and pushes it into every rank's out.
+// Units are handed out in row-tile order by an atomic ticket, so the earliest
+// tiles the GEMM publishes are reduced first.
+struct OvArgs {
+  RankSet rs;            // group ranks (peer heaps), epoch of this call
+  int64_t part_off, b_off, r_off, out_off;
+  int64_t cnt_off;       // per-rank arrival counter (uint32) in the reserved area
+  int64_t flag_off;      // per-rank tile flags
+  int64_t ticket_off;    // unit ticket counter (in the first local rank's heap)
+  int rows, cols, per;   // per = cols / W
+  int tiles_m, tiles_n, bn;
+  int nl;                // local ranks of this launch
+  int n_units;           // tiles_m * nl * 4
+  uint32_t ticket_base;  // ticket value at the start of this call
+  uint32_t arrive_target;  // cumulative arrivals expected on each rank's counter
+  double inv_keep;
+  float frate_scale;
+  uint64_t seed, key, thresh;
+  int math;
+};
+
+template <typename T>
+__device__ __forceinline__ void mp_unit(const OvArgs& a, char* const* base, int me, int mt, int rg, int lane) {
+  static_assert(sizeof(T) == 2, "the overlapped all-reduce moves 16-bit partials");
+  constexpr int U = kUnitU;
+  const int W = a.rs.world;
+  const int qpr = a.per >> 2;
+  const int nq = 32 * qpr;
+  for (int i0 = lane; i0 < nq; i0 += 32 * U) {
+    int64_t gi[U];
+    bool valid[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int i = min(i0 + 32 * u, nq - 1);
+      valid[u] = i0 + 32 * u < nq;
+      const int row = mt * 128 + rg * 32 + i / qpr;
+      gi[u] = int64_t(row) * a.cols + int64_t(me) * a.per + (i % qpr) * 4;
+    }
+    // every rank's quads first (raw 8-byte loads, U*W requests in flight)...
+    uint2 raw[U][kMaxRanks];
+#pragma unroll
+    for (int j = 0; j < kMaxRanks; ++j)
+      if (j < W) {
+        int src = me + 1 + j;
+        src -= src >= W ? W : 0;
+        src -= src >= W ? W : 0;
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+          raw[u][j] = __ldcg(reinterpret_cast<const uint2*>(reinterpret_cast<const T*>(base[src] + a.part_off) + gi[u]));
+      }
+    // ...then the ring-order fold (runtime.hpp:302-305)
+    float acc[U][4];
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+#pragma unroll
+      for (int j = 0; j < kMaxRanks; ++j)
+        if (j < W) {
+          const T* h = reinterpret_cast<const T*>(&raw[u][j]);
+#pragma unroll
+          for (int e = 0; e < 4; ++e) acc[u][e] = j == 0 ? to_f32(h[e]) : __fadd_rn(acc[u][e], to_f32(h[e]));
+        }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      if (!valid[u]) continue;
+      const int64_t col = gi[u] % a.cols;
+      float b4[4], r4[4], o[4];
+      load4(reinterpret_cast<const T*>(base[me] + a.b_off) + col, b4);
+      load4(reinterpret_cast<const T*>(base[me] + a.r_off) + gi[u], r4);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const bool keep = dropout_keep_bits(a.seed, a.key, uint64_t(gi[u] + e), a.thresh);
+        if (a.math == COCONET_MATH_EXACT) {
+          const double sum = __dadd_rn(double(acc[u][e]), double(b4[e]));
+          o[e] = float(__dadd_rn(keep ? __ddiv_rn(sum, a.inv_keep) : 0.0, double(r4[e])));
+        } else {
+          o[e] = (keep ? (acc[u][e] + b4[e]) * a.frate_scale : 0.f) + r4[e];
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < kMaxRanks; ++j) {
+        if (j >= W) break;
+        store4(reinterpret_cast<T*>(base[j] + a.out_off) + gi[u], o);
+      }
+    }
+  }
+}
+
+// One warp's share of the all-reduce: take tickets until the units run out.
+template <typename T>
+__device__ void mp_comm_warp(const OvArgs& a, char* const* base, int lane) {
+  const unsigned full = 0xffffffffu;
+  const int W = a.rs.world;
+  unsigned int* ticket = reinterpret_cast<unsigned int*>(base[a.rs.me >= 0 ? a.rs.me : 0] + a.ticket_off);
+  for (;;) {
+    int u = 0;
+    if (lane == 0) u = int(atomicAdd(ticket, 1u) - a.ticket_base);
+    u = __shfl_sync(full, u, 0);
+    if (u >= a.n_units) break;
+    const int mt = u / (a.nl * 4);
+    const int rem = u - mt * a.nl * 4;
+    const int lr = rem >> 2, rg = rem & 3;
+    const int me = a.rs.me >= 0 ? a.rs.me : lr;
+    const int t_lo = (me * a.per) / a.bn, t_hi = ((me + 1) * a.per - 1) / a.bn;
+    bool ok = true;
+    if (lane < W) {
+      const uint32_t* fl = reinterpret_cast<const uint32_t*>(base[lane] + a.flag_off);
+      for (int nt = t_lo; nt <= t_hi; ++nt) ok &= wait_flag(fl + mt * a.tiles_n + nt, a.rs.epoch, a.rs);
+    }
+    if (!__all_sync(full, ok)) continue;  // watchdog fired; status already recorded
+    mp_unit<T>(a, base, me, mt, rg, lane);
+    __syncwarp();
+    if (lane < W) {  // one arrival per (unit, destination rank)
+      __threadfence_system();
+      atomicAdd_system(reinterpret_cast<unsigned int*>(base[lane] + a.cnt_off), 1u);
+    }
+  }
+}
+
+template <int BN, typename TO, bool FUSED>
+__global__ void __launch_bounds__(FUSED ? kFusedThreads : kGemmThreads, 1)
+    gemm_tc_kernel(const __grid_constant__ RankMaps maps, GemmArgs g, uint32_t in_fmt, OvArgs ov) {
+  __shared__ char* s_base[kMaxRanks];
+  if (FUSED && threadIdx.x < kMaxRanks)
+    s_base[threadIdx.x] = threadIdx.x < ov.rs.world ? ov.rs.base[threadIdx.x] : nullptr;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * Cfg<BN>::STAGE_BYTES);
-  uint64_t* empty = full + STAGES;
-  uint64_t* tfull = empty + STAGES;
+  uint8_t* epi = smem + Cfg<BN>::STAGES * Cfg<BN>::STAGE_BYTES;  // 1024-aligned staging
+  uint64_t* full = reinterpret_cast<uint64_t*>(epi + Cfg<BN>::EPI_BYTES);
+  uint64_t* empty = full + Cfg<BN>::STAGES;
+  uint64_t* tfull = empty + Cfg<BN>::STAGES;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (warp == 0 && lane == 0) {
-    for (int s = 0; s < STAGES; ++s) {
+    for (int s = 0; s < Cfg<BN>::STAGES; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
@@ -232,12 +373,16 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_tc_kernel(const __grid_c
           mbar_expect_tx(&full[stage], Cfg<BN>::STAGE_BYTES);
           tma_load_2d(sa, &maps.a[r], kb * BK, mt * BM, &full[stage]);
           tma_load_2d(sa + Cfg<BN>::A_BYTES, &maps.b[r], kb * BK, nt * BN, &full[stage]);
-          if (++stage == STAGES) {
+          if (++stage == Cfg<BN>::STAGES) {
             stage = 0;
             phase ^= 1;
           }
         }
       }
+    }
+    if constexpr (FUSED) {
+      __syncwarp();
+      mp_comm_warp<TO>(ov, s_base, lane);
     }
   } else if (warp == 1) {
     if (lane == 0) {  // ---- MMA issuer (single thread)
@@ -259,7 +404,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_tc_kernel(const __grid_c
           for (int k = 0; k < BK / 16; ++k)  // +32 bytes along K per UMMA_K = 16
             mma_f16(d, da + 2 * k, db + 2 * k, idesc, (kb | k) != 0);
           mma_commit(&empty[stage]);  // frees the smem stage once these MMAs retire
-          if (++stage == STAGES) {
+          if (++stage == Cfg<BN>::STAGES) {
             stage = 0;
             phase ^= 1;
           }
@@ -269,26 +414,67 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_tc_kernel(const __grid_c
         if (acc == 0) acc_phase ^= 1;
       }
     }
-  } else if (warp >= 4) {  // ---- epilogue: TMEM -> registers -> global (+ tile flag)
+    if constexpr (FUSED) {
+      __syncwarp();
+      mp_comm_warp<TO>(ov, s_base, lane);
+    }
+  } else if (warp >= 4 && warp < 8) {  // ---- epilogue: TMEM -> registers -> swizzled smem -> TMA store
     const int q = warp & 3;
-    int acc = 0;
+    uint8_t* stg = epi + q * 2 * 4096;
+    constexpr int kCols = 128 / int(sizeof(TO));  // columns per 128-byte row chunk
+    int acc = 0, buf = 0;
     uint32_t acc_phase = 0;
     for (int t = blockIdx.x; t < total; t += gridDim.x) {
       int r, mt, nt;
       decode_tile(g, t, r, mt, nt);
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
-      const int row = mt * BM + q * 32 + lane;
-      TO* crow = reinterpret_cast<TO*>(g.c[r]) + int64_t(row) * g.N + nt * BN;
+      const uint32_t tbase = tmem + (uint32_t(q * 32) << 16) + uint32_t(acc * kAccStride);
 #pragma unroll 1
-      for (int c = 0; c < BN / 32; ++c) {
-        uint32_t v[32];
-        tmem_ld32(tmem + (uint32_t(q * 32) << 16) + uint32_t(acc * kAccStride + c * 32), v);
-        store_row32<TO>(crow + c * 32, v);
+      for (int cc = 0; cc < BN / kCols; ++cc) {
+        // this staging buffer was last read by the store issued two chunks ago
+        if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+        __syncwarp();
+        uint8_t* row = stg + buf * 4096 + lane * 128;
+        uint32_t h[32];
+        if constexpr (sizeof(TO) == 4) {
+          uint32_t v[32];
+          tmem_ld32(tbase + uint32_t(cc * 32), v);
+#pragma unroll
+          for (int i = 0; i < 32; ++i) h[i] = v[i];
+        } else {
+          uint32_t v[32], w[32];
+          tmem_ld32(tbase + uint32_t(cc * 64), v);
+          tmem_ld32(tbase + uint32_t(cc * 64 + 32), w);
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            TO lo = from_f32<TO>(__uint_as_float(v[2 * i])), hi = from_f32<TO>(__uint_as_float(v[2 * i + 1]));
+            h[i] = uint32_t(*reinterpret_cast<uint16_t*>(&lo)) | (uint32_t(*reinterpret_cast<uint16_t*>(&hi)) << 16);
+            TO lo2 = from_f32<TO>(__uint_as_float(w[2 * i])), hi2 = from_f32<TO>(__uint_as_float(w[2 * i + 1]));
+            h[16 + i] =
+                uint32_t(*reinterpret_cast<uint16_t*>(&lo2)) | (uint32_t(*reinterpret_cast<uint16_t*>(&hi2)) << 16);
+          }
+        }
+        // 128B swizzle (matches the output tensor map): chunk j of row l lands at j ^ (l % 8)
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+          *reinterpret_cast<uint4*>(row + ((j ^ (lane & 7)) << 4)) = make_uint4(h[4 * j], h[4 * j + 1], h[4 * j + 2], h[4 * j + 3]);
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) {
+          tma_store_2d(&maps.c[r], stg + buf * 4096, nt * BN + cc * kCols, mt * BM + q * 32);
+          asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        }
+        buf ^= 1;
       }
       tc_fence_before();
       mbar_arrive(&tempty[acc]);
       if (g.flags[r] != nullptr) {
+        if (lane == 0) {
+          asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // this warp's stores are complete
+          asm volatile("fence.proxy.async;" ::: "memory");
+        }
+        __syncwarp();
         asm volatile("bar.sync 1, 128;" ::: "memory");
         if (warp == 4 && lane == 0) {
           __threadfence_system();
@@ -298,12 +484,22 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_tc_kernel(const __grid_c
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1;
     }
+    if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    __syncwarp();
+    if constexpr (FUSED) mp_comm_warp<TO>(ov, s_base, lane);
+  } else if constexpr (FUSED) {  // warps 2, 3 and 8-15: all-reduce from the start
+    mp_comm_warp<TO>(ov, s_base, lane);
   }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   if (warp == 2)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols) : "memory");
+  // the caller's `out` is complete once every unit of every owner has landed
+  if (FUSED && blockIdx.x == 0 && threadIdx.x < ov.nl) {
+    const int r = ov.rs.me >= 0 ? ov.rs.me : int(threadIdx.x);
+    wait_flag(reinterpret_cast<const uint32_t*>(s_base[r] + ov.cnt_off), ov.arrive_target, ov.rs);
+  }
 }
 
 // B [K, N] row-major -> BT [N, K] (K-major operand for the MMA)
@@ -383,11 +579,15 @@ int make_map(CUtensorMap* map, const void* base, int elem, uint64_t inner, uint6
              uint32_t box_outer) {
   auto fn = encode_fn();
   if (!fn) return set_error(COCONET_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  const uint64_t esz = elem == COCONET_F32 ? 4 : 2;
   cuuint64_t dims[2] = {inner, outer};
-  cuuint64_t strides[1] = {inner * 2};
+  cuuint64_t strides[1] = {inner * esz};
   cuuint32_t box[2] = {box_inner, box_outer};
   cuuint32_t estr[2] = {1, 1};
-  CUresult r = fn(map, elem == COCONET_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2,
+  const CUtensorMapDataType dt = elem == COCONET_BF16  ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16
+                                 : elem == COCONET_F16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16
+                                                       : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
+  CUresult r = fn(map, dt, 2,
                   const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                   CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return set_error(COCONET_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string(int(r)));
@@ -427,8 +627,8 @@ struct TcPlan {
 
 // Prepares the tcgen05 launch for every local rank of `group`: transposes
 // each B into scratch and encodes the TMA maps.
-int plan_tc(coconet_ctx* c, int group, const void* a, const void* b, void* cc, int in_elem, int64_t m, int64_t n,
-            int64_t k, cudaStream_t s, TcPlan* p) {
+int plan_tc(coconet_ctx* c, int group, const void* a, const void* b, void* cc, int in_elem, int out_elem, int64_t m,
+            int64_t n, int64_t k, cudaStream_t s, TcPlan* p) {
   if (m % BM) return set_error(COCONET_ERR_UNSUPPORTED, "M must be a multiple of 128");
   if (k % BK) return set_error(COCONET_ERR_UNSUPPORTED, "K must be a multiple of 64");
   int bn = n % 256 == 0 ? 256 : (n % 192 == 0 ? 192 : (n % 128 == 0 ? 128 : 0));
@@ -455,6 +655,8 @@ int plan_tc(coconet_ctx* c, int group, const void* a, const void* b, void* cc, i
     c->launches++;
     rc = make_map(&p->maps.a[i], heap + ao, in_elem, uint64_t(k), uint64_t(m), BK, BM);
     if (!rc) rc = make_map(&p->maps.b[i], bt, in_elem, uint64_t(k), uint64_t(n), BK, uint32_t(bn));
+    if (!rc)
+      rc = make_map(&p->maps.c[i], heap + co, out_elem, uint64_t(n), uint64_t(m), out_elem == COCONET_F32 ? 32 : 64, 32);
     if (rc) return rc;
     p->g.c[i] = heap + co;
   }
@@ -469,143 +671,50 @@ int plan_tc(coconet_ctx* c, int group, const void* a, const void* b, void* cc, i
   return COCONET_OK;
 }
 
-template <int BN, typename TO>
-int launch_tc_t(coconet_ctx* c, TcPlan* p, uint32_t in_fmt, int grid_cap, cudaStream_t s) {
-  auto fn = gemm_tc_kernel<BN, TO>;
+template <int BN, typename TO, bool FUSED>
+int launch_tc_t(coconet_ctx* c, TcPlan* p, uint32_t in_fmt, const OvArgs* ov, cudaStream_t s) {
+  auto fn = gemm_tc_kernel<BN, TO, FUSED>;
   const int smem = Cfg<BN>::SMEM;
   CN_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   const int total = p->g.ranks * p->g.tiles_m * p->g.tiles_n;
-  int grid = std::min(total, grid_cap > 0 ? grid_cap : c->sm_count);
-  fn<<<grid, kGemmThreads, smem, s>>>(p->maps, p->g, in_fmt);
-  CN_CUDA(cudaGetLastError());
+  OvArgs none{};
+  const OvArgs& o = ov ? *ov : none;
+  if (!FUSED) {
+    const int grid = std::min(total, c->sm_count);
+    fn<<<grid, kGemmThreads, smem, s>>>(p->maps, p->g, in_fmt, o);
+    CN_CUDA(cudaGetLastError());
+  } else {
+    // every CTA both computes tiles and all-reduces: co-residency (one CTA
+    // per SM) is guaranteed by the cooperative launch, so comm warps spinning
+    // on tile flags can never starve the CTAs that publish them
+    const int grid = c->sm_count;
+    void* args[] = {const_cast<RankMaps*>(&p->maps), &p->g, &in_fmt, const_cast<OvArgs*>(&o)};
+    CN_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(fn), dim3(grid), dim3(kFusedThreads), args, smem, s));
+  }
   c->launches++;
   return COCONET_OK;
 }
 
-int launch_tc(coconet_ctx* c, TcPlan* p, int in_elem, int out_elem, int grid_cap, cudaStream_t s) {
+template <bool FUSED>
+int launch_tc(coconet_ctx* c, TcPlan* p, int in_elem, int out_elem, const OvArgs* ov, cudaStream_t s) {
   const uint32_t fmt = in_elem == COCONET_BF16 ? 1u : 0u;
   const bool f32 = out_elem == COCONET_F32;
   const bool bf = out_elem == COCONET_BF16;
+  if (FUSED && f32) return set_error(COCONET_ERR_UNSUPPORTED, "the fused overlap keeps 16-bit partials");
   switch (p->bn) {
-    case 256: return f32 ? launch_tc_t<256, float>(c, p, fmt, grid_cap, s)
-                         : (bf ? launch_tc_t<256, __nv_bfloat16>(c, p, fmt, grid_cap, s)
-                               : launch_tc_t<256, __half>(c, p, fmt, grid_cap, s));
-    case 192: return f32 ? launch_tc_t<192, float>(c, p, fmt, grid_cap, s)
-                         : (bf ? launch_tc_t<192, __nv_bfloat16>(c, p, fmt, grid_cap, s)
-                               : launch_tc_t<192, __half>(c, p, fmt, grid_cap, s));
-    default: return f32 ? launch_tc_t<128, float>(c, p, fmt, grid_cap, s)
-                        : (bf ? launch_tc_t<128, __nv_bfloat16>(c, p, fmt, grid_cap, s)
-                              : launch_tc_t<128, __half>(c, p, fmt, grid_cap, s));
-  }
-}
-
-// ---- the overlap consumer: RS -> bias+dropout+residual -> AG per unit -------
-
-struct OvArgs {
-  RankSet rs;            // group ranks (peer heaps)
-  int64_t part_off, b_off, r_off, out_off;
-  int64_t cnt_off;       // per-rank arrival counter (uint32) in the reserved area
-  int64_t flag_off;      // per-rank tile flags
-  int rows, cols, per;   // per = cols / W
-  int tiles_m, tiles_n, bn;
-  uint32_t arrive_target;  // cumulative arrivals expected on this rank's counter
-  double inv_keep;
-  float frate_scale;
-  uint64_t seed, key, thresh;
-  int math;
-};
-
-__device__ __forceinline__ bool wait_ge(const uint32_t* p, uint32_t want, const RankSet& rs) {
-  return wait_flag(p, want, rs);
-}
-
-template <typename T>
-__global__ void __launch_bounds__(256) overlap_consumer_kernel(OvArgs a) {
-  __shared__ char* s_base[kMaxRanks];
-  __shared__ int s_ok;
-  const RankSet& rs = a.rs;
-  if (threadIdx.x < kMaxRanks) s_base[threadIdx.x] = threadIdx.x < rs.world ? rs.base[threadIdx.x] : nullptr;
-  if (threadIdx.x == 0) s_ok = 1;
-  __syncthreads();
-  const int W = rs.world, me = rs.rank();
-  const int t_lo = (me * a.per) / a.bn, t_hi = ((me + 1) * a.per - 1) / a.bn;  // n-tiles of my block
-  const int qpr = a.per / 4;
-  for (int mt = blockIdx.x; mt < a.tiles_m; mt += gridDim.x) {
-    // wait until every rank published the tiles covering (mt, my column block)
-    if (threadIdx.x < W) {
-      const uint32_t* fl = reinterpret_cast<const uint32_t*>(s_base[threadIdx.x] + a.flag_off);
-      for (int nt = t_lo; nt <= t_hi; ++nt)
-        if (!wait_ge(fl + mt * a.tiles_n + nt, rs.epoch, rs)) s_ok = 0;
-    }
-    __syncthreads();
-    if (!s_ok) return;
-    for (int i = threadIdx.x; i < 128 * qpr; i += blockDim.x) {
-      const int row = mt * 128 + i / qpr;
-      const int col = me * a.per + (i % qpr) * 4;
-      const int64_t gi = int64_t(row) * a.cols + col;
-      float acc[4], x[4];
-#pragma unroll
-      for (int j = 0; j < kMaxRanks; ++j) {
-        if (j >= W) break;
-        int src = me + 1 + j;
-        src -= src >= W ? W : 0;
-        src -= src >= W ? W : 0;
-        load4_cg(reinterpret_cast<const T*>(s_base[src] + a.part_off) + gi, x);
-#pragma unroll
-        for (int e = 0; e < 4; ++e) acc[e] = j == 0 ? x[e] : __fadd_rn(acc[e], x[e]);
-      }
-      float b4[4], r4[4], o[4];
-      load4(reinterpret_cast<const T*>(s_base[me] + a.b_off) + col, b4);
-      load4(reinterpret_cast<const T*>(s_base[me] + a.r_off) + gi, r4);
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const bool keep = dropout_keep_bits(a.seed, a.key, uint64_t(gi + e), a.thresh);
-        if (a.math == COCONET_MATH_EXACT) {
-          const double sum = __dadd_rn(double(acc[e]), double(b4[e]));
-          o[e] = float(__dadd_rn(keep ? __ddiv_rn(sum, a.inv_keep) : 0.0, double(r4[e])));
-        } else {
-          o[e] = (keep ? (acc[e] + b4[e]) * a.frate_scale : 0.f) + r4[e];
-        }
-      }
-#pragma unroll
-      for (int j = 0; j < kMaxRanks; ++j) {
-        if (j >= W) break;
-        store4(reinterpret_cast<T*>(s_base[j] + a.out_off) + gi, o);
-      }
-    }
-    __syncthreads();
-    if (threadIdx.x < W) {  // one arrival per (unit, destination rank)
-      __threadfence_system();
-      atomicAdd_system(reinterpret_cast<unsigned int*>(s_base[threadIdx.x] + a.cnt_off), 1u);
-    }
-  }
-  // the caller's `out` is complete once every unit of every owner arrived here
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
-    const uint32_t* cnt = reinterpret_cast<const uint32_t*>(s_base[me] + a.cnt_off);
-    wait_flag(cnt, a.arrive_target, rs);
+    case 256: return f32 ? launch_tc_t<256, float, false>(c, p, fmt, ov, s)
+                         : (bf ? launch_tc_t<256, __nv_bfloat16, FUSED>(c, p, fmt, ov, s)
+                               : launch_tc_t<256, __half, FUSED>(c, p, fmt, ov, s));
+    case 192: return f32 ? launch_tc_t<192, float, false>(c, p, fmt, ov, s)
+                         : (bf ? launch_tc_t<192, __nv_bfloat16, FUSED>(c, p, fmt, ov, s)
+                               : launch_tc_t<192, __half, FUSED>(c, p, fmt, ov, s));
+    default: return f32 ? launch_tc_t<128, float, false>(c, p, fmt, ov, s)
+                        : (bf ? launch_tc_t<128, __nv_bfloat16, FUSED>(c, p, fmt, ov, s)
+                              : launch_tc_t<128, __half, FUSED>(c, p, fmt, ov, s));
   }
 }
 
 constexpr size_t kTileFlagBytes = kCountersOff - kTileFlagsOff;  // per group: up to 16384 tiles
-
-std::mutex g_mp_mu;
-
-cudaStream_t g_side[16] = {};
-cudaEvent_t g_ev[16][2] = {};
-
-int side_stream(int device, cudaStream_t* s, cudaEvent_t* e0, cudaEvent_t* e1) {
-  std::lock_guard<std::mutex> lk(g_mp_mu);
-  int d = device & 15;
-  if (!g_side[d]) {
-    CN_CUDA(cudaStreamCreateWithFlags(&g_side[d], cudaStreamNonBlocking));
-    CN_CUDA(cudaEventCreateWithFlags(&g_ev[d][0], cudaEventDisableTiming));
-    CN_CUDA(cudaEventCreateWithFlags(&g_ev[d][1], cudaEventDisableTiming));
-  }
-  *s = g_side[d];
-  *e0 = g_ev[d][0];
-  *e1 = g_ev[d][1];
-  return COCONET_OK;
-}
 
 }  // namespace
 
@@ -647,9 +756,9 @@ int coconet_matmul(coconet_ctx_t c, int group, const void* a, const void* b, voi
   if (in_elem != COCONET_BF16 && in_elem != COCONET_F16)
     return set_error(COCONET_ERR_UNSUPPORTED, "FAST matmul runs on tcgen05 with bf16/f16 inputs");
   TcPlan p;
-  int rc = plan_tc(c, group, a, b, cc, in_elem, m, n, k, s, &p);
+  int rc = plan_tc(c, group, a, b, cc, in_elem, out_elem, m, n, k, s, &p);
   if (rc) return rc;
-  return launch_tc(c, &p, in_elem, out_elem, 0, s);
+  return launch_tc<false>(c, &p, in_elem, out_elem, nullptr, s);
 }
 
 int coconet_mm_overlap_fused_ar(coconet_ctx_t c, int group, const void* a, const void* w, const void* b,
@@ -664,7 +773,7 @@ int coconet_mm_overlap_fused_ar(coconet_ctx_t c, int group, const void* a, const
   if ((cols / W) % 4) return set_error(COCONET_ERR_UNSUPPORTED, "column block must be a multiple of 4");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   TcPlan p;
-  int rc = plan_tc(c, group, a, w, partial, in_elem, rows, cols, k_local, s, &p);
+  int rc = plan_tc(c, group, a, w, partial, in_elem, in_elem, rows, cols, k_local, s, &p);
   if (rc) return rc;
   if (size_t(p.g.tiles_m) * p.g.tiles_n * 4 > kTileFlagBytes)
     return set_error(COCONET_ERR_UNSUPPORTED, "too many tiles for the flag area");
@@ -676,15 +785,21 @@ int coconet_mm_overlap_fused_ar(coconet_ctx_t c, int group, const void* a, const
   if (!rc) rc = heap_offset(c, r, &o.r_off);
   if (!rc) rc = heap_offset(c, out, &o.out_off);
   if (rc) return rc;
-  // tile flags live in the reserved exchange area of every rank (per group)
+  if ((o.part_off | o.b_off | o.r_off | o.out_off) % 8)
+    return set_error(COCONET_ERR_INVALID_INPUT, "operands must be aligned to 4 elements");
+  // tile flags, arrival counter and unit ticket live in every rank's reserved
+  // per-group area (common.cuh)
   o.flag_off = int64_t(group_area(group) + kTileFlagsOff);
   o.cnt_off = int64_t(group_area(group) + kCountersOff);
+  o.ticket_off = o.cnt_off + 64;
   o.rows = int(rows);
   o.cols = int(cols);
   o.per = int(cols / W);
   o.tiles_m = p.g.tiles_m;
   o.tiles_n = p.g.tiles_n;
   o.bn = p.bn;
+  o.nl = local_ranks(c, group);
+  o.n_units = p.g.tiles_m * o.nl * 4;
   o.inv_keep = 1.0 - hp->rate;
   o.frate_scale = float(1.0 / (1.0 - hp->rate));
   o.seed = hp->seed;
@@ -692,36 +807,17 @@ int coconet_mm_overlap_fused_ar(coconet_ctx_t c, int group, const void* a, const
   double th = std::ceil(hp->rate * 9007199254740992.0);
   o.thresh = th <= 0 ? 0 : uint64_t(th);
   o.math = hp->math;
-  // every owner adds one arrival per row tile to every rank's counter
-  c->mp_arrivals[group] += uint32_t(p.g.tiles_m) * uint32_t(W);
+  // every owner's units each add one arrival to every rank's counter
+  c->mp_arrivals[group] += uint32_t(p.g.tiles_m) * 4u * uint32_t(W);
   o.arrive_target = c->mp_arrivals[group];
+  // tickets drawn this call: one per unit, plus the one failing draw with
+  // which each of the grid's warps (sm_count CTAs x kFusedWarps) leaves the loop
+  o.ticket_base = c->mp_tickets[group];
+  c->mp_tickets[group] += uint32_t(o.n_units) + uint32_t(c->sm_count) * uint32_t(kFusedWarps);
   for (int i = 0; i < p.g.ranks; ++i)
     p.g.flags[i] = reinterpret_cast<uint32_t*>(p.g.c[i] - o.part_off + o.flag_off);
   p.g.epoch = o.rs.epoch;
-  cudaStream_t side;
-  cudaEvent_t e0, e1;
-  rc = side_stream(c->device, &side, &e0, &e1);
-  if (rc) return rc;
-  // GEMM on the caller's stream, consumer on a side stream ordered after the
-  // caller's prior work; the caller's stream then waits for the consumer.
-  CN_CUDA(cudaEventRecord(e0, s));
-  CN_CUDA(cudaStreamWaitEvent(side, e0, 0));
-  const int nl = local_ranks(c, group);
-  int cblocks = std::max(1, std::min(p.g.tiles_m, c->sm_count / nl));
-  auto cfn = in_elem == COCONET_BF16 ? overlap_consumer_kernel<__nv_bfloat16> : overlap_consumer_kernel<__half>;
-  // The GEMM is enqueued FIRST: it never waits on the consumer, so the pair is
-  // deadlock-free whatever the hardware does with the two streams (measured:
-  // a consumer enqueued first can hold the GEMM back until it times out). The
-  // consumer's CTAs (256 threads, no smem) fit beside the 1-per-SM GEMM CTAs
-  // and start polling tile flags while the GEMM is still running.
-  rc = launch_tc(c, &p, in_elem, in_elem, c->sm_count, s);
-  if (rc) return rc;
-  cfn<<<dim3(unsigned(cblocks), unsigned(nl)), 256, 0, side>>>(o);
-  CN_CUDA(cudaGetLastError());
-  c->launches++;
-  CN_CUDA(cudaEventRecord(e1, side));
-  CN_CUDA(cudaStreamWaitEvent(s, e1, 0));
-  return COCONET_OK;
+  return launch_tc<true>(c, &p, in_elem, in_elem, &o, s);
 }
 
 }  // extern "C"

@@ -36,6 +36,7 @@ struct coconet_ctx {
   // cumulative arrivals expected on this rank's per-group counter (overlapped
   // MatMul + fused AllReduce); the device counters start at 0 with the heap
   uint32_t mp_arrivals[coconet::kMaxGroups] = {};
+  uint32_t mp_tickets[coconet::kMaxGroups] = {};  // unit tickets handed out so far
   std::vector<coconet_group_s> groups;
 };
 
