@@ -25,7 +25,6 @@ import argparse
 import json
 import os
 import statistics
-import subprocess
 import sys
 import threading
 import time
@@ -37,6 +36,7 @@ sys.path.insert(0, str(ROOT))
 METRIC = "fused AR+Adam/LAMB step time & NVLink-roofline fraction, 1/2/4/8 B200"
 UNIT = "Gelem/s"
 NVLINK_GBS = 770.0  # measured peer copy per direction (B200_PROFILING.md)
+CPU_SAMPLE = 1 << 22  # elements per core for cpu_baseline: ~10-30 s of CPU work
 
 
 def peaks():
@@ -51,51 +51,50 @@ def peaks():
 # clocks sampled during the timed region (B200_PROFILING.md recipe)
 
 class ClockSampler:
+    """Polls NVML every 10 ms during the timed region: SM clock and the
+    throttle reasons the recipe rejects on (B200_PROFILING.md)."""
+
+    REASONS = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+               "sw_power_cap": 0x4}
+
     def __init__(self, device: int):
         self.device = device
         self.samples = []
-        self.proc = None
+        self.stop_flag = threading.Event()
         self.thread = None
+        self.max_mhz = None
 
     def start(self):
-        cmd = ["nvidia-smi", "-i", str(self.device),
-               "--query-gpu=clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
-               "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-               "clocks_event_reasons.sw_power_cap", "--format=csv,noheader,nounits", "-lms", "100"]
         try:
-            self.proc = subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-        except FileNotFoundError:
+            import pynvml
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.device)
+            self.max_mhz = float(pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM))
+        except Exception:
             return
 
-        def rd():
-            for line in self.proc.stdout:
-                self.samples.append([x.strip() for x in line.split(",")])
+        def run():
+            while not self.stop_flag.is_set():
+                try:
+                    mhz = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+                    reasons = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+                    self.samples.append((float(mhz), int(reasons)))
+                except Exception:
+                    pass
+                time.sleep(0.01)
 
-        self.thread = threading.Thread(target=rd, daemon=True)
+        self.thread = threading.Thread(target=run, daemon=True)
         self.thread.start()
 
     def stop(self):
-        if self.proc:
-            self.proc.terminate()
-            try:
-                self.proc.wait(timeout=2)
-            except Exception:
-                self.proc.kill()
+        self.stop_flag.set()
         if self.thread:
             self.thread.join(timeout=1)
-        rows = [s for s in self.samples if len(s) >= 7]
-        if not rows:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
-        reasons = set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for r in rows:
-            for n, v in zip(names, r[3:7]):
-                if v.lower() == "active":
-                    reasons.add(n)
-        return {"sm_mhz": statistics.median(sm) if sm else None,
-                "sm_max_mhz": float(rows[0][1]) if rows[0][1].replace(".", "").isdigit() else None,
-                "samples": len(rows), "reasons": sorted(reasons)}
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "samples": 0, "reasons": ["unsampled"]}
+        active = sorted({n for _, bits in self.samples for n, m in self.REASONS.items() if bits & m})
+        return {"sm_mhz": statistics.median(m for m, _ in self.samples), "sm_max_mhz": self.max_mhz,
+                "samples": len(self.samples), "reasons": active, "source": "NVML, 10 ms"}
 
 
 # ---------------------------------------------------------------------------
@@ -144,7 +143,7 @@ def run_reference(args):
                           "unavailable": "oracle/_ref/libccopt_ref.so not built (needs /root/reference at build time)"}))
         return
     cores = os.cpu_count() or 1
-    sample = 1 << 18
+    sample = 1 << 21  # per core per step: ~3-4 s of CPU work on 16 cores
     # warmup steps, then timed steps; each step is a bounded sample per core
     for _ in range(max(0, min(args.warmup, 1))):
         reference_cpu(sample, cores, 1)
@@ -296,15 +295,28 @@ def run_coconet(args):
         except Exception:
             pass
 
+    extras = None
+    if rank == 0 and world == 1 and not args.no_extras:
+        # the other BASELINE configs on this GPU with virtual ranks (kernel and
+        # protocol cost; "NVLink" traffic is local HBM here) - see DESIGN.md
+        try:
+            ctx.close()
+            from tools.pattern_probe import c1, c3, c4
+            extras = {"note": "one GPU, virtual ranks: all ranks' traffic is local HBM"}
+            for f in (c1, c3, c4):
+                f(extras)
+        except Exception as e:
+            extras = {"failed": repr(e)}
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
             from oracle import ref
             if ref.available():
                 cores = os.cpu_count() or 1
-                rate, wall = reference_cpu(1 << 18, cores, 1)
+                rate, wall = reference_cpu(CPU_SAMPLE, cores, 1)
                 cpu = {"value": rate / 1e9, "unit": UNIT, "cores": cores, "kind": "reference",
-                       "sample": f"{cores} concurrent reference Engines x 262144-element LAMB "
+                       "sample": f"{cores} concurrent reference Engines x {CPU_SAMPLE}-element LAMB "
                                  f"(tests/golden/lamb_fused_program.json, W=1) in {wall:.1f} s"}
         except Exception as e:  # the baseline is reported, not required
             cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "reference", "sample": f"failed: {e}"}
@@ -326,9 +338,11 @@ def run_coconet(args):
                     "what": "pinned H2D of this rank's fp16 grads + fused step + D2H of updated fp32 params"},
             "gpu_launches": launches, "clocks": clocks,
             "kernel_ms": ms,
+            "extras": extras,
         }
         print(json.dumps(line))
-    ctx.close()
+    if ctx.handle:
+        ctx.close()
     if distributed:
         dist.destroy_process_group()
 
@@ -340,6 +354,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="coconet", choices=["coconet", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-extras", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

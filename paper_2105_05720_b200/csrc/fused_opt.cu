@@ -28,6 +28,7 @@
 #include <cooperative_groups.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cmath>
 
 #include "fused_opt.h"
@@ -338,8 +339,8 @@ __device__ __forceinline__ float lamb_u(float m, float v, float p, const LambK& 
 //  deterministic) -> pushed into every peer's exchange area -> flag barrier
 //  -> totals combined in rank order (state.hpp:163-167)
 //  pass 2: trust ratio -> p update -> AG push.
-template <typename G, int WT, int U>
-__global__ void __launch_bounds__(kThreads, 2) lamb_kernel(OptArgs a, LambK k) {
+template <typename G, int WT, int U, int MINB = 2>
+__global__ void __launch_bounds__(kThreads, MINB) lamb_kernel(OptArgs a, LambK k) {
   __shared__ char* s_base[kMaxRanks];
   const RankSet& rs = a.rs;
   if (threadIdx.x < kMaxRanks) s_base[threadIdx.x] = threadIdx.x < rs.world ? rs.base[threadIdx.x] : nullptr;
@@ -554,7 +555,8 @@ const void* adam_pick(int math, bool os, int W) {
 template <typename T, int RED, bool OS>
 const void* ar_w(int W) {
   switch (W) {
-    case 1: return reinterpret_cast<const void*>(&allreduce_kernel<T, RED, OS, 1, 4>);
+    // 16-bit elements move 8 bytes per quad: twice the quads in flight
+    case 1: return reinterpret_cast<const void*>(&allreduce_kernel<T, RED, OS, 1, sizeof(T) == 2 ? 8 : 4>);
     case 2: return reinterpret_cast<const void*>(&allreduce_kernel<T, RED, OS, 2, 4>);
     case 4: return reinterpret_cast<const void*>(&allreduce_kernel<T, RED, OS, 4, 2>);
     case 8: return reinterpret_cast<const void*>(&allreduce_kernel<T, RED, OS, 8, 1>);
@@ -572,7 +574,14 @@ const void* ar_pick(int red, bool os, int W) {
 template <typename G>
 const void* lamb_pick(int W) {
   switch (W) {
-    case 1: return reinterpret_cast<const void*>(&lamb_kernel<G, 1, 4>);
+    case 1: {
+      // occupancy/unroll trade-off at W=1 (probe with COCONET_LAMB_VARIANT)
+      const char* v = getenv("COCONET_LAMB_VARIANT");
+      if (v && v[0] == '1') return reinterpret_cast<const void*>(&lamb_kernel<G, 1, 2, 3>);
+      if (v && v[0] == '2') return reinterpret_cast<const void*>(&lamb_kernel<G, 1, 3, 3>);
+      if (v && v[0] == '3') return reinterpret_cast<const void*>(&lamb_kernel<G, 1, 2, 4>);
+      return reinterpret_cast<const void*>(&lamb_kernel<G, 1, 4>);
+    }
     case 2: return reinterpret_cast<const void*>(&lamb_kernel<G, 2, 2>);
     case 4: return reinterpret_cast<const void*>(&lamb_kernel<G, 4, 2>);
     case 8: return reinterpret_cast<const void*>(&lamb_kernel<G, 8, 1>);

@@ -3,6 +3,7 @@ the fused DP kernels at BERT-336M size on one GPU, next to a torch copy as the
 bandwidth yardstick. Usage: python tools/probe.py [--steps K]"""
 import argparse
 import json
+import os
 import sys
 from pathlib import Path
 
@@ -59,9 +60,12 @@ def main():
                 ctx.view(v, r).fill_(1e-3)
             gb = 2 if gdt == torch.float16 else 4
             hp = LambHParams(lr=1e-3, beta1=0.9, beta2=0.999, t=1.0)
-            ms = timeit(lambda: fused_rs_lamb_ag(ctx, tl, grads, params, m, v, hp), args.steps)
             byt = (gb + 12 + 8 + 12 + 4) * N
-            out[f"lamb_W{W}_g{gname}"] = {"ms": ms, "GBs": byt / ms / 1e6, "bytes": byt}
+            for var in ("0", "1", "2", "3"):
+                os.environ["COCONET_LAMB_VARIANT"] = var
+                ms = timeit(lambda: fused_rs_lamb_ag(ctx, tl, grads, params, m, v, hp), args.steps)
+                out[f"lamb_W{W}_g{gname}_v{var}"] = {"ms": ms, "GBs": byt / ms / 1e6, "bytes": byt}
+            os.environ.pop("COCONET_LAMB_VARIANT", None)
             for math, mn in ((_lib.MATH_FAST, "fast"), (_lib.MATH_EXACT, "exact")):
                 hpa = AdamHParams(lr=1e-3, beta1=0.9, beta2=0.999, t=1.0, eps=1e-8, math=math,
                                   algo=_lib.ALGO_TWO_SHOT)
