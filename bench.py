@@ -176,17 +176,25 @@ def run_coconet(args):
 
     from paper_2105_05720_b200 import _lib
     from paper_2105_05720_b200.collectives import LambHParams, TensorList, fused_rs_lamb_ag, gen_values
-    from paper_2105_05720_b200.runtime import Context
+    from paper_2105_05720_b200.runtime import Context, max_over_ranks
     from paper_2105_05720_b200.workloads import BERT_LARGE_PARAMS, bert_large_counts
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    # test-only: run every rank on GPU 0 (CUDA IPC works between processes on
+    # one device; NCCL does not accept duplicate GPUs, so bootstrap over gloo)
+    share = os.environ.get("COCONET_SHARE_DEVICE") == "1"
+    if share:
+        local_rank = 0
     assert world == args.gpus, f"--gpus {args.gpus} but WORLD_SIZE={world}"
     torch.cuda.set_device(local_rank)
     distributed = world > 1
     if distributed:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if share:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     counts = bert_large_counts()
     padded = [(n + 63) // 64 * 64 for n in counts]
     W = world
@@ -237,9 +245,7 @@ def run_coconet(args):
     launches = ctx.launch_count() - launches0
     ms = e0.elapsed_time(e1) / args.steps
     if distributed:
-        t = torch.tensor([ms], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+        ms = max_over_ranks(ms)
     N = BERT_LARGE_PARAMS
     value = W * N / (ms * 1e-3) / 1e9
 
@@ -263,9 +269,7 @@ def run_coconet(args):
     barrier()
     e2e_s = (time.perf_counter() - t0) / e2e_steps
     if distributed:
-        t = torch.tensor([e2e_s], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_s = float(t.item())
+        e2e_s = max_over_ranks(e2e_s)
     h2d = sum(counts) * 2
     d2h = sum(counts) * 4
 
@@ -289,7 +293,7 @@ def run_coconet(args):
                 "algorithmic_bytes_per_launch": nvl_bytes}
     prof = ROOT / "profiles" / "ncu_traffic.json"
     roof["traffic"] = None
-    if prof.exists():
+    if prof.exists() and W == 1:  # the committed capture is of the W=1 launch
         try:
             roof["traffic"] = json.loads(prof.read_text()).get("lamb_kernel", {}).get("dram_bytes_per_launch")
         except Exception:
