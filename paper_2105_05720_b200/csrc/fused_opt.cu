@@ -322,6 +322,12 @@ __global__ void __launch_bounds__(kThreads, 2) allreduce_kernel(OptArgs a) {
   rank_barrier(rs, 1);
 }
 
+__device__ __forceinline__ float warp_sumf(float x) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+  return x;
+}
+
 __device__ __forceinline__ double warp_sum(double x) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
@@ -361,7 +367,7 @@ __global__ void __launch_bounds__(kThreads, MINB) lamb_kernel(OptArgs a, LambK k
     const SegD d = it.get();
     const int64_t s = it.index();
     const int64_t q0 = d.toff >> 2, q1 = (d.toff + d.len + 3) >> 2;
-    double sp = 0.0, su = 0.0;
+    float sp = 0.f, su = 0.f;  // <=1024 squares per segment: fp32 is ample
     for (int64_t qb = q0 + lane; qb < q1; qb += 32 * U) {
       float g[U][Ranks<WT>::kMax][4], mm[U][4], vv[U][4], pp[U][4];
 #pragma unroll
@@ -399,18 +405,18 @@ __global__ void __launch_bounds__(kThreads, MINB) lamb_kernel(OptArgs a, LambK k
               fu = fmaf(uu, uu, fu);
             }
           }
-          sp += double(fp);
-          su += double(fu);
+          sp += fp;
+          su += fu;
           st4m(m + si, mm[u], lo, hi);
           st4m(v + si, vv[u], lo, hi);
         }
       }
     }
-    sp = warp_sum(sp);
-    su = warp_sum(su);
+    sp = warp_sumf(sp);
+    su = warp_sumf(su);
     if (lane == 0) {
-      k.seg_part[2 * s] = sp;
-      k.seg_part[2 * s + 1] = su;
+      k.seg_part[2 * s] = double(sp);
+      k.seg_part[2 * s + 1] = double(su);
     }
   }
   __threadfence();

@@ -80,5 +80,61 @@ def main():
     print(json.dumps(out, indent=1))
 
 
-if __name__ == "__main__":
+if __name__ == "__main__" and not os.environ.get("PROBE_EXTRA"):
     main()
+
+
+def extra_probes(steps=10):
+    """LAMB bucket-capacity sensitivity; torch's fused multi-tensor Adam on the
+    same list (library baseline); C5 = 3.9e9-parameter Adam at W=1."""
+    out = {}
+    counts = bert_large_counts()
+    N = sum(counts)
+    ctx = Context(1, heap_bytes=N * 24 + (1 << 30))
+    for cap in (1024, 4096, 16384):
+        tl = TensorList(ctx, counts, bucket_cap=cap)
+        grads = [ctx.alloc([n], torch.float16) for n in counts]
+        params = [ctx.alloc([n]) for n in counts]
+        m, v = ctx.alloc([tl.shard_elems]), ctx.alloc([tl.shard_elems])
+        for i, n in enumerate(counts):
+            ctx.view(grads[i], 0).normal_()
+            ctx.view(params[i], 0).uniform_(0.1, 0.9)
+        ctx.view(m, 0).zero_()
+        ctx.view(v, 0).fill_(1e-3)
+        hp = LambHParams(lr=1e-3, beta1=0.9, beta2=0.999, t=1.0)
+        ms = timeit(lambda: fused_rs_lamb_ag(ctx, tl, grads, params, m, v, hp), steps)
+        out[f"lamb_cap{cap}_ms"] = ms
+        tl.close()
+        ctx.reset()
+    ctx.close()
+    # torch fused multi-tensor Adam (fp32 grads/params/state), same 398 tensors
+    ps = [torch.rand(n, device="cuda") for n in counts]
+    gs = [torch.randn(n, device="cuda") for n in counts]
+    ms_ = [torch.zeros(n, device="cuda") for n in counts]
+    vs_ = [torch.full((n,), 1e-3, device="cuda") for n in counts]
+    steps_t = [torch.tensor(1.0, device="cuda") for _ in counts]
+    f = lambda: torch._fused_adam_(ps, gs, ms_, vs_, [], steps_t, amsgrad=False, lr=1e-3, beta1=0.9,
+                                   beta2=0.999, weight_decay=0.0, eps=1e-8, maximize=False)
+    out["torch_fused_adam_fp32_ms"] = timeit(f, steps)
+    del ps, gs, ms_, vs_
+    torch.cuda.empty_cache()
+    # C5 at W=1: 3.9e9 parameters, fp32 grads/params/state (64-bit indexing)
+    n5 = 3_900_000_000
+    ctx = Context(1, heap_bytes=n5 * 16 + (1 << 30))
+    tl = TensorList(ctx, [n5])
+    g, p = ctx.alloc([n5]), ctx.alloc([n5])
+    m, v = ctx.alloc([tl.shard_elems]), ctx.alloc([tl.shard_elems])
+    gen_values(ctx, ctx.view(g, 0), 1, "g", "local", 0, [n5], group_size=1)
+    gen_values(ctx, ctx.view(p, 0), 1, "p", "replicated", 0, [n5], group_size=1)
+    ctx.view(m, 0).zero_()
+    ctx.view(v, 0).fill_(1e-3)
+    hp = AdamHParams(lr=1e-3, beta1=0.9, beta2=0.999, t=1.0, eps=1e-8, math=_lib.MATH_FAST, algo=_lib.ALGO_TWO_SHOT)
+    ms = timeit(lambda: fused_rs_adam_ag(ctx, tl, [g], [p], m, v, hp), 5)
+    out["c5_adam_3.9e9_W1_fast_ms"] = ms
+    out["c5_adam_GBs"] = 28 * n5 / (ms * 1e-3) / 1e9
+    ctx.close()
+    return out
+
+
+if __name__ == "__main__" and os.environ.get("PROBE_EXTRA"):
+    print(json.dumps(extra_probes(), indent=1))
