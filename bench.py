@@ -206,8 +206,16 @@ def run_coconet(args):
     # the parity tests pin; for this workload 4096-element buckets amortise the
     # per-segment cost (descriptor + per-segment norm reduction), DESIGN.md §3
     tl = TensorList(ctx, counts, bucket_cap=BUCKET_CAP)
-    grads = [ctx.alloc([n], torch.float16) for n in counts]
-    params = [ctx.alloc([n], torch.float32) for n in counts]
+    # one flat buffer per dtype (tensors at 64-element aligned offsets) so the
+    # unfused baseline can hand all gradients to ONE NCCL all_reduce
+    from paper_2105_05720_b200.runtime import SymmBuffer
+    flat_g = ctx.alloc([sum(padded)], torch.float16)
+    flat_p = ctx.alloc([sum(padded)], torch.float32)
+    grads, params, off = [], [], 0
+    for n, pn in zip(counts, padded):
+        grads.append(SymmBuffer(flat_g.offset + off * 2, (n,), torch.float16))
+        params.append(SymmBuffer(flat_p.offset + off * 4, (n,), torch.float32))
+        off += pn
     m = ctx.alloc([tl.shard_elems], torch.float32)
     v = ctx.alloc([tl.shard_elems], torch.float32)
     my_ranks = ctx.local_ranks()
@@ -252,6 +260,41 @@ def run_coconet(args):
         ms = max_over_ranks(ms)
     N = BERT_LARGE_PARAMS
     value = W * N / (ms * 1e-3) / 1e9
+
+    # -- the unfused GPU baseline (north star): NCCL all_reduce of the flat
+    # fp16 gradients, then a separate LAMB over ALL elements on every rank
+    # (replicated state, DDP + fused-optimizer style), on the same box
+    nccl_baseline = None
+    if distributed and not share:
+        try:  # the baseline is reported, never allowed to sink the bench line
+            g1 = ctx.group(rank, 1)
+            tl1 = TensorList(ctx, counts, group=g1, bucket_cap=BUCKET_CAP)
+            m1 = ctx.alloc([tl1.shard_elems], torch.float32)
+            v1 = ctx.alloc([tl1.shard_elems], torch.float32)
+            ctx.view(m1).zero_()
+            ctx.view(v1).fill_(1e-4)
+            flat = ctx.view(flat_g)
+
+            def base_step():
+                dist.all_reduce(flat)
+                fused_rs_lamb_ag(ctx, tl1, grads, params, m1, v1, hp)
+
+            for _ in range(args.warmup):
+                base_step()
+            barrier()
+            b0 = torch.cuda.Event(enable_timing=True)
+            b1 = torch.cuda.Event(enable_timing=True)
+            b0.record(stream)
+            for _ in range(args.steps):
+                base_step()
+            b1.record(stream)
+            barrier()
+            bms = max_over_ranks(b0.elapsed_time(b1) / args.steps)
+            nccl_baseline = {"ms_per_step": bms, "value": W * N / (bms * 1e-3) / 1e9, "unit": UNIT,
+                             "what": "NCCL all_reduce (fp16, flat) + separate LAMB over all elements per rank",
+                             "speedup_of_fused": bms / ms}
+        except Exception as e:
+            nccl_baseline = {"failed": repr(e)}
 
     # -- e2e: through the public API with HOST buffers (pinned), H2D of the
     # step's gradients and D2H of the updated parameters inside the timed region
@@ -347,6 +390,7 @@ def run_coconet(args):
             "gpu_launches": launches, "clocks": clocks,
             "kernel_ms": ms,
             "extras": extras,
+            "nccl_baseline": nccl_baseline,
         }
         print(json.dumps(line))
     if ctx.handle:
