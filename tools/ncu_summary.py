@@ -69,7 +69,7 @@ def summarize_launches(path: Path):
     for r in rows[start + 1:]:
         if len(r) > iv and r[im] == "gpu__time_duration.sum":
             v = float(r[iv].replace(",", ""))
-            scale = {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3}.get(r[iu], 1.0)
+            scale = {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3}[r[iu]]
             per[r[ik]].append(v * scale)
     total = sum(sum(v) for v in per.values()) or 1.0
     return {"total_us": total, "kernels": sorted(
