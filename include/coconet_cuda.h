@@ -154,6 +154,12 @@ int64_t coconet_tlist_segments(coconet_tlist_t tl, int r, int64_t* tensor, int64
                                int64_t* len, int64_t* sidx, int64_t cap);
 /* Shard index of flat position `pos` inside its owner's shard storage. */
 int64_t coconet_tlist_shard_index(coconet_tlist_t tl, int64_t pos);
+/* STREAMED-LAMB work list of rank r for a pass-1 -> pass-2 lag of `lag`
+ * elements (see coconet_lamb_sched): items in execution order with their pass
+ * (0/1). Host-only (works on a plan-only list). Returns the item count,
+ * -count if cap is too small, -(2^62) on error. */
+int64_t coconet_tlist_stream_items(coconet_tlist_t tl, int64_t lag, int r, int64_t* tensor,
+                                   int64_t* toff, int64_t* len, int64_t* pass, int64_t cap);
 
 /* ---- fused data-parallel optimizer: FusedAllReduce (runtime.hpp:471-516) -- */
 /* Adam step of goldens/adam.json under schedules/adam_fused.json:
@@ -191,8 +197,19 @@ int coconet_fused_rs_adam_ag(coconet_ctx_t ctx, coconet_tlist_t tl, const void* 
  * the same kernel (K12). */
 typedef struct {
   float lr, beta1, beta2, t, eps, wd;
-  int math; /* FAST only for now (EXACT is rejected: sums cannot match bit-wise) */
+  int math;  /* FAST only for now (EXACT is rejected: sums cannot match bit-wise) */
+  int sched; /* coconet_lamb_sched; both give bit-identical results */
+  int64_t lag_elems; /* STREAMED: pass-1 -> pass-2 distance in elements (0 = default) */
 } coconet_lamb_params;
+
+/* LAMB schedules (bit-identical results). GRID: pass 1 over the whole shard,
+ * grid-wide sync, norms, pass 2 over the whole shard (m, v, p read twice
+ * from HBM: 38 B/element at fp16 g). STREAMED: the shard's segments in tensor
+ * order, one small CTA per segment; a tensor's pass 2 is scheduled lag_elems
+ * of pass-1 work after its pass 1 and waits only on that tensor's norms
+ * (per-tensor completion counters, cross-rank ready flags), so part of its
+ * m, v, p re-reads hit L2. AUTO = GRID, measured faster on B200. */
+enum coconet_lamb_sched { COCONET_LAMB_AUTO = 0, COCONET_LAMB_GRID = 1, COCONET_LAMB_STREAMED = 2 };
 
 int coconet_fused_rs_lamb_ag(coconet_ctx_t ctx, coconet_tlist_t tl, const void* const* g,
                              int g_elem, float* const* p, float* m_shard, float* v_shard,

@@ -16,6 +16,7 @@ F32, F16, BF16 = 0, 1, 2
 SUM, MAX, MIN = 0, 1, 2
 MATH_EXACT, MATH_FAST = 0, 1
 ALGO_AUTO, ALGO_TWO_SHOT, ALGO_ONE_SHOT = 0, 1, 2
+LAMB_AUTO, LAMB_GRID, LAMB_STREAMED = 0, 1, 2
 MODE_VIRTUAL, MODE_DISTRIBUTED = 0, 1
 MAX_RANKS = 8
 
@@ -50,7 +51,8 @@ class AdamParams(C.Structure):
 
 class LambParams(C.Structure):
     _fields_ = [("lr", C.c_float), ("beta1", C.c_float), ("beta2", C.c_float), ("t", C.c_float),
-                ("eps", C.c_float), ("wd", C.c_float), ("math", C.c_int)]
+                ("eps", C.c_float), ("wd", C.c_float), ("math", C.c_int), ("sched", C.c_int),
+                ("lag_elems", C.c_int64)]
 
 
 class BdrParams(C.Structure):
@@ -93,6 +95,7 @@ _SIGNATURES = {
     "coconet_tlist_chunk": (_I, [_P, _I, _PI64, _PI64]),
     "coconet_tlist_shard_index": (_I64, [_P, _I64]),
     "coconet_tlist_segments": (_I64, [_P, _I, _PI64, _PI64, _PI64, _PI64, _I64]),
+    "coconet_tlist_stream_items": (_I64, [_P, _I64, _I, _PI64, _PI64, _PI64, _PI64, _I64]),
     "coconet_fused_rs_adam_ag": (_I, [_P, _P, _PP, _I, _PP, _P, _P, C.POINTER(AdamParams), _P]),
     "coconet_fused_rs_lamb_ag": (_I, [_P, _P, _PP, _I, _PP, _P, _P, C.POINTER(LambParams), _P]),
     "coconet_allreduce": (_I, [_P, _P, _PP, _PP, _I, _I, _I, _P]),

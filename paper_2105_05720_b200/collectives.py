@@ -69,6 +69,15 @@ class TensorList:
         check(0 if got >= 0 else 3)
         return np.stack([np.frombuffer(b, dtype=np.int64)[:got] for b in bufs], axis=1)
 
+    def stream_items(self, lag: int, r: int) -> np.ndarray:
+        """[n, 4] int64 (tensor, toff, len, pass) of rank r's STREAMED-LAMB work
+        list for a pass-1 -> pass-2 lag of `lag` elements, in execution order."""
+        n = 2 * (self.n_buckets + 16 * _lib.MAX_RANKS)
+        bufs = [(C.c_int64 * n)() for _ in range(4)]
+        got = int(self.lib.coconet_tlist_stream_items(self.handle, int(lag), r, *bufs, n))
+        check(0 if got >= 0 else 3)
+        return np.stack([np.frombuffer(b, dtype=np.int64)[:got] for b in bufs], axis=1)
+
     def state_index_map(self, r: int):
         """(tensor, element, state index) arrays of every element rank r owns."""
         segs = self.segments(r)
@@ -120,6 +129,8 @@ class LambHParams:
     eps: float = 1e-6
     wd: float = 0.01
     math: int = _lib.MATH_FAST
+    sched: int = _lib.LAMB_AUTO   # GRID or STREAMED (L2-resident pass 2); results are bit-identical
+    lag_elems: int = 0            # STREAMED: pass-1 -> pass-2 distance in elements (0 = library default)
 
 
 def fused_rs_adam_ag(ctx: Context, tl: TensorList, grads, params, m: SymmBuffer, v: SymmBuffer,
@@ -135,7 +146,7 @@ def fused_rs_adam_ag(ctx: Context, tl: TensorList, grads, params, m: SymmBuffer,
 def fused_rs_lamb_ag(ctx: Context, tl: TensorList, grads, params, m: SymmBuffer, v: SymmBuffer,
                      hp: LambHParams, stream=None) -> None:
     g_elem = elem_of(grads[0].dtype)
-    p = _lib.LambParams(hp.lr, hp.beta1, hp.beta2, hp.t, hp.eps, hp.wd, hp.math)
+    p = _lib.LambParams(hp.lr, hp.beta1, hp.beta2, hp.t, hp.eps, hp.wd, hp.math, hp.sched, hp.lag_elems)
     check(ctx.lib.coconet_fused_rs_lamb_ag(
         ctx.handle, tl.handle, _ptrs(ctx, grads), g_elem, _ptrs(ctx, params), ctx.ptr(m), ctx.ptr(v),
         C.byref(p), ctx.stream_ptr(stream)))

@@ -134,20 +134,22 @@ struct SegD {
   int len, owner, tensor;
 };
 
-// Iterates this warp's segments [s, se) with stride `st`, prefetching the
-// descriptor two segments ahead and the tensor offsets one ahead:
-//   for (SegIter it(...); it.valid(); it.next()) { SegD d = it.get(); ... }
+// Iterates this warp's descriptors [s, se) with stride `st` (D = Seg, or Item
+// for the STREAMED schedule), prefetching the descriptor two ahead and the
+// tensor offsets one ahead:
+//   for (DescIter<Seg> it(...); it.valid(); it.next()) { SegD d = it.get(); ... }
 // (no lambdas: capturing kernel parameters by reference spills them).
-struct SegIter {
-  const Seg* segs;
+template <typename D>
+struct DescIter {
+  const D* segs;
   const int64_t* offs;
   int n;
   int64_t s, se, st;
-  Seg d1, d2, d3;
+  D d1, d2, d3;
   int64_t a1, b1, a2, b2;
 
-  __device__ __forceinline__ SegIter(const Seg* segs_, const int64_t* offs_, int n_, int64_t s_, int64_t se_,
-                                     int64_t st_)
+  __device__ __forceinline__ DescIter(const D* segs_, const int64_t* offs_, int n_, int64_t s_, int64_t se_,
+                                      int64_t st_)
       : segs(segs_), offs(offs_), n(n_), s(s_), se(se_), st(st_) {
     if (s < se) {
       d1 = segs[s];
@@ -164,6 +166,9 @@ struct SegIter {
   }
   __device__ __forceinline__ bool valid() const { return s < se; }
   __device__ __forceinline__ int64_t index() const { return s; }
+  __device__ __forceinline__ const D& raw() const { return d1; }
+  __device__ __forceinline__ bool has_next() const { return s + st < se; }
+  __device__ __forceinline__ const D& peek() const { return d2; }  // next descriptor (valid if has_next)
   __device__ __forceinline__ SegD get() const {
     return SegD{d1.toff, d1.sidx, a1, b1, meta_len(d1.meta), meta_owner(d1.meta), meta_tensor(d1.meta)};
   }
@@ -176,6 +181,7 @@ struct SegIter {
     if (s < se) prefetch();
   }
 };
+using SegIter = DescIter<Seg>;
 
 __device__ __forceinline__ void quad_range(const SegD& d, int64_t e0, int& lo, int& hi) {
   lo = int(max(int64_t(0), d.toff - e0));
@@ -490,6 +496,303 @@ __global__ void __launch_bounds__(kThreads, MINB) lamb_kernel(OptArgs a, LambK k
   rank_barrier(rs, 1);
 }
 
+// STREAMED-LAMB bookkeeping (tlist_stream_plan).
+struct LambS {
+  const Item* items;
+  const int64_t* p1_first;  // [rank][tensor]
+  const uint32_t* holders;  // [tensor] rank bitmask
+  uint32_t* cnt;            // [rank][tensor] pass-1 completion counters
+  double* part;             // [item] sum p^2, sum u^2 (pass-1 items)
+  int64_t item_begin[kMaxRanks + 1];
+  int64_t rdy_off;          // ready flags [src rank][tensor] in the group area
+  uint32_t call;            // launches of this schedule so far, this one included
+};
+
+// Sum of n (p^2, u^2) pairs at part[2*first ...], lane-strided in list order
+// then a butterfly: the same additions, in the same order, as the GRID
+// kernel's CSR walk (the pass-1 items of a tensor are its CSR list), so both
+// schedules produce bit-identical norms.
+__device__ __forceinline__ void reduce_parts(const double* part, int64_t first, int64_t n, int lane,
+                                             double& P, double& Uu) {
+  P = 0.0;
+  Uu = 0.0;
+  int64_t i = lane;
+  for (; i + 96 < n; i += 128) {  // four independent 16-byte loads in flight per lane
+    double2 x[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) x[j] = __ldcg(reinterpret_cast<const double2*>(part + 2 * (first + i + 32 * j)));
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      P += x[j].x;
+      Uu += x[j].y;
+    }
+  }
+  for (; i < n; i += 32) {
+    const double2 x = __ldcg(reinterpret_cast<const double2*>(part + 2 * (first + i)));
+    P += x.x;
+    Uu += x.y;
+  }
+  P = warp_sum(P);
+  Uu = warp_sum(Uu);
+}
+
+__device__ __forceinline__ void fence_acq_rel_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
+
+// Per-CTA state of the STREAMED kernel that lives in shared memory.
+struct StreamSmem {
+  // speculative norms of upcoming pass-2 items, 3 slots by item parity mod 3
+  // (a slot is rewritten two items after it was read; each item has a barrier)
+  double2 spec[3][kMaxRanks];
+  int rdy[3][kMaxRanks];
+};
+
+// Warp 0 of a STREAMED CTA: publish the pending pass-1 completion of tensor t
+// (fence + per-tensor counter). Returns (warp-uniform) whether this CTA
+// completed the tensor and must run stream_reduce for it.
+__device__ __forceinline__ bool stream_count(uint32_t* cnt, uint32_t call, int64_t nseg, int t) {
+  int last = 0;
+  if ((threadIdx.x & 31) == 0) {
+    fence_acq_rel_gpu();  // this CTA's m, v and partial (ordered by the barrier) before the count
+    const uint32_t old = atomicAdd(cnt + t, 1u);
+    last = old + 1u == call * uint32_t(nseg);
+  }
+  return __shfl_sync(0xffffffffu, last, 0) != 0;
+}
+
+// Warp 0 of the CTA that completed tensor t: reduce its pass-1 partials in
+// list order and push them, with a ready flag, to every peer. Runs between
+// items (no data registers live).
+__device__ __noinline__ void stream_reduce(char* const* s_base, const double* part, int64_t first, int64_t nseg,
+                                           int64_t xch_off, int64_t rdy_off, uint32_t epoch, int n, int W, int me,
+                                           int t) {
+  const int lane = threadIdx.x & 31;
+  fence_acq_rel_gpu();
+  double P, Uu;
+  reduce_parts(part, first, nseg, lane, P, Uu);
+  if (lane < W) {
+    double* xq = reinterpret_cast<double*>(s_base[lane] + xch_off);
+    *reinterpret_cast<double2*>(xq + (int64_t(me) * n + t) * 2) = make_double2(P, Uu);
+    __threadfence_system();
+    st_release_sys(reinterpret_cast<uint32_t*>(s_base[lane] + xch_off + rdy_off) + int64_t(me) * n + t, epoch);
+  }
+}
+
+// Threads 32 + q (q < W, warp 1: warp 0 is busy publishing counts) of a
+// STREAMED CTA: non-blocking readiness check and (P, U) partials of rank q
+// for tensor t, into speculation slot `sl`.
+__device__ __forceinline__ void stream_speculate(StreamSmem& ss, const LambS& ls, const uint32_t* rdy_me,
+                                              const double* xch_me, uint32_t epoch, int n, int t, int sl) {
+  const int q = threadIdx.x - 32;
+  int r = 1;
+  double2 x = make_double2(0.0, 0.0);
+  if ((ls.holders[t] >> q) & 1u) {
+    r = int32_t(ld_acquire_sys(rdy_me + int64_t(q) * n + t) - epoch) >= 0;
+    if (r) x = __ldcg(reinterpret_cast<const double2*>(xch_me + (int64_t(q) * n + t) * 2));
+  }
+  ss.spec[sl][q] = x;
+  ss.rdy[sl][q] = r;
+}
+
+// LAMB, STREAMED schedule (coconet_lamb_sched): one persistent cooperative
+// grid walks the rank's item list (tlist_stream_plan's order), ONE CTA PER
+// ITEM, so only gridDim.x items (~1.2M elements) are in flight at once and a
+// pass-2 item is never dequeued before its tensor's pass 1 is done.
+//  pass-1 item: RS pull -> m, v update -> per-quad (p^2, u^2) partials in smem,
+//    summed by warp 0 in the GRID kernel's lane order (lane l: quads l+32j, j
+//    ascending, then a butterfly), so the segment partial is bit-identical.
+//    Its completion (fence + per-tensor counter) is published by warp 0 one
+//    item LATER, after that item's loads are in flight; the CTA that
+//    completes a tensor reduces its partials in list order and pushes them,
+//    with a ready flag, to every peer;
+//  pass-2 item: its tensor's ready flags and (P, U) partials were read
+//    speculatively while the previous item's loads were in flight (a blocking
+//    wait only if they were not ready yet); combined in rank order
+//    (state.hpp:163-167) -> trust ratio -> p update -> AG push. Its m, v, p
+//    were touched `lag` elements earlier, so the re-reads hit L2, not HBM.
+template <typename G, int WT, int NT, int U>
+__global__ void __launch_bounds__(NT, 512 / NT) lamb_stream_kernel(OptArgs a, LambK k, LambS ls) {
+  constexpr int kChunkQuads = NT * U;  // quads per CTA sweep (NT * U = 256: 1024 elements)
+  __shared__ char* s_base[kMaxRanks];
+  __shared__ float2 s_part[kChunkQuads];
+  __shared__ StreamSmem ss;
+  const RankSet& rs = a.rs;
+  if (threadIdx.x < kMaxRanks) s_base[threadIdx.x] = threadIdx.x < rs.world ? rs.base[threadIdx.x] : nullptr;
+  const int W = WT > 0 ? WT : rs.world;
+  const int me = rs.rank();
+  const bool ok = rank_barrier(rs, 0);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int n = a.n_tensors;
+  const int64_t ib = ls.item_begin[me], ie = ok ? ls.item_begin[me + 1] : ib;
+  float* m = reinterpret_cast<float*>(s_base[me] + a.m_off);
+  float* v = reinterpret_cast<float*>(s_base[me] + a.v_off);
+  const char* pme = s_base[me];
+  const int64_t* ptr = k.csr_ptr + k.csr_begin[me];
+  uint32_t* cnt = ls.cnt + int64_t(me) * n;
+  const int64_t* p1_first = ls.p1_first + int64_t(me) * n;
+  const int64_t xch_off = int64_t(group_area(rs.group));
+  const double* xch_me = reinterpret_cast<const double*>(s_base[me] + xch_off);
+  const uint32_t* rdy_me = reinterpret_cast<const uint32_t*>(s_base[me] + xch_off + ls.rdy_off);
+  int pend_t = -1;  // warp 0: pass-1 item whose completion is not yet published
+  int red_t = -1;   // warp 0: tensor this CTA completed, to reduce after the item
+  int slot = 0;  // this item's speculation slot
+  if (tid < W) ss.rdy[0][tid] = 0;  // the first item is never speculated
+  static_assert(NT >= 64, "speculation runs on warp 1");
+  for (DescIter<Item> it(ls.items, a.offs, n, ib + blockIdx.x, ie, gridDim.x); it.valid(); it.next()) {
+    const SegD d = it.get();
+    const int t = d.tensor;
+    const int nslot = slot == 2 ? 0 : slot + 1;
+    const bool spec_next = it.has_next() && meta_pass(it.peek().meta) == 1;
+    const int64_t q0 = d.toff >> 2, q1 = (d.toff + d.len + 3) >> 2;
+    if (meta_pass(it.raw().meta) == 0) {
+      float sp = 0.f, su = 0.f;  // warp 0's lane accumulators (GRID order)
+      for (int64_t qc = q0; qc < q1; qc += kChunkQuads) {
+        float g[U][Ranks<WT>::kMax][4], mm[U][4], vv[U][4], pp[U][4];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int64_t q = min(qc + tid + NT * u, q1 - 1);  // clamped, unconditional loads
+          const int64_t e0 = q << 2;
+          const int64_t si = d.sidx + (e0 - d.toff);
+          ring_load4<G, COCONET_SUM, WT>(s_base, d.aoff + e0 * int64_t(sizeof(G)), me, W, g[u]);
+          ld4(m + si, mm[u]);
+          ld4(v + si, vv[u]);
+          ld4(reinterpret_cast<const float*>(pme + d.boff) + e0, pp[u]);
+        }
+        if (qc == q0) {  // overlap the previous item's publish and the next item's speculation
+          if (warp == 0 && pend_t >= 0) {
+            if (stream_count(cnt, ls.call, ptr[pend_t + 1] - ptr[pend_t], pend_t)) red_t = pend_t;
+            pend_t = -1;
+          }
+          if (spec_next && tid >= 32 && tid < 32 + W) stream_speculate(ss, ls, rdy_me, xch_me, rs.epoch, n, meta_tensor(it.peek().meta), nslot);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int64_t q = qc + tid + NT * u;
+          float fp = 0.f, fu = 0.f;
+          if (q < q1) {
+            const int64_t e0 = q << 2;
+            int lo, hi;
+            quad_range(d, e0, lo, hi);
+            const int64_t si = d.sidx + (e0 - d.toff);
+            float gs[4];
+            ring_fold4<COCONET_SUM, WT>(g[u], W, gs);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              const float mn = fmaf(k.fcm, gs[i], mm[u][i] * k.fb1);
+              const float vn = fmaf(k.fcv * gs[i], gs[i], vv[u][i] * k.fb2);
+              mm[u][i] = mn;
+              vv[u][i] = vn;
+              if (i >= lo && i < hi) {
+                const float uu = lamb_u(mn, vn, pp[u][i], k);
+                fp = fmaf(pp[u][i], pp[u][i], fp);
+                fu = fmaf(uu, uu, fu);
+              }
+            }
+            st4m(m + si, mm[u], lo, hi);
+            st4m(v + si, vv[u], lo, hi);
+          }
+          s_part[tid + NT * u] = make_float2(fp, fu);  // +0.0 past the end: no effect
+        }
+        __syncthreads();
+        if (warp == 0) {
+          const int nq = int(min(int64_t(kChunkQuads), q1 - qc));
+          for (int j = lane; j < nq; j += 32) {
+            const float2 x = s_part[j];
+            sp += x.x;
+            su += x.y;
+          }
+        }
+        __syncthreads();
+      }
+      if (warp == 0) {
+        sp = warp_sumf(sp);
+        su = warp_sumf(su);
+        if (lane == 0)
+          *reinterpret_cast<double2*>(ls.part + 2 * it.index()) = make_double2(double(sp), double(su));
+        pend_t = t;
+      }
+    } else {
+      __syncthreads();  // this item's speculation slot is visible
+      bool ready = true;
+#pragma unroll
+      for (int q = 0; q < Ranks<WT>::kMax; ++q)
+        if (Ranks<WT>::has(q, W)) ready &= ss.rdy[slot][q] != 0;
+      const double2* xs = ss.spec[slot];  // the rank partials: speculated, or filled below
+      if (!ready) {  // rare: block on the flags BEFORE loading m, v (pass 1 may still be writing them)
+        if (warp == 0 && pend_t >= 0) {  // we may hold the count it needs ...
+          if (stream_count(cnt, ls.call, ptr[pend_t + 1] - ptr[pend_t], pend_t)) red_t = pend_t;
+          pend_t = -1;
+        }
+        if (warp == 0 && red_t >= 0) {  // ... or the reduction
+          stream_reduce(s_base, ls.part, p1_first[red_t], ptr[red_t + 1] - ptr[red_t], xch_off, ls.rdy_off,
+                        rs.epoch, n, W, me, red_t);
+          red_t = -1;
+        }
+        bool okw = true;
+        if (tid < W && ((ls.holders[t] >> tid) & 1u)) okw = wait_flag(rdy_me + int64_t(tid) * n + t, rs.epoch, rs);
+        if (tid < W)
+          ss.spec[slot][tid] = ((ls.holders[t] >> tid) & 1u) && okw
+                                   ? __ldcg(reinterpret_cast<const double2*>(xch_me + (int64_t(tid) * n + t) * 2))
+                                   : make_double2(0.0, 0.0);
+        if (!__syncthreads_and(okw)) break;  // watchdog fired: skip, never hang
+      }
+      for (int64_t qc = q0; qc < q1; qc += kChunkQuads) {
+        float mm[U][4], vv[U][4], pp[U][4];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int64_t q = min(qc + tid + NT * u, q1 - 1);
+          const int64_t e0 = q << 2;
+          const int64_t si = d.sidx + (e0 - d.toff);
+          load4_cg(m + si, mm[u]);
+          load4_cg(v + si, vv[u]);
+          load4_cg(reinterpret_cast<const float*>(pme + d.boff) + e0, pp[u]);
+        }
+        if (qc == q0) {
+          if (warp == 0 && pend_t >= 0) {
+            if (stream_count(cnt, ls.call, ptr[pend_t + 1] - ptr[pend_t], pend_t)) red_t = pend_t;
+            pend_t = -1;
+          }
+          if (spec_next && tid >= 32 && tid < 32 + W) stream_speculate(ss, ls, rdy_me, xch_me, rs.epoch, n, meta_tensor(it.peek().meta), nslot);
+        }
+        double P = 0.0, Uu = 0.0;
+#pragma unroll
+        for (int q = 0; q < Ranks<WT>::kMax; ++q)  // rank order 0..W-1; non-holders add +0.0
+          if (Ranks<WT>::has(q, W)) {
+            P += xs[q].x;
+            Uu += xs[q].y;
+          }
+        const float ratio = float((k.lr * sqrt(P)) / sqrt(Uu));
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int64_t q = qc + tid + NT * u;
+          if (q < q1) {
+            const int64_t e0 = q << 2;
+            int lo, hi;
+            quad_range(d, e0, lo, hi);
+            float pn[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) pn[i] = pp[u][i] - ratio * lamb_u(mm[u][i], vv[u][i], pp[u][i], k);
+#pragma unroll
+            for (int j = 0; j < Ranks<WT>::kMax; ++j)
+              if (Ranks<WT>::has(j, W)) st4m(reinterpret_cast<float*>(s_base[j] + d.boff) + e0, pn, lo, hi);
+          }
+        }
+      }
+    }
+    if (warp == 0 && red_t >= 0) {
+      stream_reduce(s_base, ls.part, p1_first[red_t], ptr[red_t + 1] - ptr[red_t], xch_off, ls.rdy_off, rs.epoch,
+                    n, W, me, red_t);
+      red_t = -1;
+    }
+    slot = nslot;
+  }
+  if (warp == 0 && pend_t >= 0) {
+    if (stream_count(cnt, ls.call, ptr[pend_t + 1] - ptr[pend_t], pend_t))
+      stream_reduce(s_base, ls.part, p1_first[pend_t], ptr[pend_t + 1] - ptr[pend_t], xch_off, ls.rdy_off,
+                    rs.epoch, n, W, me, pend_t);
+  }
+  rank_barrier(rs, 1);
+}
+
 int fill_args(coconet_tlist* tl, OptArgs* a, const RankSet& rs, int64_t m_off, int64_t v_off) {
   a->rs = rs;
   a->segs = tl->d_segs;
@@ -595,6 +898,22 @@ const void* lamb_pick(int W) {
   }
 }
 
+template <typename G>
+const void* lamb_stream_pick(int W) {
+  switch (W) {
+    case 1: return reinterpret_cast<const void*>(&lamb_stream_kernel<G, 1, 64, 4>);
+    case 2: return reinterpret_cast<const void*>(&lamb_stream_kernel<G, 2, 128, 2>);
+    case 4: return reinterpret_cast<const void*>(&lamb_stream_kernel<G, 4, 128, 2>);
+    case 8: return reinterpret_cast<const void*>(&lamb_stream_kernel<G, 8, 256, 1>);
+    default: return reinterpret_cast<const void*>(&lamb_stream_kernel<G, 0, 256, 1>);
+  }
+}
+
+// Default STREAMED lag: 2^21 elements (m, v, p = 24 MB): covers the grid's
+// in-flight window (2 CTAs x 148 SMs x 4096-element items = 1.2M elements)
+// while tensor + lag stay inside the 126 MB L2 for tensors up to ~4M.
+constexpr int64_t kDefaultLag = int64_t(1) << 21;
+
 int check_state(coconet_ctx* c, const void* ptr, int64_t* off) {
   int rc = heap_offset(c, ptr, off);
   if (rc) return rc;
@@ -660,7 +979,10 @@ int coconet_fused_rs_lamb_ag(coconet_ctx_t c, coconet_tlist_t tl, const void* co
     return set_error(COCONET_ERR_UNSUPPORTED,
                      "LAMB runs in FAST math only: its whole-tensor sums cannot reproduce the "
                      "reference's sequential double accumulation bit-for-bit");
-  if (size_t(kMaxRanks) * tl->n_tensors * 2 * sizeof(double) > kTileFlagsOff)
+  if (hp->sched < COCONET_LAMB_AUTO || hp->sched > COCONET_LAMB_STREAMED)
+    return set_error(COCONET_ERR_INVALID_INPUT, "bad LAMB schedule");
+  // exchange [rank][tensor] (P, U) doubles + ready flags [rank][tensor]
+  if (size_t(kMaxRanks) * tl->n_tensors * (2 * sizeof(double) + sizeof(uint32_t)) > kTileFlagsOff)
     return set_error(COCONET_ERR_UNSUPPORTED, "too many tensors for the exchange area");
   cudaStream_t stream = static_cast<cudaStream_t>(stream_);
   const int W = c->groups[size_t(tl->group)].size;
@@ -688,11 +1010,39 @@ int coconet_fused_rs_lamb_ag(coconet_ctx_t c, coconet_tlist_t tl, const void* co
   if (rc) return rc;
   OptArgs a;
   fill_args(tl, &a, rs, m_off, v_off);
-  const void* fn = g_elem == COCONET_F32   ? lamb_pick<float>(W)
-                   : g_elem == COCONET_F16 ? lamb_pick<__half>(W)
-                                           : lamb_pick<__nv_bfloat16>(W);
-  void* args[] = {&a, &k};
-  return launch_opt(c, tl, fn, args, false, stream);
+  // AUTO = GRID: measured faster on B200 ("STREAMED schedule")
+  if (hp->sched != COCONET_LAMB_STREAMED) {
+    const void* fn = g_elem == COCONET_F32   ? lamb_pick<float>(W)
+                     : g_elem == COCONET_F16 ? lamb_pick<__half>(W)
+                                             : lamb_pick<__nv_bfloat16>(W);
+    void* args[] = {&a, &k};
+    return launch_opt(c, tl, fn, args, false, stream);
+  }
+  // STREAMED (default)
+  const int64_t lag = hp->lag_elems > 0 ? hp->lag_elems : kDefaultLag;
+  rc = tlist_stream_plan(tl, lag);
+  if (rc) return rc;
+  LambS ls;
+  ls.items = tl->d_items;
+  ls.p1_first = tl->d_p1_first;
+  ls.holders = tl->d_holders;
+  ls.cnt = tl->d_cnt;
+  ls.part = tl->d_item_part;
+  for (int r = 0; r <= kMaxRanks; ++r) ls.item_begin[r] = r <= W ? tl->item_begin[r] : 0;
+  ls.rdy_off = int64_t(kMaxRanks) * tl->n_tensors * 2 * int64_t(sizeof(double));
+  ls.call = ++tl->stream_calls;
+  const void* fn = g_elem == COCONET_F32   ? lamb_stream_pick<float>(W)
+                   : g_elem == COCONET_F16 ? lamb_stream_pick<__half>(W)
+                                           : lamb_stream_pick<__nv_bfloat16>(W);
+  void* args[] = {&a, &k, &ls};
+  int64_t most = 0;
+  for (int r = 0; r < W; ++r) most = std::max(most, tl->item_begin[r + 1] - tl->item_begin[r]);
+  int blocks = 0;
+  const int nt = W == 1 ? 64 : (W == 2 || W == 4) ? 128 : 256;  // lamb_stream_pick's CTA sizes
+  rc = coop_blocks(c, fn, nt, 0, tl->group, most, &blocks);
+  if (rc) return rc;
+  return coop_launch(c, fn, dim3(unsigned(blocks), unsigned(local_ranks(c, tl->group))), dim3(unsigned(nt)),
+                     args, 0, stream);
 }
 
 int coconet_allreduce(coconet_ctx_t c, coconet_tlist_t tl, const void* const* x, void* const* out,

@@ -15,12 +15,19 @@ struct Seg {
   int64_t meta;  // tensor (32 bits) | len (24 bits) | owner rank (8 bits)
 };
 
+// One STREAMED-LAMB work item: a segment whose meta carries its pass in bit 7
+// of the owner byte (0: RS + m/v update + norm partials, 1: trust ratio +
+// p update + AG); the owner of a TWO_SHOT segment is the rank itself.
+using Item = Seg;
+constexpr int64_t kPass2Bit = 0x80;
+
 __host__ __device__ __forceinline__ int64_t pack_meta(int tensor, int len, int owner) {
   return (int64_t(tensor) << 32) | (int64_t(len & 0xffffff) << 8) | int64_t(owner & 0xff);
 }
 __host__ __device__ __forceinline__ int meta_tensor(int64_t m) { return int(m >> 32); }
 __host__ __device__ __forceinline__ int meta_len(int64_t m) { return int((m >> 8) & 0xffffff); }
-__host__ __device__ __forceinline__ int meta_owner(int64_t m) { return int(m & 0xff); }
+__host__ __device__ __forceinline__ int meta_owner(int64_t m) { return int(m & 0x7f); }
+__host__ __device__ __forceinline__ int meta_pass(int64_t m) { return (m & kPass2Bit) ? 1 : 0; }
 
 }  // namespace coconet
 
@@ -51,9 +58,25 @@ struct coconet_tlist {
   int64_t* d_csr_idx = nullptr;
   int64_t* d_offs = nullptr;       // [2][n_tensors] heap offsets bound per call
   double* d_seg_part = nullptr;    // per-segment partial sums (LAMB)
+  // STREAMED LAMB schedule (built on first use for a lag, tlist_stream_plan)
+  int64_t stream_wave = -1;              // the lag the lists were built for
+  int64_t item_begin[coconet::kMaxRanks + 1] = {};
+  std::vector<coconet::Item> items;      // per rank, execution order (tlist_stream_plan)
+  std::vector<int64_t> p1_first;         // [rank][tensor]: item index of the tensor's first pass-1 item
+  std::vector<uint32_t> holders;         // [tensor]: bitmask of ranks holding segments of it
+  void* stream_mem = nullptr;
+  coconet::Item* d_items = nullptr;
+  int64_t* d_p1_first = nullptr;
+  uint32_t* d_holders = nullptr;
+  uint32_t* d_cnt = nullptr;             // [rank][tensor] pass-1 completion counters
+  double* d_item_part = nullptr;         // per pass-1 item: sum p^2, sum u^2
+  uint32_t stream_calls = 0;
 };
 
 namespace coconet {
+// Builds (or keeps) the STREAMED-LAMB work lists for a pass-1 -> pass-2 lag
+// of `lag` elements; uploads them when the list has a device table.
+int tlist_stream_plan(coconet_tlist* tl, int64_t lag);
 int tlist_bind(coconet_tlist* tl, const void* const* a, const void* const* b, int a_elem_bytes,
                int b_elem_bytes, cudaStream_t stream);
 }

@@ -212,10 +212,9 @@ int coconet_tlist_plan(int world, int n_tensors, const int64_t* counts, int64_t 
 
 int coconet_tlist_destroy(coconet_tlist_t tl) {
   if (!tl) return COCONET_OK;
-  if (tl->dev_mem) {
-    cudaDeviceSynchronize();
-    cudaFree(tl->dev_mem);
-  }
+  if (tl->dev_mem || tl->stream_mem) cudaDeviceSynchronize();
+  if (tl->dev_mem) cudaFree(tl->dev_mem);
+  if (tl->stream_mem) cudaFree(tl->stream_mem);
   delete tl;
   return COCONET_OK;
 }
@@ -259,9 +258,123 @@ int64_t coconet_tlist_segments(coconet_tlist_t tl, int r, int64_t* tensor, int64
   return e - b;
 }
 
+int64_t coconet_tlist_stream_items(coconet_tlist_t tl, int64_t lag, int r, int64_t* tensor,
+                                   int64_t* toff, int64_t* len, int64_t* pass, int64_t cap) {
+  if (!tl) return set_error(COCONET_ERR_INVALID_INPUT, "null tlist");
+  if (r < 0 || r >= tl->world) return set_error(COCONET_ERR_NO_SUCH_RANK, "rank out of range");
+  int rc = tlist_stream_plan(tl, lag);
+  if (rc) return -(int64_t(1) << 62);  // message in coconet_last_error
+  const int64_t b = tl->item_begin[r], e = tl->item_begin[r + 1];
+  if (e - b > cap) return -(e - b);
+  for (int64_t i = 0; i < e - b; ++i) {
+    const Item& it = tl->items[size_t(b + i)];
+    tensor[i] = meta_tensor(it.meta);
+    toff[i] = it.toff;
+    len[i] = meta_len(it.meta);
+    pass[i] = meta_pass(it.meta);
+  }
+  return e - b;
+}
+
 }  // extern "C"
 
 namespace coconet {
+
+// STREAMED-LAMB work lists. One GLOBAL sequence of groups (pass, tensor) is
+// built from the tensors' largest per-rank share (so it is identical on every
+// rank): pass-1 groups in tensor order, and the pass-2 group of tensor t is
+// emitted as soon as the pass-1 stream has advanced `lag` elements past the
+// end of t's pass 1 (all remaining pass-2 groups at the end). Every rank lists
+// its own segments group by group, each group in CSR (toff) order.
+//  - L2 reuse: t's m, v, p are re-read about `lag` (+ t) elements of pass-1
+//    traffic after they were touched, so a lag that covers the grid's
+//    in-flight window (gridDim.x items) but fits L2 keeps pass 2 out of HBM.
+//  - No deadlock: every rank's list is a subsequence of the global sequence,
+//    and P2(t) follows P1(t) in it. CTAs walk their items in list order, so the
+//    unfinished item first in (group, rank, index) order always has its
+//    dependencies (P1(t) items of every rank, in earlier groups) done.
+//  - The pass-1 items of a tensor are contiguous, so its norm partials reduce
+//    without an index list.
+int tlist_stream_plan(coconet_tlist* tl, int64_t lag) {
+  if (lag <= 0) return set_error(COCONET_ERR_INVALID_INPUT, "lag must be positive");
+  if (tl->stream_wave == lag) return COCONET_OK;
+  const int W = tl->world, n = tl->n_tensors;
+  std::vector<int64_t> size(size_t(n), 0);
+  tl->holders.assign(size_t(n), 0);
+  {
+    std::vector<int64_t> elems(size_t(W) * size_t(n), 0);
+    for (int r = 0; r < W; ++r)
+      for (int64_t s = tl->seg_begin[r]; s < tl->seg_begin[r + 1]; ++s) {
+        const Seg& g = tl->table[size_t(s)];
+        elems[size_t(r) * size_t(n) + size_t(meta_tensor(g.meta))] += meta_len(g.meta);
+      }
+    for (int t = 0; t < n; ++t)
+      for (int r = 0; r < W; ++r) {
+        const int64_t e = elems[size_t(r) * size_t(n) + size_t(t)];
+        size[size_t(t)] = std::max(size[size_t(t)], e);
+        if (e > 0) tl->holders[size_t(t)] |= 1u << r;
+      }
+  }
+  // the global group sequence: (pass, tensor)
+  std::vector<std::pair<int, int>> groups;
+  groups.reserve(size_t(2 * n));
+  std::vector<std::pair<int, int64_t>> pending;  // (tensor, pass-1 end position)
+  size_t head = 0;
+  int64_t pos = 0;
+  for (int t = 0; t < n; ++t) {
+    groups.emplace_back(0, t);
+    pos += size[size_t(t)];
+    pending.emplace_back(t, pos);
+    while (head < pending.size() && pending[head].second + lag <= pos) groups.emplace_back(1, pending[head++].first);
+  }
+  while (head < pending.size()) groups.emplace_back(1, pending[head++].first);
+  tl->items.clear();
+  tl->p1_first.assign(size_t(W) * size_t(n), 0);
+  for (int r = 0; r < W; ++r) {
+    tl->item_begin[r] = int64_t(tl->items.size());
+    const int64_t* ptr = tl->csr_ptr.data() + tl->csr_begin[r];
+    for (auto [pass, t] : groups) {
+      if (pass == 0) tl->p1_first[size_t(r) * size_t(n) + size_t(t)] = int64_t(tl->items.size());
+      for (int64_t i = ptr[t]; i < ptr[t + 1]; ++i) {
+        const Seg& g = tl->table[size_t(tl->csr_idx[size_t(i)])];
+        tl->items.push_back(Item{g.toff, g.sidx, g.meta | (pass ? kPass2Bit : 0)});
+      }
+    }
+  }
+  tl->item_begin[W] = int64_t(tl->items.size());
+  tl->stream_wave = lag;
+  if (!tl->dev_mem) return COCONET_OK;  // plan-only list
+  // device copies: items, p1_first, holders, counters [kMaxRanks][n], partials
+  if (tl->stream_mem) {
+    CN_CUDA(cudaDeviceSynchronize());
+    CN_CUDA(cudaFree(tl->stream_mem));
+    tl->stream_mem = nullptr;
+  }
+  const size_t b_items = tl->items.size() * sizeof(Item);
+  const size_t b_first = tl->p1_first.size() * sizeof(int64_t);
+  const size_t b_hold = size_t(n) * sizeof(uint32_t);
+  const size_t b_cnt = size_t(kMaxRanks) * size_t(n) * sizeof(uint32_t);
+  const size_t b_part = std::max<size_t>(1, tl->items.size()) * 2 * sizeof(double);
+  const size_t total = b_items + b_first + b_hold + b_cnt + b_part + 5 * 256;
+  CN_CUDA(cudaMalloc(&tl->stream_mem, total));
+  char* p = static_cast<char*>(tl->stream_mem);
+  auto carve = [&](size_t nb) {
+    char* q = p;
+    p += (nb + 255) & ~size_t(255);
+    return q;
+  };
+  tl->d_items = reinterpret_cast<Item*>(carve(b_items));
+  tl->d_p1_first = reinterpret_cast<int64_t*>(carve(b_first));
+  tl->d_holders = reinterpret_cast<uint32_t*>(carve(b_hold));
+  tl->d_cnt = reinterpret_cast<uint32_t*>(carve(b_cnt));
+  tl->d_item_part = reinterpret_cast<double*>(carve(b_part));
+  CN_CUDA(cudaMemcpy(tl->d_items, tl->items.data(), b_items, cudaMemcpyHostToDevice));
+  CN_CUDA(cudaMemcpy(tl->d_p1_first, tl->p1_first.data(), b_first, cudaMemcpyHostToDevice));
+  CN_CUDA(cudaMemcpy(tl->d_holders, tl->holders.data(), b_hold, cudaMemcpyHostToDevice));
+  CN_CUDA(cudaMemset(tl->d_cnt, 0, b_cnt));
+  tl->stream_calls = 0;
+  return COCONET_OK;
+}
 
 // Uploads per-tensor heap offsets of the g/x and p/out tensors when they
 // changed since the last call (pageable source: the copy is staged before

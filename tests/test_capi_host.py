@@ -115,3 +115,72 @@ def test_bert_large_list_plan():
     assert tl.n_buckets == sum(-(-n // 1024) for n in counts)
     # shard storage overhead of the alignment padding is tiny
     assert tl.shard_elems < BERT_LARGE_PARAMS / 8 * 1.01
+
+
+def _global_groups(counts_per_rank, lag):
+    """Restatement of tlist_stream_plan's global (pass, tensor) sequence."""
+    size = np.max(counts_per_rank, axis=0)
+    groups, pending, pos = [], [], 0
+    for t in range(len(size)):
+        groups.append((0, t))
+        pos += int(size[t])
+        pending.append((t, pos))
+        while pending and pending[0][1] + lag <= pos:
+            groups.append((1, pending.pop(0)[0]))
+    groups += [(1, t) for t, _ in pending]
+    return groups
+
+
+@pytest.mark.parametrize("W", [1, 2, 3, 4, 8])
+@pytest.mark.parametrize("counts,cap,lag", [([10, 1500, 3, 700], 1024, 512),
+                                             ([1024] * 5, 256, 1024),
+                                             ([1, 1, 1, 1, 1, 1, 1, 1, 5000], 1024, 64),
+                                             ([336_232 + 2, 4096, 31, 9000, 70_000], 4096, 20_000)])
+def test_stream_plan_is_complete_and_deadlock_free(W, counts, cap, lag):
+    """STREAMED-LAMB work lists: every segment of rank r appears once per pass;
+    each tensor's pass-1 items are contiguous and in toff order; every rank's
+    (pass, tensor) group order is a subsequence of ONE global sequence in which
+    P2(t) follows P1(t) and P2(t) starts only after `lag` more elements of
+    pass 1 (or at the end) - which is what makes the persistent grid
+    deadlock-free across ranks."""
+    if sum(counts) < W:
+        pytest.skip()
+    tl = TensorList(None, counts, world=W, bucket_cap=cap)
+    elems = np.zeros((W, len(counts)), np.int64)
+    for r in range(W):
+        segs = tl.segments(r)
+        np.add.at(elems[r], segs[:, 0], segs[:, 2])
+    glob = _global_groups(elems, lag)
+    gpos = {g: i for i, g in enumerate(glob)}
+    for t in range(len(counts)):
+        assert gpos[(1, t)] > gpos[(0, t)]
+    for r in range(W):
+        items = tl.stream_items(lag, r)
+        segs = tl.segments(r)
+        key = lambda a: sorted(map(tuple, a[:, :3].tolist()))
+        assert key(items[items[:, 3] == 0]) == key(segs[:, :3]) == key(items[items[:, 3] == 1])
+        order = [gpos[(int(p), int(t))] for t, p in zip(items[:, 0], items[:, 3])]
+        assert np.all(np.diff(order) >= 0), "rank list must follow the global group sequence"
+        for t in np.unique(items[:, 0]):
+            idx1 = np.nonzero((items[:, 0] == t) & (items[:, 3] == 0))[0]
+            assert np.all(np.diff(idx1) == 1)
+            assert np.all(np.diff(items[idx1, 1]) > 0)
+
+
+def test_stream_plan_bert_large_lag():
+    """BERT-336M at W=1, default lag 2^21: between a tensor's last pass-1 item
+    and its first pass-2 item there are at least `lag` elements of pass-1 work
+    (except the tail), so the grid's in-flight window (~1.2M elements) never
+    reaches a tensor whose pass 1 is still running."""
+    from paper_2105_05720_b200.workloads import bert_large_counts
+    counts = bert_large_counts()
+    lag = 1 << 21
+    tl = TensorList(None, counts, world=1, bucket_cap=4096)
+    items = tl.stream_items(lag, 0)
+    assert len(items) == 2 * len(tl.segments(0))
+    p1_elems = np.cumsum(np.where(items[:, 3] == 0, items[:, 2], 0))
+    total = p1_elems[-1]
+    for t in range(len(counts)):
+        i1 = np.nonzero((items[:, 0] == t) & (items[:, 3] == 0))[0][-1]
+        i2 = np.nonzero((items[:, 0] == t) & (items[:, 3] == 1))[0][0]
+        assert p1_elems[i2] - p1_elems[i1] >= lag or p1_elems[i2] == total
