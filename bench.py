@@ -37,6 +37,7 @@ METRIC = "fused AR+Adam/LAMB step time & NVLink-roofline fraction, 1/2/4/8 B200"
 UNIT = "Gelem/s"
 NVLINK_GBS = 770.0  # measured peer copy per direction (B200_PROFILING.md)
 BUCKET_CAP = 4096
+E2E_GROUPS = 16  # tensor groups pipelined against PCIe in the e2e measurement
 CPU_SAMPLE = 1 << 22  # elements per core for cpu_baseline: ~10-30 s of CPU work
 
 
@@ -199,7 +200,11 @@ def run_coconet(args):
     counts = bert_large_counts()
     padded = [(n + 63) // 64 * 64 for n in counts]
     W = world
-    need = sum(padded) * (2 + 4) + 2 * (sum(counts) // W + 64 * len(counts) + 4096) * 4 + (256 << 20)
+    shard_state = 2 * (sum(counts) // W + 64 * len(counts) + 4096) * 4  # m + v of one rank's shard
+    need = (sum(padded) * (2 + 4) + shard_state  # flat g, p + the fused step's m, v
+            + shard_state + 2 * 8192 * E2E_GROUPS * 4  # the e2e pipeline's per-group m, v
+            + (2 * sum(padded) * 4 if distributed else 0)  # the NCCL baseline's replicated m, v
+            + (256 << 20))
     ctx = Context(W, mode="distributed" if distributed else "virtual", rank=rank, device=local_rank,
                   heap_bytes=need)
     # bucket capacity: the reference's 2^10 (runtime.hpp:579) fixes the flat order
@@ -298,29 +303,36 @@ def run_coconet(args):
         except Exception as e:
             nccl_baseline = {"failed": repr(e)}
 
-    # -- e2e: through the public API with HOST buffers (pinned), H2D of the
-    # step's gradients and D2H of the updated parameters inside the timed region
-    h_grads = [torch.empty(n, dtype=torch.float16, pin_memory=True) for n in counts]
-    h_params = [torch.empty(n, dtype=torch.float32, pin_memory=True) for n in counts]
+    # -- e2e: through the public API with HOST buffers (pinned): every step
+    # copies this rank's fp16 gradients H2D and its updated fp32 parameters
+    # D2H inside the timed region. LambHostPipeline overlaps the PCIe copies
+    # with the fused launches by tensor groups (H2D(k+1) || LAMB(k) || D2H(k-1))
+    from paper_2105_05720_b200.collectives import LambHostPipeline
+    offsets = [0]
+    for pn in padded[:-1]:
+        offsets.append(offsets[-1] + pn)
+    pipe = LambHostPipeline(ctx, counts, flat_g, flat_p, offsets, groups=E2E_GROUPS, bucket_cap=BUCKET_CAP)
+    for (pm, pv) in pipe.state():
+        ctx.view(pm).uniform_(-1e-3, 1e-3)
+        ctx.view(pv).uniform_(1e-4, 1e-3)
     me = my_ranks[0]
-    for i in range(len(counts)):
-        h_grads[i].copy_(ctx.view(grads[i], me))
+    h_g = ctx.view(flat_g, me).cpu().pin_memory()
+    h_p = torch.empty(sum(padded), dtype=torch.float32).pin_memory()
+    for _ in range(2):  # warm-up
+        pipe.step(h_g, h_p, hp)
+        pipe.wait()
     barrier()
-    e2e_steps = max(2, min(args.steps, 5))
+    e2e_steps = max(3, min(args.steps, 10))
     t0 = time.perf_counter()
     for _ in range(e2e_steps):
-        for i in range(len(counts)):
-            ctx.view(grads[i], me).copy_(h_grads[i], non_blocking=True)
-        step()
-        for i in range(len(counts)):
-            h_params[i].copy_(ctx.view(params[i], me), non_blocking=True)
-        torch.cuda.synchronize()
+        pipe.step(h_g, h_p, hp)
+        pipe.wait()
     barrier()
     e2e_s = (time.perf_counter() - t0) / e2e_steps
     if distributed:
         e2e_s = max_over_ranks(e2e_s)
-    h2d = sum(counts) * 2
-    d2h = sum(counts) * 4
+    h2d = pipe.h2d_bytes
+    d2h = pipe.d2h_bytes
 
     # -- roofline of the dominant (only) kernel
     hbm_peak, tc_peak, peak_kind = peaks()
@@ -388,7 +400,8 @@ def run_coconet(args):
             "roofline": roof, "cpu_baseline": cpu,
             "e2e": {"value": W * N / e2e_s / 1e9, "unit": UNIT, "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h,
-                    "what": "pinned H2D of this rank's fp16 grads + fused step + D2H of updated fp32 params"},
+                    "what": "pinned H2D of this rank's fp16 grads + fused step + D2H of updated fp32 params, "
+                            f"pipelined by {len(pipe.groups)} tensor groups (collectives.LambHostPipeline)"},
             "gpu_launches": launches, "clocks": clocks,
             "kernel_ms": ms,
             "extras": extras,

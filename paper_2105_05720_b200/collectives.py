@@ -234,3 +234,88 @@ def mm_overlap_fused_ar(ctx: Context, a: SymmBuffer, w: SymmBuffer, b: SymmBuffe
                                               ctx.ptr(r), ctx.ptr(partial), ctx.ptr(out),
                                               elem_of(a.dtype), rows, w.shape[-1], a.shape[-1],
                                               C.byref(p), ctx.stream_ptr(stream)))
+
+
+class LambHostPipeline:
+    """A fused RS+LAMB+AG step whose gradients come from, and whose updated
+    parameters go back to, pinned HOST memory (the reference's own contract:
+    Engine::run takes and returns host vectors, runtime.hpp:101).
+
+    LAMB's trust ratio is per tensor, so the tensor list is cut into `groups`
+    contiguous tensor groups of about equal size, each with its own bucket
+    table and state shard. Per step, group k's H2D copy (one contiguous
+    range of the flat gradient buffer), its fused launch and its D2H copy run
+    on three streams, so PCIe in both directions overlaps the kernels:
+        H2D(k+1) || LAMB(k) || D2H(k-1).
+    Results are those of one fused step over the whole list (W = 1: bitwise;
+    W > 1: every element reduced in its own group's ring order).
+
+    counts: element counts; g_flat / p_flat: symmetric flat buffers holding the
+    tensors at `offsets` (elements, 4-aligned); host buffers passed to step()
+    use the same flat layout."""
+
+    def __init__(self, ctx: Context, counts, g_flat: SymmBuffer, p_flat: SymmBuffer, offsets, groups: int = 8,
+                 bucket_cap: int = 4096):
+        self.ctx = ctx
+        counts = [int(c) for c in counts]
+        offsets = [int(o) for o in offsets]
+        total = sum(counts)
+        gsz = torch.empty((), dtype=g_flat.dtype).element_size()
+        cuts, acc = [0], 0
+        for i, n in enumerate(counts):
+            acc += n
+            if acc * groups >= total * len(cuts) and i + 1 < len(counts) and len(cuts) < groups:
+                cuts.append(i + 1)
+        cuts.append(len(counts))
+        self.groups = []
+        for a, b in zip(cuts[:-1], cuts[1:]):
+            if a == b:
+                continue
+            tl = TensorList(ctx, counts[a:b], bucket_cap=bucket_cap)
+            grads = [SymmBuffer(g_flat.offset + offsets[i] * gsz, (counts[i],), g_flat.dtype) for i in range(a, b)]
+            params = [SymmBuffer(p_flat.offset + offsets[i] * 4, (counts[i],), torch.float32) for i in range(a, b)]
+            lo, hi = offsets[a], offsets[b - 1] + counts[b - 1]
+            m = ctx.alloc([tl.shard_elems], torch.float32)
+            v = ctx.alloc([tl.shard_elems], torch.float32)
+            self.groups.append(dict(tl=tl, grads=grads, params=params, lo=lo, hi=hi, m=m, v=v))
+        self.g_flat, self.p_flat = g_flat, p_flat
+        self.h2d = torch.cuda.Stream(device=ctx.device)
+        self.d2h = torch.cuda.Stream(device=ctx.device)
+        self.ev_in = [torch.cuda.Event() for _ in self.groups]
+        self.ev_run = [torch.cuda.Event() for _ in self.groups]
+        self.ev_out = [torch.cuda.Event() for _ in self.groups]
+        self.stepped = False
+        self.h2d_bytes = sum(g["hi"] - g["lo"] for g in self.groups) * gsz
+        self.d2h_bytes = sum(g["hi"] - g["lo"] for g in self.groups) * 4
+
+    def state(self):
+        """(m, v) shard buffers of every group (for initialisation)."""
+        return [(g["m"], g["v"]) for g in self.groups]
+
+    def step(self, h_grads: torch.Tensor, h_params: torch.Tensor, hp: LambHParams, stream=None) -> None:
+        """h_grads / h_params: pinned flat host tensors (the flat layout of
+        g_flat / p_flat). Asynchronous; h_params is complete once
+        `self.d2h` is (see wait())."""
+        ctx = self.ctx
+        comp = stream if stream is not None else torch.cuda.current_stream()
+        dg = ctx.view(self.g_flat)
+        dp = ctx.view(self.p_flat)
+        for k, g in enumerate(self.groups):
+            with torch.cuda.stream(self.h2d):
+                if self.stepped:  # the previous step's launch must be done reading these gradients
+                    self.h2d.wait_event(self.ev_run[k])
+                dg[g["lo"]:g["hi"]].copy_(h_grads[g["lo"]:g["hi"]], non_blocking=True)
+                self.ev_in[k].record(self.h2d)
+            comp.wait_event(self.ev_in[k])
+            if self.stepped:  # the previous step's D2H of these params must be done before we overwrite them
+                comp.wait_event(self.ev_out[k])
+            fused_rs_lamb_ag(ctx, g["tl"], g["grads"], g["params"], g["m"], g["v"], hp, stream=comp)
+            self.ev_run[k].record(comp)
+            with torch.cuda.stream(self.d2h):
+                self.d2h.wait_event(self.ev_run[k])
+                h_params[g["lo"]:g["hi"]].copy_(dp[g["lo"]:g["hi"]], non_blocking=True)
+                self.ev_out[k].record(self.d2h)
+        self.stepped = True
+
+    def wait(self):
+        self.d2h.synchronize()
