@@ -121,7 +121,8 @@ def load(path: os.PathLike | None = None):
     global _lib
     if _lib is not None:
         return _lib
-    p = Path(path) if path else LIB_PATH
+    # COCONET_LIB: an alternative build of the same library (kernel variants in probes)
+    p = Path(path) if path else Path(os.environ.get("COCONET_LIB", str(LIB_PATH)))
     if not p.exists():
         raise ImportError(
             f"{p} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'` "
