@@ -98,6 +98,29 @@ def build_engine(force: bool = False) -> Path | None:
     return ENGINE_LIB
 
 
+CLI_BIN = PKG / "coconet-ccopt"
+
+
+def build_cli(force: bool = False) -> Path | None:
+    """coconet-ccopt: the reference CLI flow (tools/ccopt.cpp) with a CUDA
+    backend; like the engine it needs the reference DSL headers to build."""
+    srcs = sorted((CSRC / "cli").glob("*.cpp")) if (CSRC / "cli").exists() else []
+    if not srcs:
+        return None
+    hdrs = list((INCLUDE / "coconet").glob("*.hpp")) + [INCLUDE / "coconet_cuda.h"]
+    if not (CCOPT_REF_DIR / "include" / "ccopt").exists():
+        return CLI_BIN if CLI_BIN.exists() else None
+    if not force and not _stale(CLI_BIN, srcs + hdrs):
+        return CLI_BIN
+    cmd = ["g++", "-std=c++20", "-O2", "-pthread", "-I", str(INCLUDE),
+           "-I", str(CCOPT_REF_DIR / "include"), "-I", str(NLOHMANN_DIR), "-I",
+           str(CUDA_HOME / "include"), "-o", str(CLI_BIN)] + [str(s) for s in srcs] + [
+        "-L", str(PKG), "-Wl,-rpath,$ORIGIN", "-lcoconet_cuda",
+        "-L", str(CUDA_HOME / "lib64"), "-Wl,-rpath," + str(CUDA_HOME / "lib64"), "-lcudart"]
+    _run(cmd)
+    return CLI_BIN
+
+
 def build_oracle() -> None:
     make = shutil.which("make")
     if not make:
@@ -111,4 +134,5 @@ def build_oracle() -> None:
 def build_all(force: bool = False) -> None:
     build_cuda(force=force)
     build_engine(force=force)
+    build_cli(force=force)
     build_oracle()

@@ -9,6 +9,7 @@
 #include "ccopt/json_io.hpp"
 #include "ccopt/transform.hpp"
 #include "coconet/gpu_engine.hpp"
+#include "coconet/gpu_tune.hpp"
 
 namespace {
 
@@ -159,6 +160,27 @@ int coconet_engine_result(void* h, const char* key, int idx, float* out, int64_t
     if (int64_t(arr.size()) != n) throw ccopt::Error(ccopt::ErrCode::ShapeMismatch, "result size");
     std::memcpy(out, arr.data(), size_t(n) * sizeof(float));
     return 0;
+  } catch (const ccopt::Error& e) {
+    return fail(e);
+  } catch (const std::exception& e) {
+    return fail_std(e);
+  }
+}
+
+// ccopt tune with candidates ranked by measured device time (gpu_tune.hpp):
+// program JSON + size symbols -> the tune report JSON in buf (returns its
+// length, -needed if buf is too small, or a negative status).
+int coconet_engine_tune(const char* program_json, const char* dims_json, uint64_t seed, double tol, int device,
+                        int math, int reps, char* buf, int64_t len) {
+  try {
+    ccopt::Program p = ccopt::program_from_json(ccopt::Json::parse(program_json), dims_of(dims_json));
+    ccopt::TuneConfig cfg;
+    cfg.seed = seed;
+    cfg.tol = tol;
+    coconet::GpuOptions opt;
+    opt.device = device;
+    opt.math = math;
+    return copy_out(coconet::gpu_tune_report_to_json(coconet::gpu_tune(p, cfg, opt, reps)).dump(), buf, len);
   } catch (const ccopt::Error& e) {
     return fail(e);
   } catch (const std::exception& e) {

@@ -37,6 +37,7 @@ def load():
             ("coconet_engine_digest", U64, [P]),
             ("coconet_engine_report", I, [P, C.c_char_p, I64]),
             ("coconet_engine_result", I, [P, C.c_char_p, I, FP, I64]),
+            ("coconet_engine_tune", I, [C.c_char_p, C.c_char_p, U64, C.c_double, I, I, I, C.c_char_p, I64]),
         ]:
             fn = getattr(lib, name)
             fn.restype = res
@@ -101,3 +102,23 @@ class GpuEngineSession:
         _check(self.lib.coconet_engine_result(self.h, key.encode(), idx,
                                               out.ctypes.data_as(C.POINTER(C.c_float)), n))
         return out
+
+
+def gpu_tune(program, dims=None, seed: int = 1, tol: float = 1e-5, device: int = 0,
+             math: int = _lib.MATH_EXACT, reps: int = 3) -> dict:
+    """ccopt tune (autotune.hpp:285-315) over the reference's own candidate
+    schedules, each verified against the oracle and ranked by MEASURED device
+    time on the GPU (include/coconet/gpu_tune.hpp). Returns the tune report
+    (reference fields + device_ms per candidate, winner by device_ms, and the
+    reference's simulated_winner)."""
+    lib = load()
+    prog = program if isinstance(program, str) else json.dumps(program)
+    n = 1 << 20
+    while True:
+        buf = C.create_string_buffer(n)
+        rc = lib.coconet_engine_tune(prog.encode(), json.dumps(dims or {}).encode(), seed, tol, device, math,
+                                     reps, buf, n)
+        if rc == -1000 or rc >= 0 or -rc <= 30:
+            _check(rc)
+            return json.loads(buf.value.decode())
+        n = -rc

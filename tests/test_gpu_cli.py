@@ -1,0 +1,67 @@
+"""coconet-ccopt with the CUDA backend on B200: the
+`ccopt run` flow reproduces the reference Engine's digests on every golden
+family, and `tune` ranks the reference's own candidate schedules by measured
+device time after verifying each against the oracle."""
+import json
+
+import pytest
+
+from tests.cli_util import GOLD, cli, dims_args, need_cli, program_file
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("case", ["adam_W4_N4096", "adam_W8_N4096", "mp_W8_B2_S16_H128", "mp_W4_B2_S8_H64",
+                                  "pp_W8_N4096", "pp_W4_N1024"])
+def test_run_cuda_matches_reference_digest(tmp_path, case):
+    need_cli()
+    from tests.dp_util import golden
+    try:
+        golden(case)
+    except KeyError:
+        pytest.skip(f"no fixture {case}")
+    f, rec = program_file(tmp_path, case, "sched_program")
+    j = json.loads(cli("run", f, *dims_args(rec), "--seed", rec.get("seed", 1), check_rc=0).stdout)
+    assert j["backend"] == "cuda" and j["math"] == "exact"
+    assert j["digest"] == rec["engine_sched_digest"]
+    assert j["deviation"] <= 1e-5 and j["device_ms"] > 0
+    assert j["lowering"]
+
+
+def test_run_cuda_fast_within_tolerance(tmp_path):
+    need_cli()
+    f, rec = program_file(tmp_path, "adam_W4_N4096", "sched_program")
+    j = json.loads(cli("run", f, *dims_args(rec), "--math", "fast", check_rc=0).stdout)
+    assert j["math"] == "fast" and j["deviation"] <= 1e-5
+
+
+def _check_tune(j, ref):
+    assert [c["schedule"] for c in j["candidates"]] == [c["schedule"] for c in ref["candidates"]]
+    for c, r in zip(j["candidates"], ref["candidates"]):
+        assert c["simulated_time"] == pytest.approx(r["simulated_time"], rel=1e-12)
+        assert c["comm_bytes"] == r["comm_bytes"] and c["kernel_steps"] == r["kernel_steps"]
+        assert c["deviation"] <= 1e-5 and c["device_ms"] > 0
+    ms = [c["device_ms"] for c in j["candidates"]]
+    assert ms[j["winner"]] == min(ms)
+    assert j["simulated_winner"] == ref["winner"]
+    assert j["ranked_by"] == "device_ms"
+
+
+def test_tune_cuda_ranks_reference_candidates_by_device_time(tmp_path):
+    need_cli()
+    ref = json.loads((GOLD / "tune_adam_W4_N4096.json").read_text())
+    f = tmp_path / "adam.json"
+    f.write_text(json.dumps(ref["program"]))
+    j = json.loads(cli("tune", f, "--ranks", "4", "--size", "N=4096", "--reps", "2", check_rc=0).stdout)
+    _check_tune(j, ref)
+
+
+def test_engine_gpu_tune_python_binding():
+    from paper_2105_05720_b200 import engine
+    ref = json.loads((GOLD / "tune_adam_W4_N4096.json").read_text())
+    try:
+        engine.load()
+    except ImportError:
+        pytest.skip("libcoconet_engine.so not built")
+    j = engine.gpu_tune(ref["program"], dims={"W": 4, "N": 4096}, reps=2)
+    _check_tune(j, ref)
