@@ -21,6 +21,7 @@
 //   Send / FusedSend / Recv           -> pointwise on the source stage + peer copy
 //   OverlapGroup {RS, FusedSend, AG}  -> coconet_rs_fused_send_ag   (one kernel)
 //   OverlapGroup (other)              -> members in order
+//   Reduce / Broadcast                -> coconet_reduce / coconet_broadcast
 // Counters (comm_bytes, intergroup_bytes, traffic_saved_bytes, kernel_steps,
 // memory_elems) follow the reference's accounting exactly; simulated_time is
 // the reference's own cost model (Engine::step_time); device_ms is measured.
@@ -307,9 +308,28 @@ class GpuEngine {
       case OpKind::Recv: vals_[n.id] = value(n.inputs[0]); break;
       case OpKind::FusedAllReduce: exec_fused_allreduce(n); break;
       case OpKind::OverlapGroup: exec_overlap(n); break;
-      case OpKind::Reduce:
-      case OpKind::Broadcast:
-        throw Error(ErrCode::InvalidInput, "reduce/broadcast are not lowered to the GPU backend");
+      case OpKind::Reduce: {  // runtime.hpp:415-428
+        const DVal& x = value(n.inputs[0]);
+        DVal& out = node_out(n, n.out_layout);
+        const int64_t total = num_elems(x.view.global);
+        ck(coconet_reduce(ctx_, cgroup(n.group), sym(x), sym(out), COCONET_F32, int(n.reducer), total, n.root,
+                          stream_));
+        // the reference's fold loop starts at rank 1 and counts inside it, so
+        // rank 0 is never counted (runtime.hpp:420-424); mirrored as is
+        for (int r = 1; r < G; ++r)
+          if (r != n.root) count(n.group, r, total * input_bw(n));
+        lowering_.push_back(n.id + ":reduce");
+        break;
+      }
+      case OpKind::Broadcast: {  // runtime.hpp:429-436: the root sends G-1 copies
+        const DVal& x = value(n.inputs[0]);
+        DVal& out = node_out(n, n.out_layout);
+        const int64_t total = num_elems(x.view.global);
+        ck(coconet_broadcast(ctx_, cgroup(n.group), sym(x), sym(out), COCONET_F32, total, n.root, stream_));
+        count(n.group, n.root, int64_t(G - 1) * total * input_bw(n));
+        lowering_.push_back(n.id + ":broadcast");
+        break;
+      }
     }
   }
 

@@ -232,6 +232,16 @@ int coconet_reduce_scatter(coconet_ctx_t ctx, int group, const void* x, void* ou
 int coconet_all_gather(coconet_ctx_t ctx, int group, const void* x, void* out, int elem, int ndim,
                        const int64_t* shape, int axis, void* stream);
 
+/* Rooted collectives (runtime.hpp:415-436). Reduce: the root's out = fold of
+ * every rank's x (n elements) in RANK order 0..G-1 in fp32 (the Engine's
+ * order), other ranks' out = 0 (Local layout: meaningful on the root only,
+ * program.hpp:315-321); x may alias out. Broadcast: every rank's out = the
+ * root's x. `root` is a group rank. */
+int coconet_reduce(coconet_ctx_t ctx, int group, const void* x, void* out, int elem, int reducer, int64_t n,
+                   int root, void* stream);
+int coconet_broadcast(coconet_ctx_t ctx, int group, const void* x, void* out, int elem, int64_t n, int root,
+                      void* stream);
+
 /* ---- fused MP / PP epilogues (goldens/model_parallel.json, pipeline.json) - */
 /* out = dropout(x + b, rate, key) + r, element-wise, dropout index = global
  * flat index (expr.hpp:15-27, state.hpp:178-181); b broadcast over leading

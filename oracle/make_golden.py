@@ -29,6 +29,10 @@ ADAM_CASES = [(w, n) for w in (1, 2, 4, 8) for n in (1024, 4096)] + [(4, 1 << 20
 MP_CASES = [(w, dims) for w in (1, 2, 4) for dims in ({"B": 2, "S": 8, "H": 64},)] + [
     (8, {"B": 2, "S": 16, "H": 128})]
 PP_CASES = [(w, n) for w in (2, 4, 8) for n in (1024, 4096)]
+# Reduce / Broadcast (runtime.hpp:415-436) + reorder_broadcast (transform.hpp:265-330):
+# no reference golden uses them, so the program is authored in the reference
+# format (tests/golden/rooted_*.json, reducer substituted) and evaluated here.
+ROOTED_CASES = [(w, n, red) for w in (2, 4, 8) for n in (1024, 4096) for red in ("sum", "max")] + [(3, 999, "min")]
 
 
 def key_digests(sess, which):
@@ -93,6 +97,13 @@ def main():
         dims = {"N": n, "W": w, "B": 2, "S": 8, "H": 64}
         recs.append(run_case(f"pp_W{w}_N{n}", pp.read_text(), pp_s.read_text(), dims))
     (OUT / "pp_cases.json").write_text(json.dumps(recs, indent=1))
+    rooted = (OUT / "rooted_program.json").read_text()
+    rooted_s = (OUT / "rooted_schedule.json").read_text()
+    recs = []
+    for w, n, red in ROOTED_CASES:
+        dims = {"N": n, "W": w, "B": 2, "S": 8, "H": 64}
+        recs.append(run_case(f"rooted_{red}_W{w}_N{n}", rooted.replace("REDUCER", red), rooted_s, dims))
+    (OUT / "rooted_cases.json").write_text(json.dumps(recs, indent=1))
     # KAT: AdamScalarChainFrozenValues (test_oracle.cpp:24-48), through the reference
     # N=4 (not 1): the fused schedule needs N % W == 0 (as_slice, transform.hpp:553)
     s = ref.RefSession(adam.read_text(), adam_s.read_text(), {"N": 4, "W": 4, "B": 2, "S": 8, "H": 64})

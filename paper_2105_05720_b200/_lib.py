@@ -101,6 +101,8 @@ _SIGNATURES = {
     "coconet_allreduce": (_I, [_P, _P, _PP, _PP, _I, _I, _I, _P]),
     "coconet_reduce_scatter": (_I, [_P, _I, _P, _P, _I, _I, _I, _PI64, _I, _P]),
     "coconet_all_gather": (_I, [_P, _I, _P, _P, _I, _I, _PI64, _I, _P]),
+    "coconet_reduce": (_I, [_P, _I, _P, _P, _I, _I, _I64, _I, _P]),
+    "coconet_broadcast": (_I, [_P, _I, _P, _P, _I, _I64, _I, _P]),
     "coconet_fused_rs_bdr_ag": (_I, [_P, _I, _P, _P, _P, _P, _I, _I64, _I64, C.POINTER(BdrParams), _P]),
     "coconet_rs_fused_send_ag": (_I, [_P, _I, _I, _P, _P, _P, _P, _I, _I64, C.POINTER(BdrParams), _P]),
     "coconet_matmul": (_I, [_P, _I, _P, _P, _P, _I, _I, _I64, _I64, _I64, _I, _P]),

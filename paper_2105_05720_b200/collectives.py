@@ -177,6 +177,20 @@ def all_gather(ctx: Context, x: SymmBuffer | None, out: SymmBuffer, axis: int = 
                                      ctx.stream_ptr(stream)))
 
 
+def reduce(ctx: Context, x: SymmBuffer, out: SymmBuffer, root: int = 0, reducer: int = _lib.SUM,
+           group: int = 0, stream=None) -> None:
+    """Reduce to `root` (runtime.hpp:415-428): rank-order fp32 fold on the
+    root, zeros elsewhere."""
+    check(ctx.lib.coconet_reduce(ctx.handle, group, ctx.ptr(x), ctx.ptr(out), elem_of(x.dtype), reducer,
+                                 x.numel, root, ctx.stream_ptr(stream)))
+
+
+def broadcast(ctx: Context, x: SymmBuffer, out: SymmBuffer, root: int = 0, group: int = 0, stream=None) -> None:
+    """Broadcast from `root` (runtime.hpp:429-436)."""
+    check(ctx.lib.coconet_broadcast(ctx.handle, group, ctx.ptr(x), ctx.ptr(out), elem_of(x.dtype), x.numel, root,
+                                    ctx.stream_ptr(stream)))
+
+
 def gen_values(ctx: Context, dst: torch.Tensor, seed: int, name: str, layout: str, rank: int,
                global_shape, sliced_dim: int = -1, group_size: int = 1, stream=None) -> None:
     """gen_decl_values (state.hpp:55-74) for one decl on one rank, on device."""

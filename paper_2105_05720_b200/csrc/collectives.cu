@@ -1,4 +1,5 @@
-// Axis-sliced ReduceScatter / AllGather of one tensor over a group.
+// Axis-sliced ReduceScatter / AllGather of one tensor over a group, and the
+// rooted Reduce / Broadcast.
 //
 // Reference: Engine::run_reduce_scatter (runtime.hpp:352-363) and the
 // AllGather case (runtime.hpp:396-414) with ChunkSpec::axis_chunks
@@ -10,6 +11,16 @@
 // folds in ring order) and push-AG (each rank stores its slice into every
 // peer); quads of 4 elements when the contiguous runs allow, flag barriers at
 // entry/exit as in fused_opt.cu.
+//
+// Reduce (runtime.hpp:415-428): the root pulls every rank's tensor and folds
+// in RANK order 0..G-1 in fp32 (acc = x_0; acc = reduce_apply(acc, x_r)),
+// exactly as the Engine does; other ranks' outputs are zero (Local layout,
+// meaningful on the root only, program.hpp:315-321). Broadcast (:429-436):
+// every rank pulls the root's tensor (the root's NVLink egress is (G-1)*N,
+// as in the reference's byte count).
+#include <algorithm>
+#include <string>
+
 #include "internal.h"
 
 using namespace coconet;
@@ -41,6 +52,74 @@ __device__ __forceinline__ float fold(float acc, float x) {
 }
 
 // RS: out_r[li] = ring-order fold over q of x_q[to_global(r, li)].
+struct RootArgs {
+  RankSet rs;
+  int64_t x_off, out_off, n;
+  int root;
+};
+
+// Reduce: the root folds x over ranks 0..G-1; after the exit barrier (the
+// root is done reading every x) the other ranks zero their output, so x may
+// alias out.
+template <typename T, int RED, int VEC>
+__global__ void __launch_bounds__(kThreads) reduce_kernel(RootArgs a) {
+  __shared__ char* s_base[kMaxRanks];
+  const RankSet& rs = a.rs;
+  if (threadIdx.x < kMaxRanks) s_base[threadIdx.x] = threadIdx.x < rs.world ? rs.base[threadIdx.x] : nullptr;
+  const int W = rs.world, me = rs.rank();
+  if (!rank_barrier(rs, 0)) return;
+  const int64_t nq = a.n / VEC;
+  const int64_t st = int64_t(gridDim.x) * kThreads;
+  if (me == a.root) {
+    T* out = reinterpret_cast<T*>(s_base[me] + a.out_off);
+    for (int64_t q = int64_t(blockIdx.x) * kThreads + threadIdx.x; q < nq; q += st) {
+      float acc[VEC], x[VEC];
+#pragma unroll
+      for (int j = 0; j < kMaxRanks; ++j) {
+        if (j >= W) break;
+        const T* xs = reinterpret_cast<const T*>(s_base[j] + a.x_off) + q * VEC;
+        if (VEC == 4) load4_cg(xs, x);
+        else x[0] = to_f32(xs[0]);
+#pragma unroll
+        for (int i = 0; i < VEC; ++i) acc[i] = j == 0 ? x[i] : fold<T, RED>(acc[i], x[i]);
+      }
+      if (VEC == 4) store4(out + q * VEC, acc);
+      else out[q] = from_f32<T>(acc[0]);
+    }
+  }
+  if (!rank_barrier(rs, 1)) return;
+  if (me != a.root) {
+    T* out = reinterpret_cast<T*>(s_base[me] + a.out_off);
+    for (int64_t i = int64_t(blockIdx.x) * kThreads + threadIdx.x; i < a.n; i += st) out[i] = from_f32<T>(0.f);
+  }
+}
+
+// Broadcast: every rank copies the root's x into its out.
+template <typename T, int VEC>
+__global__ void __launch_bounds__(kThreads) bcast_kernel(RootArgs a) {
+  __shared__ char* s_base[kMaxRanks];
+  const RankSet& rs = a.rs;
+  if (threadIdx.x < kMaxRanks) s_base[threadIdx.x] = threadIdx.x < rs.world ? rs.base[threadIdx.x] : nullptr;
+  const int me = rs.rank();
+  if (!rank_barrier(rs, 0)) return;
+  const bool same = me == a.root && a.x_off == a.out_off;
+  if (!same) {
+    const T* src = reinterpret_cast<const T*>(s_base[a.root] + a.x_off);
+    T* out = reinterpret_cast<T*>(s_base[me] + a.out_off);
+    const int64_t nq = a.n / VEC;
+    for (int64_t q = int64_t(blockIdx.x) * kThreads + threadIdx.x; q < nq; q += int64_t(gridDim.x) * kThreads) {
+      if (VEC == 4) {
+        float x[4];
+        load4_cg(src + q * 4, x);
+        store4(out + q * 4, x);
+      } else {
+        out[q] = src[q];
+      }
+    }
+  }
+  rank_barrier(rs, 1);  // nobody overwrites the root's x while peers still read it
+}
+
 template <typename T, int RED, int VEC>
 __global__ void __launch_bounds__(kThreads) rs_kernel(AxisArgs a) {
   __shared__ char* s_base[kMaxRanks];
@@ -151,6 +230,54 @@ int launch(coconet_ctx* c, int group, const void* fn, AxisArgs* a, bool vec, cud
 
 int elem_size(int e) { return e == COCONET_F32 ? 4 : 2; }
 
+template <typename T, int VEC>
+const void* reduce_fn(int red) {
+  if (red == COCONET_MAX) return reinterpret_cast<const void*>(&reduce_kernel<T, COCONET_MAX, VEC>);
+  if (red == COCONET_MIN) return reinterpret_cast<const void*>(&reduce_kernel<T, COCONET_MIN, VEC>);
+  return reinterpret_cast<const void*>(&reduce_kernel<T, COCONET_SUM, VEC>);
+}
+
+template <typename T>
+const void* reduce_pick(int red, bool vec) { return vec ? reduce_fn<T, 4>(red) : reduce_fn<T, 1>(red); }
+
+template <typename T>
+const void* bcast_pick(bool vec) {
+  return vec ? reinterpret_cast<const void*>(&bcast_kernel<T, 4>) : reinterpret_cast<const void*>(&bcast_kernel<T, 1>);
+}
+
+int rooted(coconet_ctx* c, int group, const void* x, void* out, int elem, int64_t n, int root, bool is_reduce,
+           int reducer, cudaStream_t s) {
+  if (!c || !x || !out) return set_error(COCONET_ERR_INVALID_INPUT, "null argument");
+  if (!valid_group(c, group)) return set_error(COCONET_ERR_NO_SUCH_RANK, "no such group");
+  const int W = c->groups[size_t(group)].size;
+  if (root < 0 || root >= W) return set_error(COCONET_ERR_NO_SUCH_RANK, "root " + std::to_string(root) + " out of range");
+  if (n < 0) return set_error(COCONET_ERR_SHAPE_MISMATCH, "negative element count");
+  if (elem < COCONET_F32 || elem > COCONET_BF16) return set_error(COCONET_ERR_INVALID_INPUT, "bad elem");
+  if (is_reduce && (reducer < COCONET_SUM || reducer > COCONET_MIN))
+    return set_error(COCONET_ERR_INVALID_INPUT, "bad reducer");
+  RootArgs a{};
+  int rc = heap_offset(c, x, &a.x_off);
+  if (!rc) rc = heap_offset(c, out, &a.out_off);
+  if (rc) return rc;
+  a.n = n;
+  a.root = root;
+  const bool vec = n % 4 == 0 && (a.x_off | a.out_off) % (4 * elem_size(elem)) == 0;
+  const void* fn = is_reduce ? (elem == COCONET_F32   ? reduce_pick<float>(reducer, vec)
+                                : elem == COCONET_F16 ? reduce_pick<__half>(reducer, vec)
+                                                      : reduce_pick<__nv_bfloat16>(reducer, vec))
+                             : (elem == COCONET_F32   ? bcast_pick<float>(vec)
+                                : elem == COCONET_F16 ? bcast_pick<__half>(vec)
+                                                      : bcast_pick<__nv_bfloat16>(vec));
+  const int64_t units = vec ? n / 4 : n;
+  int blocks = 0;
+  rc = coop_blocks(c, fn, kThreads, 0, group, std::max<int64_t>(1, (units + kThreads - 1) / kThreads), &blocks);
+  if (rc) return rc;
+  rc = make_rankset(c, group, &a.rs);
+  if (rc) return rc;
+  void* args[] = {&a};
+  return coop_launch(c, fn, dim3(unsigned(blocks), unsigned(local_ranks(c, group))), dim3(kThreads), args, 0, s);
+}
+
 }  // namespace
 
 extern "C" {
@@ -187,6 +314,16 @@ int coconet_all_gather(coconet_ctx_t c, int group, const void* x, void* out, int
                    : elem == COCONET_F16 ? ag_pick<__half>(vec)
                                          : ag_pick<__nv_bfloat16>(vec);
   return launch(c, group, fn, &a, vec, static_cast<cudaStream_t>(stream));
+}
+
+int coconet_reduce(coconet_ctx_t c, int group, const void* x, void* out, int elem, int reducer, int64_t n,
+                   int root, void* stream) {
+  return rooted(c, group, x, out, elem, n, root, true, reducer, static_cast<cudaStream_t>(stream));
+}
+
+int coconet_broadcast(coconet_ctx_t c, int group, const void* x, void* out, int elem, int64_t n, int root,
+                      void* stream) {
+  return rooted(c, group, x, out, elem, n, root, false, COCONET_SUM, static_cast<cudaStream_t>(stream));
 }
 
 }  // extern "C"

@@ -19,7 +19,7 @@ GOLD = Path(__file__).resolve().parent / "golden"
 
 def all_cases():
     out = []
-    for kind in ("adam", "mp", "pp"):
+    for kind in ("adam", "mp", "pp", "rooted"):
         for rec in json.loads((GOLD / f"{kind}_cases.json").read_text()):
             if rec["name"] in ("adam_W4_N1048576",):
                 continue  # covered by the kernel-level test; keep this suite quick
@@ -56,6 +56,8 @@ def test_scheduled_program_matches_reference_engine(rec, fused):
             assert "rs_fused_send_ag" in low
         if rec["name"].startswith("mp") and rec["dims"]["H"] // rec["dims"]["W"] % 4 == 0:
             assert "fused_rs_bdr_ag" in low
+        if rec["name"].startswith("rooted"):
+            assert ":reduce" in low and ":broadcast" in low
 
 
 @pytest.mark.parametrize("rec", CASES, ids=lambda r: r["name"])
