@@ -111,3 +111,101 @@ def test_distributed_processes_share_one_gpu(world):
         assert err is None, err
         assert ok_p, f"rank {rank}: fused Adam differs from the reference"
         assert ok_ar, f"rank {rank}: allreduce differs from the reference"
+
+
+def _worker_lamb_rooted(rank, world, port, counts, q):
+    """LAMB (GRID and STREAMED: cross-process per-tensor ready flags) and the
+    rooted collectives, one process per rank."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from oracle import coconet_oracle as co
+        from paper_2105_05720_b200 import _lib
+        from paper_2105_05720_b200.collectives import LambHParams, TensorList, broadcast, fused_rs_lamb_ag, reduce
+        from paper_2105_05720_b200.runtime import Context
+
+        torch.cuda.set_device(0)
+        ctx = Context(world, mode="distributed", rank=rank, device=0, heap_bytes=64 << 20, timeout_ms=60000)
+        g, p, m, v = _inputs(world, counts)
+        outs = {}
+        for sched in (_lib.LAMB_GRID, _lib.LAMB_STREAMED):
+            tl = TensorList(ctx, counts, bucket_cap=512)
+            gb = [ctx.alloc([n]) for n in counts]
+            pb = [ctx.alloc([n]) for n in counts]
+            mb, vb = ctx.alloc([tl.shard_elems]), ctx.alloc([tl.shard_elems])
+            tens, elem, sidx = tl.state_index_map(rank)
+            ms = np.zeros(tl.shard_elems, np.float32)
+            vs = np.zeros(tl.shard_elems, np.float32)
+            for t in range(len(counts)):
+                ctx.view(gb[t]).copy_(torch.from_numpy(g[t][rank]))
+                ctx.view(pb[t]).copy_(torch.from_numpy(p[t]))
+                sel = tens == t
+                ms[sidx[sel]] = m[t][elem[sel]]
+                vs[sidx[sel]] = v[t][elem[sel]]
+            ctx.view(mb).copy_(torch.from_numpy(ms))
+            ctx.view(vb).copy_(torch.from_numpy(vs))
+            torch.cuda.synchronize()
+            dist.barrier()
+            first = None
+            for step in range(3):
+                fused_rs_lamb_ag(ctx, tl, gb, pb, mb, vb,
+                                 LambHParams(lr=0.01, beta1=0.9, beta2=0.999, t=float(step + 1), sched=sched,
+                                             lag_elems=2000))
+                ctx.check()
+                if step == 0:
+                    first = [ctx.view(b).cpu().numpy().copy() for b in pb]
+            outs[sched] = ([ctx.view(b).cpu().numpy() for b in pb], first)
+        same = all(np.array_equal(a, b) for a, b in zip(outs[_lib.LAMB_GRID][0], outs[_lib.LAMB_STREAMED][0]))
+        k = co.lamb_consts(0.01, 0.9, 0.999, 1.0, 1e-6, 0.01)
+        table = co.bucket_table(counts)
+        flat = co.flatten_bucket_order(g, table)
+        bounds = co.flat_chunks(flat.shape[1], world)
+        owner = np.searchsorted(np.asarray(bounds[1:]), np.arange(flat.shape[1]), side="right")
+        gr = co.unflatten_bucket_order(co.ring_reduce(flat, owner), counts, table)
+        dev = max(co.max_rel_deviation(outs[_lib.LAMB_STREAMED][1][t], co.lamb_oracle(gr[t], m[t], v[t], p[t], k)[2])
+                  for t in range(len(counts)))
+        # rooted collectives
+        n = 4099
+        x, o = ctx.alloc([n]), ctx.alloc([n])
+        xs = np.random.default_rng(3).uniform(-1, 1, (world, n)).astype(np.float32)
+        ctx.view(x).copy_(torch.from_numpy(xs[rank]))
+        torch.cuda.synchronize()
+        dist.barrier()
+        reduce(ctx, x, o, root=world - 1)
+        ctx.check()
+        acc = xs[0].copy()
+        for r in range(1, world):
+            acc = (acc + xs[r]).astype(np.float32)
+        got = ctx.view(o).cpu().numpy()
+        ok_red = np.array_equal(got, acc if rank == world - 1 else np.zeros(n, np.float32))
+        dist.barrier()
+        broadcast(ctx, x, o, root=0)
+        ctx.check()
+        ok_bc = np.array_equal(ctx.view(o).cpu().numpy(), xs[0])
+        dist.barrier()
+        ctx.close()
+        q.put((rank, same, dev, ok_red, ok_bc, None))
+    except Exception as e:  # report, don't hang the parent
+        q.put((rank, False, 1.0, False, False, repr(e)))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_distributed_lamb_schedules_and_rooted(world):
+    counts = [3000, 1024, 77, 5000, 12_000]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_lamb_rooted, args=(r, world, port, counts, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=300) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=120)
+    for rank, same, dev, ok_red, ok_bc, err in res:
+        assert err is None, err
+        assert same, f"rank {rank}: STREAMED differs from GRID across processes"
+        assert dev <= 1e-5, f"rank {rank}: LAMB deviates {dev}"
+        assert ok_red and ok_bc, f"rank {rank}: reduce {ok_red} broadcast {ok_bc}"
