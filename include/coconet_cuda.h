@@ -208,8 +208,14 @@ typedef struct {
  * order, one small CTA per segment; a tensor's pass 2 is scheduled lag_elems
  * of pass-1 work after its pass 1 and waits only on that tensor's norms
  * (per-tensor completion counters, cross-rank ready flags), so part of its
- * m, v, p re-reads hit L2. AUTO = GRID, measured faster on B200. */
-enum coconet_lamb_sched { COCONET_LAMB_AUTO = 0, COCONET_LAMB_GRID = 1, COCONET_LAMB_STREAMED = 2 };
+ * m, v, p re-reads hit L2. AUTO = TMA at group size 1, GRID otherwise. */
+enum coconet_lamb_sched {
+  COCONET_LAMB_AUTO = 0,
+  COCONET_LAMB_GRID = 1,
+  COCONET_LAMB_STREAMED = 2,
+  COCONET_LAMB_TMA = 3 /* GRID's two passes fed by TMA bulk copies into a shared-memory ring
+                          (group size 1; norms summed in a different fixed order) */
+};
 
 int coconet_fused_rs_lamb_ag(coconet_ctx_t ctx, coconet_tlist_t tl, const void* const* g,
                              int g_elem, float* const* p, float* m_shard, float* v_shard,

@@ -32,6 +32,7 @@
 #include <cmath>
 
 #include "fused_opt.h"
+#include "pipeline.cuh"
 
 namespace cg = cooperative_groups;
 using namespace coconet;
@@ -490,6 +491,261 @@ __global__ void __launch_bounds__(kThreads, MINB) lamb_kernel(OptArgs a, LambK k
           for (int j = 0; j < Ranks<WT>::kMax; ++j)
             if (Ranks<WT>::has(j, W)) st4m(reinterpret_cast<float*>(s_base[j] + poff) + e0, pn, lo, hi);
         }
+      }
+    }
+  }
+  rank_barrier(rs, 1);
+}
+
+// ---- LAMB, TMA schedule (W = 1): the GRID algorithm with its two streaming
+// passes fed by the TMA engine. One persistent CTA per SM: warp 8 (one
+// elected lane) walks the CTA's segments and issues cp.async.bulk copies of
+// each 1024-element chunk of g, m, v, p into a ring of shared-memory stages
+// (mbarrier complete_tx); warps 0-7 consume a chunk per stage, one quad per
+// thread, write m, v (pass 1) or p (pass 2) straight to global memory and
+// release the stage. Tens of KB per SM stay in flight without spending
+// registers, which is what bounds the LDG kernel at 25% occupancy.
+// Per-segment norm partials are summed in a fixed order (deterministic, not
+// bit-identical to GRID's lane order); the per-tensor totals, the grid-wide
+// syncs and the exchange are GRID's.
+constexpr int kTmaConsumerWarps = 8;
+constexpr int kTmaThreads = (kTmaConsumerWarps + 1) * 32;
+constexpr int kTmaChunkQ = kTmaConsumerWarps * 32;  // quads per chunk (1024 elements)
+
+template <typename G>
+struct TmaStage {
+  static constexpr int G_BYTES = (kTmaChunkQ * 4 * int(sizeof(G)) + 16 + 15) / 16 * 16;  // + alignment slack
+  static constexpr int A_BYTES = kTmaChunkQ * 16;                                      // m, v, p
+  static constexpr int BYTES = G_BYTES + 3 * A_BYTES;
+};
+
+struct TmaArgs {
+  int stages;
+};
+
+// 32 segment descriptors of a CTA's list loaded at once by a warp (lane i:
+// segment base + i*stride) and handed out with shuffles, so the
+// descriptor -> tensor-offset chain costs one latency per 32 segments.
+struct SegBatch {
+  int64_t toff, sidx, aoff, boff;
+  int len, tensor;
+  __device__ __forceinline__ void load(const OptArgs& a, int64_t s, int64_t se) {
+    if (s < se) {
+      const Seg sg = a.segs[s];
+      toff = sg.toff;
+      sidx = sg.sidx;
+      len = meta_len(sg.meta);
+      tensor = meta_tensor(sg.meta);
+      aoff = a.offs[tensor];
+      boff = a.offs[a.n_tensors + tensor];
+    } else {
+      toff = sidx = aoff = boff = 0;
+      len = 0;
+      tensor = 0;
+    }
+  }
+  __device__ __forceinline__ SegD get(int j, int me) const {
+    const unsigned f = 0xffffffffu;
+    return SegD{__shfl_sync(f, toff, j), __shfl_sync(f, sidx, j), __shfl_sync(f, aoff, j), __shfl_sync(f, boff, j),
+                __shfl_sync(f, len, j), me, __shfl_sync(f, tensor, j)};
+  }
+};
+
+template <typename G>
+__global__ void __launch_bounds__(kTmaThreads) lamb_tma_kernel(OptArgs a, LambK k, TmaArgs ta) {
+  using ST = TmaStage<G>;
+  extern __shared__ __align__(128) uint8_t smem_raw[];
+  __shared__ char* s_base[kMaxRanks];
+  __shared__ float s_red[2][kTmaConsumerWarps][2];
+  const RankSet& rs = a.rs;
+  if (threadIdx.x < kMaxRanks) s_base[threadIdx.x] = threadIdx.x < rs.world ? rs.base[threadIdx.x] : nullptr;
+  const int S = ta.stages;
+  uint8_t* stage0 = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
+  uint64_t* full = reinterpret_cast<uint64_t*>(stage0 + size_t(S) * ST::BYTES);
+  uint64_t* empty = full + S;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < S; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], kTmaConsumerWarps);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  const int me = rs.rank();
+  const bool ok = rank_barrier(rs, 0);  // also publishes the barrier inits to the CTA
+  const int64_t sb = a.seg_begin[me], se = ok ? a.seg_begin[me + 1] : sb;
+  float* m = reinterpret_cast<float*>(s_base[me] + a.m_off);
+  float* v = reinterpret_cast<float*>(s_base[me] + a.v_off);
+  char* pme = s_base[me];
+  const bool producer = warp == kTmaConsumerWarps;
+  const int ctid = threadIdx.x;  // consumer thread 0..255
+  uint32_t st = 0, ph = 0;       // ring slot and phase of the next chunk (both roles advance identically)
+  for (int pass = 0; pass < 2; ++pass) {
+    if (pass == 1) {
+      // ---- between the passes: per-tensor partials -> exchange -> totals (GRID)
+      __threadfence();
+      cg::this_grid().sync();
+      const int64_t xch_off = int64_t(group_area(rs.group));
+      const int64_t wstride = int64_t(gridDim.x) * (kTmaThreads / 32);
+      const int64_t wid = int64_t(blockIdx.x) * (kTmaThreads / 32) + warp;
+      for (int64_t t = ok ? wid : a.n_tensors; t < a.n_tensors; t += wstride) {
+        const int64_t* ptr = k.csr_ptr + k.csr_begin[me];
+        const int64_t b = ptr[t], e = ptr[t + 1];
+        double sp = 0.0, su = 0.0;
+        for (int64_t i = b + lane; i < e; i += 32) {
+          const int64_t s = k.csr_idx[i];
+          sp += k.seg_part[2 * s];
+          su += k.seg_part[2 * s + 1];
+        }
+        sp = warp_sum(sp);
+        su = warp_sum(su);
+        if (lane == 0) {
+          double* xq = reinterpret_cast<double*>(s_base[me] + xch_off);
+          xq[(int64_t(me) * a.n_tensors + t) * 2] = sp;
+          xq[(int64_t(me) * a.n_tensors + t) * 2 + 1] = su;
+        }
+      }
+      __threadfence();
+      cg::this_grid().sync();
+    }
+    const double* xch_me = reinterpret_cast<const double*>(s_base[me] + group_area(rs.group));
+    if (producer) {
+      const int64_t st32 = int64_t(gridDim.x) * 32;
+      for (int64_t s0 = sb + blockIdx.x; s0 < se; s0 += st32) {
+        SegBatch batch;
+        batch.load(a, s0 + int64_t(lane) * gridDim.x, se);
+        for (int j = 0; j < 32; ++j) {
+          if (s0 + int64_t(j) * gridDim.x >= se) break;
+          const SegD d = batch.get(j, me);
+          if (lane != 0) continue;
+          const int64_t q0 = d.toff >> 2, q1 = (d.toff + d.len + 3) >> 2;
+          for (int64_t qa = q0; qa < q1; qa += kTmaChunkQ) {
+            const int64_t qb = min(qa + int64_t(kTmaChunkQ), q1);
+            mbar_wait(&empty[st], ph ^ 1u);
+            uint8_t* dst = stage0 + size_t(st) * ST::BYTES;
+            const uint32_t abytes = uint32_t(qb - qa) * 16u;
+            const char* ga = s_base[me] + d.aoff + qa * 4 * int64_t(sizeof(G));
+            const char* g0 = reinterpret_cast<const char*>(reinterpret_cast<uintptr_t>(ga) & ~uintptr_t(15));
+            const char* g1 = reinterpret_cast<const char*>(
+                (reinterpret_cast<uintptr_t>(s_base[me] + d.aoff + qb * 4 * int64_t(sizeof(G))) + 15) &
+                ~uintptr_t(15));
+            const uint32_t gbytes = pass == 0 ? uint32_t(g1 - g0) : 0u;
+            const int64_t si = d.sidx + (qa * 4 - d.toff);
+            mbar_expect_tx(&full[st], gbytes + 3u * abytes);
+            if (pass == 0) bulk_load(dst, g0, gbytes, &full[st]);
+            bulk_load(dst + ST::G_BYTES, m + si, abytes, &full[st]);
+            bulk_load(dst + ST::G_BYTES + ST::A_BYTES, v + si, abytes, &full[st]);
+            bulk_load(dst + ST::G_BYTES + 2 * ST::A_BYTES, pme + d.boff + qa * 16, abytes, &full[st]);
+            if (++st == uint32_t(S)) {
+              st = 0;
+              ph ^= 1u;
+            }
+          }
+        }
+      }
+      __syncwarp();
+      st = __shfl_sync(0xffffffffu, st, 0);
+      ph = __shfl_sync(0xffffffffu, ph, 0);
+    } else {
+      int red = 0;  // s_red buffer of the next segment reduction
+      const int64_t st32 = int64_t(gridDim.x) * 32;
+      for (int64_t s0 = sb + blockIdx.x; s0 < se; s0 += st32) {
+       SegBatch batch;
+       batch.load(a, s0 + int64_t(lane) * gridDim.x, se);
+       for (int j = 0; j < 32; ++j) {
+        const int64_t s = s0 + int64_t(j) * gridDim.x;
+        if (s >= se) break;
+        const SegD d = batch.get(j, me);
+        const int tens = d.tensor;
+        const int64_t aoff = d.aoff, boff = d.boff;
+        const int64_t q0 = d.toff >> 2, q1 = (d.toff + d.len + 3) >> 2;
+        float ratio = 0.f;
+        if (pass == 1) {
+          const double P = __ldcg(xch_me + (int64_t(me) * a.n_tensors + tens) * 2);
+          const double U = __ldcg(xch_me + (int64_t(me) * a.n_tensors + tens) * 2 + 1);
+          ratio = float((k.lr * sqrt(P)) / sqrt(U));
+        }
+        float sp = 0.f, su = 0.f;
+        for (int64_t qa = q0; qa < q1; qa += kTmaChunkQ) {
+          const int64_t qb = min(qa + int64_t(kTmaChunkQ), q1);
+          mbar_wait(&full[st], ph);
+          const uint8_t* src = stage0 + size_t(st) * ST::BYTES;
+          const int64_t q = qa + ctid;
+          if (q < qb) {
+            const int64_t e0 = q << 2;
+            int lo, hi;
+            quad_range(d, e0, lo, hi);
+            const int64_t si = d.sidx + (e0 - d.toff);
+            const float4 mq = *reinterpret_cast<const float4*>(src + ST::G_BYTES + (q - qa) * 16);
+            const float4 vq = *reinterpret_cast<const float4*>(src + ST::G_BYTES + ST::A_BYTES + (q - qa) * 16);
+            const float4 pq = *reinterpret_cast<const float4*>(src + ST::G_BYTES + 2 * ST::A_BYTES + (q - qa) * 16);
+            float mm[4] = {mq.x, mq.y, mq.z, mq.w}, vv[4] = {vq.x, vq.y, vq.z, vq.w}, pp[4] = {pq.x, pq.y, pq.z, pq.w};
+            if (pass == 0) {
+              const uintptr_t ga = reinterpret_cast<uintptr_t>(s_base[me] + aoff + qa * 4 * int64_t(sizeof(G)));
+              const uintptr_t goff = (ga & 15u) + uintptr_t(q - qa) * 4u * sizeof(G);
+              float gs[4];
+              if constexpr (sizeof(G) == 4) {
+                const float4 gq = *reinterpret_cast<const float4*>(src + goff);
+                gs[0] = gq.x; gs[1] = gq.y; gs[2] = gq.z; gs[3] = gq.w;
+              } else {
+                const uint2 gq = *reinterpret_cast<const uint2*>(src + goff);
+                const G* h = reinterpret_cast<const G*>(&gq);
+#pragma unroll
+                for (int i = 0; i < 4; ++i) gs[i] = to_f32(h[i]);
+              }
+              float fp = 0.f, fu = 0.f;
+#pragma unroll
+              for (int i = 0; i < 4; ++i) {
+                const float mn = fmaf(k.fcm, gs[i], mm[i] * k.fb1);
+                const float vn = fmaf(k.fcv * gs[i], gs[i], vv[i] * k.fb2);
+                mm[i] = mn;
+                vv[i] = vn;
+                if (i >= lo && i < hi) {
+                  const float uu = lamb_u(mn, vn, pp[i], k);
+                  fp = fmaf(pp[i], pp[i], fp);
+                  fu = fmaf(uu, uu, fu);
+                }
+              }
+              sp += fp;
+              su += fu;
+              st4m(m + si, mm, lo, hi);
+              st4m(v + si, vv, lo, hi);
+            } else {
+              float pn[4];
+#pragma unroll
+              for (int i = 0; i < 4; ++i) pn[i] = pp[i] - ratio * lamb_u(mm[i], vv[i], pp[i], k);
+              st4m(reinterpret_cast<float*>(pme + boff) + e0, pn, lo, hi);
+            }
+          }
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&empty[st]);
+          if (++st == uint32_t(S)) {
+            st = 0;
+            ph ^= 1u;
+          }
+        }
+        if (pass == 0) {  // segment partial: fixed-order sum over the 256 consumer threads
+          sp = warp_sumf(sp);
+          su = warp_sumf(su);
+          if (lane == 0) {
+            s_red[red][warp][0] = sp;
+            s_red[red][warp][1] = su;
+          }
+          asm volatile("bar.sync 1, %0;" ::"n"(kTmaConsumerWarps * 32) : "memory");
+          if (ctid == 0) {
+            float tp = 0.f, tu = 0.f;
+#pragma unroll
+            for (int w = 0; w < kTmaConsumerWarps; ++w) {
+              tp += s_red[red][w][0];
+              tu += s_red[red][w][1];
+            }
+            k.seg_part[2 * s] = double(tp);
+            k.seg_part[2 * s + 1] = double(tu);
+          }
+          red ^= 1;
+        }
+       }
       }
     }
   }
@@ -979,7 +1235,7 @@ int coconet_fused_rs_lamb_ag(coconet_ctx_t c, coconet_tlist_t tl, const void* co
     return set_error(COCONET_ERR_UNSUPPORTED,
                      "LAMB runs in FAST math only: its whole-tensor sums cannot reproduce the "
                      "reference's sequential double accumulation bit-for-bit");
-  if (hp->sched < COCONET_LAMB_AUTO || hp->sched > COCONET_LAMB_STREAMED)
+  if (hp->sched < COCONET_LAMB_AUTO || hp->sched > COCONET_LAMB_TMA)
     return set_error(COCONET_ERR_INVALID_INPUT, "bad LAMB schedule");
   // exchange [rank][tensor] (P, U) doubles + ready flags [rank][tensor]
   if (size_t(kMaxRanks) * tl->n_tensors * (2 * sizeof(double) + sizeof(uint32_t)) > kTileFlagsOff)
@@ -1010,8 +1266,29 @@ int coconet_fused_rs_lamb_ag(coconet_ctx_t c, coconet_tlist_t tl, const void* co
   if (rc) return rc;
   OptArgs a;
   fill_args(tl, &a, rs, m_off, v_off);
-  // AUTO = GRID: measured faster on B200 ("STREAMED schedule")
-  if (hp->sched != COCONET_LAMB_STREAMED) {
+  // AUTO: TMA at W = 1, GRID otherwise
+  const int sched = hp->sched == COCONET_LAMB_AUTO ? (W == 1 ? COCONET_LAMB_TMA : COCONET_LAMB_GRID) : hp->sched;
+  if (sched == COCONET_LAMB_TMA) {
+    if (W != 1) return set_error(COCONET_ERR_UNSUPPORTED, "the TMA LAMB schedule runs at group size 1");
+    const bool f32 = g_elem == COCONET_F32;
+    const int sbytes = f32 ? TmaStage<float>::BYTES : TmaStage<__half>::BYTES;
+    TmaArgs ta;
+    // COCONET_LAMB_TMA_CTAS: CTAs per SM (probe; each gets 1/n of the ring)
+    const char* ce = getenv("COCONET_LAMB_TMA_CTAS");
+    const int per_sm = ce ? std::max(1, std::min(4, atoi(ce))) : 2;  // 2: measured best
+    ta.stages = std::min(16, (200 << 10) / per_sm / sbytes);
+    const size_t smem = size_t(ta.stages) * size_t(sbytes) + size_t(ta.stages) * 16 + 128;
+    const void* fn = f32 ? reinterpret_cast<const void*>(&lamb_tma_kernel<float>)
+                     : g_elem == COCONET_F16 ? reinterpret_cast<const void*>(&lamb_tma_kernel<__half>)
+                                             : reinterpret_cast<const void*>(&lamb_tma_kernel<__nv_bfloat16>);
+    CN_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    int blocks = 0;
+    rc = coop_blocks(c, fn, kTmaThreads, smem, tl->group, int64_t(c->sm_count) * per_sm, &blocks);
+    if (rc) return rc;
+    void* args[] = {&a, &k, &ta};
+    return coop_launch(c, fn, dim3(unsigned(blocks), 1u), dim3(kTmaThreads), args, smem, stream);
+  }
+  if (sched == COCONET_LAMB_GRID) {
     const void* fn = g_elem == COCONET_F32   ? lamb_pick<float>(W)
                      : g_elem == COCONET_F16 ? lamb_pick<__half>(W)
                                              : lamb_pick<__nv_bfloat16>(W);

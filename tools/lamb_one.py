@@ -12,7 +12,7 @@ from paper_2105_05720_b200.collectives import LambHParams, TensorList, fused_rs_
 from paper_2105_05720_b200.runtime import Context  # noqa: E402
 from paper_2105_05720_b200.workloads import bert_large_counts  # noqa: E402
 
-sched = {"grid": _lib.LAMB_GRID, "stream": _lib.LAMB_STREAMED}[sys.argv[1]]
+sched = {"grid": _lib.LAMB_GRID, "stream": _lib.LAMB_STREAMED, "tma": _lib.LAMB_TMA}[sys.argv[1]]
 cap, wave = int(sys.argv[2]), int(sys.argv[3])
 steps = int(sys.argv[4]) if len(sys.argv) > 4 else 4
 counts = bert_large_counts()

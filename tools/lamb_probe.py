@@ -22,7 +22,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--caps", default="1024,4096")
-    ap.add_argument("--waves", default="524288,1048576,2097152,4194304,8388608")
+    ap.add_argument("--waves", default="")
     args = ap.parse_args()
     counts = bert_large_counts()
     N = sum(counts)
@@ -45,8 +45,8 @@ def main():
             return torch.cat([ctx.view(p, 0) for p in params] + [ctx.view(m, 0), ctx.view(v, 0)]).clone()
 
         ref = None
-        configs = [("grid", _lib.LAMB_GRID, 0)] + [(f"stream_lag{w}", _lib.LAMB_STREAMED, int(w))
-                                                   for w in args.waves.split(",")]
+        configs = [("grid", _lib.LAMB_GRID, 0), ("tma", _lib.LAMB_TMA, 0)] + [
+            (f"stream_lag{w}", _lib.LAMB_STREAMED, int(w)) for w in args.waves.split(",") if w]
         for name, sched, wave in configs:
             hp = LambHParams(lr=1e-3, beta1=0.9, beta2=0.999, t=1.0, sched=sched, lag_elems=wave)
             reset()
@@ -56,11 +56,12 @@ def main():
             if ref is None:
                 ref = snap
             same = bool(torch.equal(snap, ref))
-            del snap
+            snap_f = snap
             ms = timeit(lambda: fused_rs_lamb_ag(ctx, tl, grads, params, m, v, hp), args.steps)
             ctx.check()
             out[f"cap{cap}_{name}"] = {"ms": ms, "GBs_at_26B": 26 * N / ms / 1e6,
                                        "GBs_at_38B": 38 * N / ms / 1e6, "bit_identical_to_grid": same,
+                                       "max_abs_diff_vs_grid": float((snap_f - ref).abs().max()),
                                        "lag": wave if sched == _lib.LAMB_STREAMED else None}
             print(json.dumps({f"cap{cap}_{name}": out[f"cap{cap}_{name}"]}), flush=True)
         del ref
