@@ -36,7 +36,7 @@ sys.path.insert(0, str(ROOT))
 METRIC = "fused AR+Adam/LAMB step time & NVLink-roofline fraction, 1/2/4/8 B200"
 UNIT = "Gelem/s"
 NVLINK_GBS = 770.0  # measured peer copy per direction (B200_PROFILING.md)
-BUCKET_CAP = 4096
+BUCKET_CAP = 16384  # segments of the TMA LAMB schedule
 E2E_GROUPS = 16  # tensor groups pipelined against PCIe in the e2e measurement
 CPU_SAMPLE = 1 << 22  # elements per core for cpu_baseline: ~10-30 s of CPU work
 

@@ -28,6 +28,7 @@
 #include <cooperative_groups.h>
 
 #include <algorithm>
+#include <type_traits>
 #include <cstdlib>
 #include <cmath>
 
@@ -502,20 +503,19 @@ __global__ void __launch_bounds__(kThreads, MINB) lamb_kernel(OptArgs a, LambK k
 // elected lane) walks the CTA's segments and issues cp.async.bulk copies of
 // each 1024-element chunk of g, m, v, p into a ring of shared-memory stages
 // (mbarrier complete_tx); warps 0-7 consume a chunk per stage, one quad per
-// thread, write m, v (pass 1) or p (pass 2) straight to global memory and
-// release the stage. Tens of KB per SM stay in flight without spending
+// thread... (QPT quads per thread), write m, v (pass 1) or p (pass 2)
+// straight to global memory and release the stage. Tens of KB per SM stay in flight without spending
 // registers, which is what bounds the LDG kernel at 25% occupancy.
 // Per-segment norm partials are summed in a fixed order (deterministic, not
 // bit-identical to GRID's lane order); the per-tensor totals, the grid-wide
 // syncs and the exchange are GRID's.
-constexpr int kTmaConsumerWarps = 8;
-constexpr int kTmaThreads = (kTmaConsumerWarps + 1) * 32;
-constexpr int kTmaChunkQ = kTmaConsumerWarps * 32;  // quads per chunk (1024 elements)
-
-template <typename G>
+// NW consumer warps, QPT quads per consumer thread per chunk.
+template <typename G, int NW, int QPT>
 struct TmaStage {
-  static constexpr int G_BYTES = (kTmaChunkQ * 4 * int(sizeof(G)) + 16 + 15) / 16 * 16;  // + alignment slack
-  static constexpr int A_BYTES = kTmaChunkQ * 16;                                      // m, v, p
+  static constexpr int THREADS = (NW + 1) * 32;
+  static constexpr int CHUNK_Q = NW * 32 * QPT;                                      // quads per chunk
+  static constexpr int G_BYTES = (CHUNK_Q * 4 * int(sizeof(G)) + 16 + 15) / 16 * 16;  // + alignment slack
+  static constexpr int A_BYTES = CHUNK_Q * 16;                                       // m, v, p
   static constexpr int BYTES = G_BYTES + 3 * A_BYTES;
 };
 
@@ -551,12 +551,15 @@ struct SegBatch {
   }
 };
 
-template <typename G>
-__global__ void __launch_bounds__(kTmaThreads) lamb_tma_kernel(OptArgs a, LambK k, TmaArgs ta) {
-  using ST = TmaStage<G>;
+template <typename G, int NW, int QPT>
+__global__ void __launch_bounds__((NW + 1) * 32) lamb_tma_kernel(OptArgs a, LambK k, TmaArgs ta) {
+  using ST = TmaStage<G, NW, QPT>;
+  constexpr int kTmaConsumerWarps = NW;
+  constexpr int kTmaThreads = ST::THREADS;
+  constexpr int kTmaChunkQ = ST::CHUNK_Q;
   extern __shared__ __align__(128) uint8_t smem_raw[];
   __shared__ char* s_base[kMaxRanks];
-  __shared__ float s_red[2][kTmaConsumerWarps][2];
+  __shared__ float s_red[2][NW][2];
   const RankSet& rs = a.rs;
   if (threadIdx.x < kMaxRanks) s_base[threadIdx.x] = threadIdx.x < rs.world ? rs.base[threadIdx.x] : nullptr;
   const int S = ta.stages;
@@ -671,7 +674,9 @@ __global__ void __launch_bounds__(kTmaThreads) lamb_tma_kernel(OptArgs a, LambK 
           const int64_t qb = min(qa + int64_t(kTmaChunkQ), q1);
           mbar_wait(&full[st], ph);
           const uint8_t* src = stage0 + size_t(st) * ST::BYTES;
-          const int64_t q = qa + ctid;
+#pragma unroll
+          for (int qq = 0; qq < QPT; ++qq) {
+          const int64_t q = qa + ctid + qq * (NW * 32);
           if (q < qb) {
             const int64_t e0 = q << 2;
             int lo, hi;
@@ -718,6 +723,7 @@ __global__ void __launch_bounds__(kTmaThreads) lamb_tma_kernel(OptArgs a, LambK 
               st4m(reinterpret_cast<float*>(pme + boff) + e0, pn, lo, hi);
             }
           }
+          }
           __syncwarp();
           if (lane == 0) mbar_arrive(&empty[st]);
           if (++st == uint32_t(S)) {
@@ -732,7 +738,7 @@ __global__ void __launch_bounds__(kTmaThreads) lamb_tma_kernel(OptArgs a, LambK 
             s_red[red][warp][0] = sp;
             s_red[red][warp][1] = su;
           }
-          asm volatile("bar.sync 1, %0;" ::"n"(kTmaConsumerWarps * 32) : "memory");
+          asm volatile("bar.sync 1, %0;" ::"n"(NW * 32) : "memory");
           if (ctid == 0) {
             float tp = 0.f, tu = 0.f;
 #pragma unroll
@@ -1270,23 +1276,48 @@ int coconet_fused_rs_lamb_ag(coconet_ctx_t c, coconet_tlist_t tl, const void* co
   const int sched = hp->sched == COCONET_LAMB_AUTO ? (W == 1 ? COCONET_LAMB_TMA : COCONET_LAMB_GRID) : hp->sched;
   if (sched == COCONET_LAMB_TMA) {
     if (W != 1) return set_error(COCONET_ERR_UNSUPPORTED, "the TMA LAMB schedule runs at group size 1");
-    const bool f32 = g_elem == COCONET_F32;
-    const int sbytes = f32 ? TmaStage<float>::BYTES : TmaStage<__half>::BYTES;
-    TmaArgs ta;
-    // COCONET_LAMB_TMA_CTAS: CTAs per SM (probe; each gets 1/n of the ring)
+    // COCONET_LAMB_TMA_CTAS / _SHAPE: CTAs per SM and consumer shape (probes)
     const char* ce = getenv("COCONET_LAMB_TMA_CTAS");
-    const int per_sm = ce ? std::max(1, std::min(4, atoi(ce))) : 2;  // 2: measured best
+    const char* sh = getenv("COCONET_LAMB_TMA_SHAPE");
+    // defaults measured on B200 (profiles/r01_lamb_tma_sweep.json): 8 consumer warps x 2 quads
+    // per thread (2048-element chunks), 3 CTAs per SM
+    const int per_sm = ce ? std::max(1, std::min(4, atoi(ce))) : 3;
+    const int shape = sh ? atoi(sh) : 1;  // 0: 8 warps x 1 quad, 1: 8 x 2, 2: 16 x 1, 3: 4 x 2
+    const void* fn = nullptr;
+    int sbytes = 0, threads = 0;
+    auto pick = [&](auto tag_g, auto tag_nw, auto tag_q) {
+      using Gt = decltype(tag_g);
+      constexpr int NW = decltype(tag_nw)::value, Q = decltype(tag_q)::value;
+      fn = reinterpret_cast<const void*>(&lamb_tma_kernel<Gt, NW, Q>);
+      sbytes = TmaStage<Gt, NW, Q>::BYTES;
+      threads = TmaStage<Gt, NW, Q>::THREADS;
+    };
+    auto pick_g = [&](auto tag_g) {
+      using I8 = std::integral_constant<int, 8>;
+      using I16 = std::integral_constant<int, 16>;
+      using I4 = std::integral_constant<int, 4>;
+      using Q1 = std::integral_constant<int, 1>;
+      using Q2 = std::integral_constant<int, 2>;
+      switch (shape) {
+        case 0: pick(tag_g, I8{}, Q1{}); break;
+        case 2: pick(tag_g, I16{}, Q1{}); break;
+        case 3: pick(tag_g, I4{}, Q2{}); break;
+        default: pick(tag_g, I8{}, Q2{}); break;
+      }
+    };
+    if (g_elem == COCONET_F32) pick_g(float{});
+    else if (g_elem == COCONET_F16) pick_g(__half{});
+    else pick_g(__nv_bfloat16{});
+    TmaArgs ta;
     ta.stages = std::min(16, (200 << 10) / per_sm / sbytes);
+    if (ta.stages < 2) return set_error(COCONET_ERR_UNSUPPORTED, "TMA ring does not fit");
     const size_t smem = size_t(ta.stages) * size_t(sbytes) + size_t(ta.stages) * 16 + 128;
-    const void* fn = f32 ? reinterpret_cast<const void*>(&lamb_tma_kernel<float>)
-                     : g_elem == COCONET_F16 ? reinterpret_cast<const void*>(&lamb_tma_kernel<__half>)
-                                             : reinterpret_cast<const void*>(&lamb_tma_kernel<__nv_bfloat16>);
     CN_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     int blocks = 0;
-    rc = coop_blocks(c, fn, kTmaThreads, smem, tl->group, int64_t(c->sm_count) * per_sm, &blocks);
+    rc = coop_blocks(c, fn, threads, smem, tl->group, int64_t(c->sm_count) * per_sm, &blocks);
     if (rc) return rc;
     void* args[] = {&a, &k, &ta};
-    return coop_launch(c, fn, dim3(unsigned(blocks), 1u), dim3(kTmaThreads), args, smem, stream);
+    return coop_launch(c, fn, dim3(unsigned(blocks), 1u), dim3(unsigned(threads)), args, smem, stream);
   }
   if (sched == COCONET_LAMB_GRID) {
     const void* fn = g_elem == COCONET_F32   ? lamb_pick<float>(W)
