@@ -165,6 +165,27 @@ def _worker_lamb_rooted(rank, world, port, counts, q):
         gr = co.unflatten_bucket_order(co.ring_reduce(flat, owner), counts, table)
         dev = max(co.max_rel_deviation(outs[_lib.LAMB_STREAMED][1][t], co.lamb_oracle(gr[t], m[t], v[t], p[t], k)[2])
                   for t in range(len(counts)))
+        # a size-1 subgroup inside DISTRIBUTED mode (the bench's NCCL-baseline
+        # leg): AUTO picks the TMA schedule; m, v equal GRID's bitwise
+        g1 = ctx.group(rank, 1)
+        local = {}
+        for sched in (_lib.LAMB_AUTO, _lib.LAMB_GRID):
+            tl1 = TensorList(ctx, counts, group=g1, bucket_cap=4096)
+            gb = [ctx.alloc([n]) for n in counts]
+            pb = [ctx.alloc([n]) for n in counts]
+            mb, vb = ctx.alloc([tl1.shard_elems]), ctx.alloc([tl1.shard_elems])
+            for t in range(len(counts)):
+                ctx.view(gb[t]).copy_(torch.from_numpy(g[t][rank]))
+                ctx.view(pb[t]).copy_(torch.from_numpy(p[t]))
+            ctx.view(mb).zero_()
+            ctx.view(vb).fill_(0.05)
+            fused_rs_lamb_ag(ctx, tl1, gb, pb, mb, vb, LambHParams(lr=0.01, beta1=0.9, beta2=0.999, t=1.0, sched=sched))
+            ctx.check()
+            local[sched] = ([ctx.view(b).cpu().numpy() for b in pb], ctx.view(mb).cpu().numpy(), ctx.view(vb).cpu().numpy())
+        pa, ma, va = local[_lib.LAMB_AUTO]
+        pg, mg, vg = local[_lib.LAMB_GRID]
+        same = same and np.array_equal(ma, mg) and np.array_equal(va, vg)
+        dev = max(dev, max(co.max_rel_deviation(x, y) for x, y in zip(pa, pg)))
         # rooted collectives
         n = 4099
         x, o = ctx.alloc([n]), ctx.alloc([n])
