@@ -49,8 +49,11 @@ constexpr int kFusedThreads = 512;  // overlap kernel: 16 warps (0/1/4-7 GEMM ro
 constexpr int kFusedWarps = kFusedThreads / 32;
 constexpr int kUnitU = 2;           // quads per lane in flight in an all-reduce unit
 
+// Stage counts: the K=384 GEMM is bound by TMA bytes in flight, so the ring
+// takes all the shared memory the epilogue leaves (4 x 48 KB at BN = 256;
+// 3 stages: 193 us for C3's 8 ranks, 4 stages: 172 us).
 template <int BN> struct Cfg {
-  static constexpr int STAGES = BN == 256 ? 3 : 4;
+  static constexpr int STAGES = 4;
   static constexpr int A_BYTES = BM * BK * 2;
   static constexpr int B_BYTES = BN * BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
@@ -467,9 +470,18 @@ __global__ void __launch_bounds__(FUSED ? kFusedThreads : kGemmThreads, 1)
   }
 }
 
-// B [K, N] row-major -> BT [N, K] (K-major operand for the MMA)
+// B [K, N] row-major -> BT [N, K] (K-major operand for the MMA), every local
+// rank in one launch (blockIdx.z = rank; the pointer table stays in the
+// parameter space, __grid_constant__)
+struct TransposeArgs {
+  const uint16_t* b[kMaxRanks];
+  uint16_t* bt[kMaxRanks];
+};
+
 template <typename T>
-__global__ void transpose_kernel(const T* __restrict__ b, T* __restrict__ bt, int K, int N) {
+__global__ void transpose_kernel(const __grid_constant__ TransposeArgs ta, int K, int N) {
+  const T* __restrict__ b = reinterpret_cast<const T*>(ta.b[blockIdx.z]);
+  T* __restrict__ bt = reinterpret_cast<T*>(ta.bt[blockIdx.z]);
   __shared__ T tile[32][33];
   const int n0 = blockIdx.x * 32, k0 = blockIdx.y * 32;
   for (int i = threadIdx.y; i < 32; i += 8) {
@@ -610,14 +622,21 @@ int plan_tc(coconet_ctx* c, int group, const void* a, const void* b, void* cc, i
   if (rc) return rc;
   std::memset(&p->maps, 0, sizeof(p->maps));
   std::memset(&p->g, 0, sizeof(p->g));
+  TransposeArgs ta{};
+  for (int i = 0; i < nl; ++i) {
+    const int wr = c->mode == COCONET_MODE_VIRTUAL ? grp.first + i : c->rank;
+    ta.b[i] = reinterpret_cast<const uint16_t*>(c->heap[wr] + bo);
+    ta.bt[i] = reinterpret_cast<uint16_t*>(static_cast<char*>(scratch) + size_t(i) * size_t(n * k) * 2);
+  }
+  {
+    dim3 tb(32, 8), tg(unsigned((n + 31) / 32), unsigned((k + 31) / 32), unsigned(nl));
+    transpose_kernel<uint16_t><<<tg, tb, 0, s>>>(ta, int(k), int(n));
+    c->launches++;
+  }
   for (int i = 0; i < nl; ++i) {
     const int wr = c->mode == COCONET_MODE_VIRTUAL ? grp.first + i : c->rank;
     char* heap = c->heap[wr];
-    void* bt = static_cast<char*>(scratch) + size_t(i) * size_t(n * k) * 2;
-    dim3 tb(32, 8), tg(unsigned((n + 31) / 32), unsigned((k + 31) / 32));
-    transpose_kernel<uint16_t><<<tg, tb, 0, s>>>(reinterpret_cast<const uint16_t*>(heap + bo),
-                                                 reinterpret_cast<uint16_t*>(bt), int(k), int(n));
-    c->launches++;
+    void* bt = ta.bt[i];
     rc = make_map(&p->maps.a[i], heap + ao, in_elem, uint64_t(k), uint64_t(m), BK, BM);
     if (!rc) rc = make_map(&p->maps.b[i], bt, in_elem, uint64_t(k), uint64_t(n), BK, uint32_t(bn));
     if (!rc)
