@@ -101,6 +101,19 @@ __device__ __forceinline__ uint64_t sw128_desc(const void* p) {
   return ((addr >> 4) & 0x3FFFull) | (1ull << 16) | (64ull << 32) | (1ull << 46) | (2ull << 61);
 }
 
+// MN-major operand tile [64 k x BN] bf16 loaded as BN/64 TMA boxes of
+// [64 k rows x 64 n] (128-byte swizzle, 1 KB per 8 k-rows): the canonical
+// UMMA MN-major SW128 layout ((T,8,m),(8,k)) : ((1,T,LBO),(8T,SBO)) with
+// LBO = 8 KB (next 64 n) and SBO = 1 KB (next 8 k), version 1 (CUTLASS
+// make_umma_desc<Major::MN>). B is read in its natural row-major [K, N]
+// layout: no transpose.
+constexpr int kMnBlockBytes = 64 * 64 * 2;
+__device__ __forceinline__ uint64_t sw128_mn_desc(const void* p) {
+  const uint64_t addr = smem_u32(p);
+  return ((addr >> 4) & 0x3FFFull) | (uint64_t(kMnBlockBytes >> 4) << 16) | (64ull << 32) | (1ull << 46) |
+         (2ull << 61);
+}
+
 __device__ __forceinline__ void mma_f16(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
   asm volatile(
       "{\n"
@@ -130,10 +143,11 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
 }
 
 // instruction descriptor: kind::f16, A/B = in_fmt (0 f16, 1 bf16), D = f32,
-// both K-major, M = 128, N = BN
+// A K-major, B MN-major (bit 16), M = 128, N = BN
 template <int BN>
 __device__ __forceinline__ uint32_t make_idesc(uint32_t in_fmt) {
-  return (1u << 4) | (in_fmt << 7) | (in_fmt << 10) | (uint32_t(BN >> 3) << 17) | (uint32_t(BM >> 4) << 24);
+  return (1u << 4) | (in_fmt << 7) | (in_fmt << 10) | (1u << 16) | (uint32_t(BN >> 3) << 17) |
+         (uint32_t(BM >> 4) << 24);
 }
 
 template <typename TO>
@@ -340,7 +354,10 @@ __global__ void __launch_bounds__(FUSED ? kFusedThreads : kGemmThreads, 1)
           uint8_t* sa = smem + stage * Cfg<BN>::STAGE_BYTES;
           mbar_expect_tx(&full[stage], Cfg<BN>::STAGE_BYTES);
           tma_load_2d(sa, &maps.a[r], kb * BK, mt * BM, &full[stage]);
-          tma_load_2d(sa + Cfg<BN>::A_BYTES, &maps.b[r], kb * BK, nt * BN, &full[stage]);
+#pragma unroll
+          for (int j = 0; j < BN / 64; ++j)  // B [K, N] row-major: 64 n x 64 k boxes
+            tma_load_2d(sa + Cfg<BN>::A_BYTES + j * kMnBlockBytes, &maps.b[r], nt * BN + j * 64, kb * BK,
+                        &full[stage]);
           if (++stage == Cfg<BN>::STAGES) {
             stage = 0;
             phase ^= 1;
@@ -367,10 +384,10 @@ __global__ void __launch_bounds__(FUSED ? kFusedThreads : kGemmThreads, 1)
           mbar_wait(&full[stage], phase);
           tc_fence_after();
           const uint8_t* sa = smem + stage * Cfg<BN>::STAGE_BYTES;
-          const uint64_t da = sw128_desc(sa), db = sw128_desc(sa + Cfg<BN>::A_BYTES);
+          const uint64_t da = sw128_desc(sa), db = sw128_mn_desc(sa + Cfg<BN>::A_BYTES);
 #pragma unroll
-          for (int k = 0; k < BK / 16; ++k)  // +32 bytes along K per UMMA_K = 16
-            mma_f16(d, da + 2 * k, db + 2 * k, idesc, (kb | k) != 0);
+          for (int k = 0; k < BK / 16; ++k)  // per UMMA_K = 16: A +32 bytes along K, B +16 k-rows (2 KB)
+            mma_f16(d, da + 2 * k, db + uint64_t(k) * ((16 * 128) >> 4), idesc, (kb | k) != 0);
           mma_commit(&empty[stage]);  // frees the smem stage once these MMAs retire
           if (++stage == Cfg<BN>::STAGES) {
             stage = 0;
@@ -470,31 +487,6 @@ __global__ void __launch_bounds__(FUSED ? kFusedThreads : kGemmThreads, 1)
   }
 }
 
-// B [K, N] row-major -> BT [N, K] (K-major operand for the MMA), every local
-// rank in one launch (blockIdx.z = rank; the pointer table stays in the
-// parameter space, __grid_constant__)
-struct TransposeArgs {
-  const uint16_t* b[kMaxRanks];
-  uint16_t* bt[kMaxRanks];
-};
-
-template <typename T>
-__global__ void transpose_kernel(const __grid_constant__ TransposeArgs ta, int K, int N) {
-  const T* __restrict__ b = reinterpret_cast<const T*>(ta.b[blockIdx.z]);
-  T* __restrict__ bt = reinterpret_cast<T*>(ta.bt[blockIdx.z]);
-  __shared__ T tile[32][33];
-  const int n0 = blockIdx.x * 32, k0 = blockIdx.y * 32;
-  for (int i = threadIdx.y; i < 32; i += 8) {
-    const int k = k0 + i, n = n0 + threadIdx.x;
-    if (k < K && n < N) tile[i][threadIdx.x] = b[int64_t(k) * N + n];
-  }
-  __syncthreads();
-  for (int i = threadIdx.y; i < 32; i += 8) {
-    const int n = n0 + i, k = k0 + threadIdx.x;
-    if (k < K && n < N) bt[int64_t(n) * K + k] = tile[threadIdx.x][i];
-  }
-}
-
 // EXACT: C = A x B with fp64 accumulation in k order (eval_matmul).
 struct ExactArgs {
   const float* a[kMaxRanks];
@@ -571,39 +563,14 @@ int make_map(CUtensorMap* map, const void* base, int elem, uint64_t inner, uint6
   return COCONET_OK;
 }
 
-// per-context scratch for transposed weights (grown on demand, never shrunk)
-struct Scratch {
-  void* p = nullptr;
-  size_t bytes = 0;
-};
-std::mutex g_scratch_mu;
-Scratch g_scratch[16];
-
-int scratch_for(coconet_ctx* c, size_t bytes, void** out) {
-  std::lock_guard<std::mutex> lk(g_scratch_mu);
-  Scratch& s = g_scratch[c->device & 15];
-  if (s.bytes < bytes) {
-    if (s.p) {
-      cudaDeviceSynchronize();
-      cudaFree(s.p);
-    }
-    s.p = nullptr;
-    s.bytes = 0;
-    CN_CUDA(cudaMalloc(&s.p, bytes));
-    s.bytes = bytes;
-  }
-  *out = s.p;
-  return COCONET_OK;
-}
-
 struct TcPlan {
   RankMaps maps;
   GemmArgs g;
   int bn;
 };
 
-// Prepares the tcgen05 launch for every local rank of `group`: transposes
-// each B into scratch and encodes the TMA maps.
+// Prepares the tcgen05 launch for every local rank of `group`: encodes the
+// TMA maps (A K-major, B read MN-major in place, C).
 int plan_tc(coconet_ctx* c, int group, const void* a, const void* b, void* cc, int in_elem, int out_elem, int64_t m,
             int64_t n, int64_t k, cudaStream_t s, TcPlan* p) {
   if (m % BM) return set_error(COCONET_ERR_UNSUPPORTED, "M must be a multiple of 128");
@@ -617,28 +584,14 @@ int plan_tc(coconet_ctx* c, int group, const void* a, const void* b, void* cc, i
   if (rc) return rc;
   const coconet_group_s& grp = c->groups[size_t(group)];
   const int nl = local_ranks(c, group);
-  void* scratch = nullptr;
-  rc = scratch_for(c, size_t(nl) * size_t(n * k) * 2, &scratch);
-  if (rc) return rc;
   std::memset(&p->maps, 0, sizeof(p->maps));
   std::memset(&p->g, 0, sizeof(p->g));
-  TransposeArgs ta{};
-  for (int i = 0; i < nl; ++i) {
-    const int wr = c->mode == COCONET_MODE_VIRTUAL ? grp.first + i : c->rank;
-    ta.b[i] = reinterpret_cast<const uint16_t*>(c->heap[wr] + bo);
-    ta.bt[i] = reinterpret_cast<uint16_t*>(static_cast<char*>(scratch) + size_t(i) * size_t(n * k) * 2);
-  }
-  {
-    dim3 tb(32, 8), tg(unsigned((n + 31) / 32), unsigned((k + 31) / 32), unsigned(nl));
-    transpose_kernel<uint16_t><<<tg, tb, 0, s>>>(ta, int(k), int(n));
-    c->launches++;
-  }
   for (int i = 0; i < nl; ++i) {
     const int wr = c->mode == COCONET_MODE_VIRTUAL ? grp.first + i : c->rank;
     char* heap = c->heap[wr];
-    void* bt = ta.bt[i];
     rc = make_map(&p->maps.a[i], heap + ao, in_elem, uint64_t(k), uint64_t(m), BK, BM);
-    if (!rc) rc = make_map(&p->maps.b[i], bt, in_elem, uint64_t(k), uint64_t(n), BK, uint32_t(bn));
+    // B in its natural row-major [K, N] layout, read MN-major (64 n x 64 k boxes)
+    if (!rc) rc = make_map(&p->maps.b[i], heap + bo, in_elem, uint64_t(n), uint64_t(k), 64, BK);
     if (!rc)
       rc = make_map(&p->maps.c[i], heap + co, out_elem, uint64_t(n), uint64_t(m), out_elem == COCONET_F32 ? 32 : 64, 32);
     if (rc) return rc;
