@@ -230,3 +230,118 @@ def test_distributed_lamb_schedules_and_rooted(world):
         assert same, f"rank {rank}: STREAMED differs from GRID across processes"
         assert dev <= 1e-5, f"rank {rank}: LAMB deviates {dev}"
         assert ok_red and ok_bc, f"rank {rank}: reduce {ok_red} broadcast {ok_bc}"
+
+
+def _mp_pp_inputs(world, rows, H, r):
+    g = torch.Generator().manual_seed(1000 + r)
+    k = H // world
+    x = torch.randn(rows, k, generator=g).to(torch.bfloat16)
+    w = (torch.randn(k, H, generator=g) * k ** -0.5).to(torch.bfloat16)
+    gs = torch.Generator().manual_seed(7)
+    b = (torch.randn(H, generator=gs) * 0.1).to(torch.bfloat16)
+    res = torch.randn(rows, H, generator=gs).to(torch.bfloat16)
+    return x, w, b, res
+
+
+def _run_mp(ctx, ranks, world, rows, H, fused):
+    """MatMul + fused RS-bias-dropout-residual-AG on `ctx` for `ranks`."""
+    from paper_2105_05720_b200 import _lib
+    from paper_2105_05720_b200.collectives import BdrHParams, fused_rs_bdr_ag, matmul, mm_overlap_fused_ar
+    k = H // world
+    xb, wb = ctx.alloc([rows, k], torch.bfloat16), ctx.alloc([k, H], torch.bfloat16)
+    bb, rb = ctx.alloc([H], torch.bfloat16), ctx.alloc([rows, H], torch.bfloat16)
+    part, out = ctx.alloc([rows, H], torch.bfloat16), ctx.alloc([rows, H], torch.bfloat16)
+    for r in ranks:
+        x, w, b, res = _mp_pp_inputs(world, rows, H, r)
+        ctx.view(xb, r if ctx.mode == "virtual" else None).copy_(x)
+        ctx.view(wb, r if ctx.mode == "virtual" else None).copy_(w)
+        ctx.view(bb, r if ctx.mode == "virtual" else None).copy_(b)
+        ctx.view(rb, r if ctx.mode == "virtual" else None).copy_(res)
+    torch.cuda.synchronize()
+    if ctx.mode == "distributed":
+        dist.barrier()
+    hp = BdrHParams(0.1, 1, 11617925594314093840, _lib.MATH_FAST)
+    if fused:
+        mm_overlap_fused_ar(ctx, xb, wb, bb, rb, part, out, hp)
+    else:
+        matmul(ctx, xb, wb, part, math=_lib.MATH_FAST)
+        fused_rs_bdr_ag(ctx, part, bb, rb, out, hp)
+    ctx.check()
+    return {r: ctx.view(out, r if ctx.mode == "virtual" else None).cpu().clone() for r in ranks}
+
+
+def _worker_mp_pp(rank, world, port, q):
+    """The MP epilogue (sequential and overlapped with the tcgen05 GEMM) and
+    the PP RS -> send -> AG across processes must equal VIRTUAL mode bitwise."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2105_05720_b200 import _lib
+        from paper_2105_05720_b200.collectives import BdrHParams, rs_fused_send_ag
+        from paper_2105_05720_b200.runtime import Context
+
+        torch.cuda.set_device(0)
+        rows, H = 256, 128 * world
+        dctx = Context(world, mode="distributed", rank=rank, device=0, heap_bytes=256 << 20, timeout_ms=60000)
+        got_seq = _run_mp(dctx, [rank], world, rows, H, fused=False)[rank]
+        got_ov = _run_mp(dctx, [rank], world, rows, H, fused=True)[rank]
+        # PP: stages of world/2 ranks
+        S = world // 2
+        N = 4096 * S
+        g0, g1 = dctx.group(0, S), dctx.group(S, S)
+        xb, bb, rb, ob = (dctx.alloc([N]) for _ in range(4))
+        gen = torch.Generator().manual_seed(50 + rank)
+        dctx.view(xb).copy_(torch.randn(N, generator=gen))
+        gs = torch.Generator().manual_seed(60)
+        dctx.view(bb).copy_(torch.randn(N, generator=gs))
+        dctx.view(rb).copy_(torch.randn(N, generator=gs))
+        dctx.view(ob).zero_()
+        torch.cuda.synchronize()
+        dist.barrier()
+        rs_fused_send_ag(dctx, g0, g1, xb, bb, rb, ob, BdrHParams(0.1, 1, 3251584743947114031, _lib.MATH_EXACT))
+        dctx.check()
+        got_pp = dctx.view(ob).cpu().clone()
+        dist.barrier()
+        dctx.close()
+        # the same in VIRTUAL mode, all ranks in this process
+        vctx = Context(world, mode="virtual", device=0, heap_bytes=256 << 20)
+        want_seq = _run_mp(vctx, list(range(world)), world, rows, H, fused=False)[rank]
+        want_ov = _run_mp(vctx, list(range(world)), world, rows, H, fused=True)[rank]
+        vg0, vg1 = vctx.group(0, S), vctx.group(S, S)
+        vx, vb, vr, vo = (vctx.alloc([N]) for _ in range(4))
+        gs = torch.Generator().manual_seed(60)
+        bvals, rvals = torch.randn(N, generator=gs), torch.randn(N, generator=gs)
+        for r in range(world):
+            gen = torch.Generator().manual_seed(50 + r)
+            vctx.view(vx, r).copy_(torch.randn(N, generator=gen))
+            vctx.view(vb, r).copy_(bvals)
+            vctx.view(vr, r).copy_(rvals)
+            vctx.view(vo, r).zero_()
+        rs_fused_send_ag(vctx, vg0, vg1, vx, vb, vr, vo, BdrHParams(0.1, 1, 3251584743947114031, _lib.MATH_EXACT))
+        vctx.check()
+        want_pp = vctx.view(vo, rank).cpu().clone()
+        vctx.close()
+        q.put((rank, torch.equal(got_seq, want_seq), torch.equal(got_ov, want_ov), torch.equal(got_pp, want_pp), None))
+    except Exception as e:  # report, don't hang the parent
+        q.put((rank, False, False, False, repr(e)))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_distributed_mp_and_pp_match_virtual(world):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_mp_pp, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=300) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=120)
+    for rank, ok_seq, ok_ov, ok_pp, err in res:
+        assert err is None, err
+        assert ok_seq, f"rank {rank}: MatMul + fused RS-BDR-AG differs from VIRTUAL mode"
+        assert ok_ov, f"rank {rank}: overlapped MatMul+AR differs from VIRTUAL mode"
+        assert ok_pp, f"rank {rank}: PP RS->send->AG differs from VIRTUAL mode"
