@@ -65,41 +65,67 @@ struct BdrArgs {
   int64_t n;                // PP: elements of the 1-D tensor
 };
 
-// MP: rank c owns column block c of every row.
+// 16-byte vectors: V = 16 / sizeof(T) elements kept raw in registers until
+// they are folded (the loads of every rank, b and r are all in flight at once).
+template <typename T> struct Vec16 {
+  static constexpr int V = 16 / int(sizeof(T));
+  uint4 raw;
+  __device__ __forceinline__ void load_cg(const T* p) { raw = __ldcg(reinterpret_cast<const uint4*>(p)); }
+  __device__ __forceinline__ void load(const T* p) { raw = __ldg(reinterpret_cast<const uint4*>(p)); }
+  __device__ __forceinline__ float get(int i) const { return to_f32(reinterpret_cast<const T*>(&raw)[i]); }
+};
+
+template <typename T>
+__device__ __forceinline__ void store16(T* p, const float (&o)[16 / sizeof(T)]) {
+  constexpr int V = 16 / int(sizeof(T));
+  uint4 raw;
+  T* h = reinterpret_cast<T*>(&raw);
+#pragma unroll
+  for (int i = 0; i < V; ++i) h[i] = from_f32<T>(o[i]);
+  *reinterpret_cast<uint4*>(p) = raw;
+}
+
+// MP: rank c owns column block c of every row. One 16-byte vector per thread
+// per rank; all W + 2 loads issued before the ring-order fold.
 template <typename T, int MATH>
 __global__ void __launch_bounds__(kThreads) rs_bdr_ag_kernel(BdrArgs a, BdrK k) {
+  constexpr int V = Vec16<T>::V;
   __shared__ char* s_base[kMaxRanks];
   const RankSet& rs = a.rs;
   if (threadIdx.x < kMaxRanks) s_base[threadIdx.x] = threadIdx.x < rs.world ? rs.base[threadIdx.x] : nullptr;
   const int W = rs.world, me = rs.rank();
   if (!rank_barrier(rs, 0)) return;
-  const int64_t qpr = a.per >> 2;  // quads per row block
-  const int64_t nq = a.rows * qpr;
+  const int64_t vpr = a.per / V;  // vectors per row block
+  const int64_t nv = a.rows * vpr;
   const T* bb = reinterpret_cast<const T*>(s_base[me] + a.b_off);
-  for (int64_t q = int64_t(blockIdx.x) * kThreads + threadIdx.x; q < nq; q += int64_t(gridDim.x) * kThreads) {
-    const int64_t row = q / qpr;
-    const int64_t col = int64_t(me) * a.per + (q - row * qpr) * 4;
+  for (int64_t q = int64_t(blockIdx.x) * kThreads + threadIdx.x; q < nv; q += int64_t(gridDim.x) * kThreads) {
+    const int64_t row = q / vpr;
+    const int64_t col = int64_t(me) * a.per + (q - row * vpr) * V;
     const int64_t gi = row * a.cols + col;
-    float acc[4], x[4];
+    Vec16<T> x[kMaxRanks], bv, rv;
 #pragma unroll
     for (int j = 0; j < kMaxRanks; ++j) {
       if (j >= W) break;
       int src = me + 1 + j;
       src -= src >= W ? W : 0;
       src -= src >= W ? W : 0;
-      load4_cg(reinterpret_cast<const T*>(s_base[src] + a.x_off) + gi, x);
-#pragma unroll
-      for (int i = 0; i < 4; ++i) acc[i] = j == 0 ? x[i] : __fadd_rn(acc[i], x[i]);
+      x[j].load_cg(reinterpret_cast<const T*>(s_base[src] + a.x_off) + gi);
     }
-    float b4[4], r4[4], o[4];
-    load4(bb + col, b4);
-    load4(reinterpret_cast<const T*>(s_base[me] + a.r_off) + gi, r4);
+    bv.load(bb + col);
+    rv.load_cg(reinterpret_cast<const T*>(s_base[me] + a.r_off) + gi);
+    float o[V];
 #pragma unroll
-    for (int i = 0; i < 4; ++i) o[i] = bdr<MATH>(acc[i], b4[i], r4[i], uint64_t(gi + i), k);
+    for (int i = 0; i < V; ++i) {
+      float acc = x[0].get(i);
+#pragma unroll
+      for (int j = 1; j < kMaxRanks; ++j)
+        if (j < W) acc = __fadd_rn(acc, x[j].get(i));  // ring order (runtime.hpp:302-305)
+      o[i] = bdr<MATH>(acc, bv.get(i), rv.get(i), uint64_t(gi + i), k);
+    }
 #pragma unroll
     for (int j = 0; j < kMaxRanks; ++j) {
       if (j >= W) break;
-      store4(reinterpret_cast<T*>(s_base[j] + a.out_off) + gi, o);
+      store16(reinterpret_cast<T*>(s_base[j] + a.out_off) + gi, o);
     }
   }
   rank_barrier(rs, 1);
@@ -121,20 +147,26 @@ __global__ void __launch_bounds__(kThreads) rs_send_ag_kernel(BdrArgs a, BdrK k)
     const int64_t nq = per >> 2;
     for (int64_t q = int64_t(blockIdx.x) * kThreads + threadIdx.x; q < nq; q += int64_t(gridDim.x) * kThreads) {
       const int64_t gi = int64_t(me) * per + q * 4;
-      float acc[4], x[4];
+      // every source rank's quad, b and r in flight before the fold
+      float acc[4], x[kMaxRanks][4], b4[4], r4[4], o[4];
 #pragma unroll
       for (int j = 0; j < kMaxRanks; ++j) {
         if (j >= S) break;
         int src = me + 1 + j;
         src -= src >= S ? S : 0;
         src -= src >= S ? S : 0;
-        load4(reinterpret_cast<const T*>(s_base[src] + a.x_off) + gi, x);
-#pragma unroll
-        for (int i = 0; i < 4; ++i) acc[i] = j == 0 ? x[i] : __fadd_rn(acc[i], x[i]);
+        load4(reinterpret_cast<const T*>(s_base[src] + a.x_off) + gi, x[j]);
       }
-      float b4[4], r4[4], o[4];
       load4(reinterpret_cast<const T*>(s_base[me] + a.b_off) + gi, b4);
       load4(reinterpret_cast<const T*>(s_base[me] + a.r_off) + gi, r4);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) acc[i] = x[0][i];
+#pragma unroll
+      for (int j = 1; j < kMaxRanks; ++j) {
+        if (j >= S) break;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) acc[i] = __fadd_rn(acc[i], x[j][i]);
+      }
 #pragma unroll
       for (int i = 0; i < 4; ++i) o[i] = bdr<MATH>(acc[i], b4[i], r4[i], uint64_t(gi + i), k);
 #pragma unroll
@@ -215,17 +247,20 @@ int coconet_fused_rs_bdr_ag(coconet_ctx_t c, int group, const void* x, const voi
   const int W = c->groups[size_t(group)].size;
   if (cols % W)
     return set_error(COCONET_ERR_DIVISIBILITY, "extent " + std::to_string(cols) + " over " + std::to_string(W) + " ranks");
-  if ((cols / W) % 4) return set_error(COCONET_ERR_UNSUPPORTED, "column block must be a multiple of 4");
+  if ((cols / W) % (16 / esz(elem)))
+    return set_error(COCONET_ERR_UNSUPPORTED, "column block must be a multiple of 16 bytes");
   BdrArgs a{};
   int rc = offsets(c, x, b, r, out, elem, &a);
   if (rc) return rc;
+  if ((a.x_off | a.b_off | a.r_off | a.out_off | (cols * esz(elem))) % 16)
+    return set_error(COCONET_ERR_INVALID_INPUT, "operands and rows must be 16-byte aligned");
   a.rows = rows;
   a.cols = cols;
   a.per = cols / W;
   BdrK k = make_k(hp);
   const void* fn = hp->math == COCONET_MATH_EXACT ? mp_fn<COCONET_MATH_EXACT>(elem) : mp_fn<COCONET_MATH_FAST>(elem);
   int blocks = 0;
-  rc = coop_blocks(c, fn, kThreads, 0, group, (rows * (a.per / 4) + kThreads - 1) / kThreads, &blocks);
+  rc = coop_blocks(c, fn, kThreads, 0, group, (rows * (a.per / (16 / esz(elem))) + kThreads - 1) / kThreads, &blocks);
   if (!rc) rc = make_rankset(c, group, &a.rs);
   if (rc) return rc;
   void* args[] = {&a, &k};
