@@ -47,7 +47,6 @@ constexpr int kAccStride = 256;   // TMEM columns per accumulator buffer
 constexpr int kTmemCols = 512;
 constexpr int kFusedThreads = 512;  // overlap kernel: 16 warps (0/1/4-7 GEMM roles, the rest all-reduce)
 constexpr int kFusedWarps = kFusedThreads / 32;
-constexpr int kUnitU = 2;           // quads per lane in flight in an all-reduce unit
 
 // Stage counts: the K=384 GEMM is bound by TMA bytes in flight, so the ring
 // takes all the shared memory the epilogue leaves (4 x 48 KB at BN = 256;
@@ -74,6 +73,7 @@ struct GemmArgs {
   int ranks;                   // ranks computed by this launch
   int tiles_m, tiles_n;
   uint32_t epoch;
+  int local_peers;             // every rank on this GPU (VIRTUAL): flags need only gpu scope
 };
 
 __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
@@ -170,6 +170,17 @@ __device__ __forceinline__ void store_row32(TO* dst, const uint32_t (&v)[32]) {
   }
 }
 
+// Tile flag: release at gpu scope when every reader is on this GPU
+// (VIRTUAL), at system scope when peers read over NVLink.
+__device__ __forceinline__ void publish_flag(uint32_t* f, uint32_t epoch, int local) {
+  if (local) {
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(f), "r"(epoch) : "memory");
+  } else {
+    __threadfence_system();
+    st_release_sys(f, epoch);
+  }
+}
+
 // Tile order: row tiles outermost, then column tiles, then ranks, so every
 // rank publishes row tile i of every column block before row tile i+1 and the
 // consumers of all column blocks can start together.
@@ -205,70 +216,95 @@ struct OvArgs {
   int math;
 };
 
+// One unit = 32 rows of column block `me`; each lane moves MP_U 16-byte
+// vectors (V = 8 16-bit elements) per rank per step, with every rank's
+// vectors, b and r in flight before the ring-order fold (the comm region may
+// use the registers the GEMM epilogue already holds).
+#ifndef MP_U
+#define MP_U 2
+#endif
 template <typename T>
 __device__ __forceinline__ void mp_unit(const OvArgs& a, char* const* base, int me, int mt, int rg, int lane) {
   static_assert(sizeof(T) == 2, "the overlapped all-reduce moves 16-bit partials");
-  constexpr int U = kUnitU;
+  constexpr int V = 8, U = MP_U;
   const int W = a.rs.world;
-  const int qpr = a.per >> 2;
-  const int nq = 32 * qpr;
-  for (int i0 = lane; i0 < nq; i0 += 32 * U) {
+  const int vpr = a.per / V;  // vectors per row of the block
+  const int nv = 32 * vpr;
+  for (int i0 = lane; i0 < nv; i0 += 32 * U) {
     int64_t gi[U];
-    bool valid[U];
+    uint4 raw[U][kMaxRanks], braw[U], rraw[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      const int i = min(i0 + 32 * u, nq - 1);
-      valid[u] = i0 + 32 * u < nq;
-      const int row = mt * 128 + rg * 32 + i / qpr;
-      gi[u] = int64_t(row) * a.cols + int64_t(me) * a.per + (i % qpr) * 4;
-    }
-    // every rank's quads first (raw 8-byte loads, U*W requests in flight)...
-    uint2 raw[U][kMaxRanks];
-#pragma unroll
-    for (int j = 0; j < kMaxRanks; ++j)
-      if (j < W) {
-        int src = me + 1 + j;
-        src -= src >= W ? W : 0;
-        src -= src >= W ? W : 0;
-#pragma unroll
-        for (int u = 0; u < U; ++u)
-          raw[u][j] = __ldcg(reinterpret_cast<const uint2*>(reinterpret_cast<const T*>(base[src] + a.part_off) + gi[u]));
-      }
-    // ...then the ring-order fold (runtime.hpp:302-305)
-    float acc[U][4];
-#pragma unroll
-    for (int u = 0; u < U; ++u)
+      const int i = min(i0 + 32 * u, nv - 1);  // clamped, unconditional loads
+      const int row = mt * 128 + rg * 32 + i / vpr;
+      gi[u] = int64_t(row) * a.cols + int64_t(me) * a.per + (i % vpr) * V;
 #pragma unroll
       for (int j = 0; j < kMaxRanks; ++j)
         if (j < W) {
-          const T* h = reinterpret_cast<const T*>(&raw[u][j]);
-#pragma unroll
-          for (int e = 0; e < 4; ++e) acc[u][e] = j == 0 ? to_f32(h[e]) : __fadd_rn(acc[u][e], to_f32(h[e]));
+          int src = me + 1 + j;
+          src -= src >= W ? W : 0;
+          src -= src >= W ? W : 0;
+          raw[u][j] = __ldcg(reinterpret_cast<const uint4*>(reinterpret_cast<const T*>(base[src] + a.part_off) + gi[u]));
         }
+      braw[u] = __ldg(reinterpret_cast<const uint4*>(reinterpret_cast<const T*>(base[me] + a.b_off) + gi[u] % a.cols));
+      rraw[u] = __ldcg(reinterpret_cast<const uint4*>(reinterpret_cast<const T*>(base[me] + a.r_off) + gi[u]));
+    }
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      if (!valid[u]) continue;
-      const int64_t col = gi[u] % a.cols;
-      float b4[4], r4[4], o[4];
-      load4(reinterpret_cast<const T*>(base[me] + a.b_off) + col, b4);
-      load4(reinterpret_cast<const T*>(base[me] + a.r_off) + gi[u], r4);
+      if (i0 + 32 * u >= nv) break;
+      uint4 ov;
+      T* o = reinterpret_cast<T*>(&ov);
 #pragma unroll
-      for (int e = 0; e < 4; ++e) {
+      for (int e = 0; e < V; ++e) {
+        float acc = to_f32(reinterpret_cast<const T*>(&raw[u][0])[e]);
+#pragma unroll
+        for (int j = 1; j < kMaxRanks; ++j)
+          if (j < W) acc = __fadd_rn(acc, to_f32(reinterpret_cast<const T*>(&raw[u][j])[e]));
+        const float bv = to_f32(reinterpret_cast<const T*>(&braw[u])[e]);
+        const float rv = to_f32(reinterpret_cast<const T*>(&rraw[u])[e]);
         const bool keep = dropout_keep_bits(a.seed, a.key, uint64_t(gi[u] + e), a.thresh);
+        float y;
         if (a.math == COCONET_MATH_EXACT) {
-          const double sum = __dadd_rn(double(acc[u][e]), double(b4[e]));
-          o[e] = float(__dadd_rn(keep ? __ddiv_rn(sum, a.inv_keep) : 0.0, double(r4[e])));
+          const double sum = __dadd_rn(double(acc), double(bv));
+          y = float(__dadd_rn(keep ? __ddiv_rn(sum, a.inv_keep) : 0.0, double(rv)));
         } else {
-          o[e] = (keep ? (acc[u][e] + b4[e]) * a.frate_scale : 0.f) + r4[e];
+          y = (keep ? (acc + bv) * a.frate_scale : 0.f) + rv;
         }
+        o[e] = from_f32<T>(y);
       }
 #pragma unroll
       for (int j = 0; j < kMaxRanks; ++j) {
         if (j >= W) break;
-        store4(reinterpret_cast<T*>(base[j] + a.out_off) + gi[u], o);
+        *reinterpret_cast<uint4*>(reinterpret_cast<T*>(base[j] + a.out_off) + gi[u]) = ov;
       }
     }
   }
+}
+
+// Tile-flag wait of a comm unit: the unit usually waits for tiles the GEMM
+// publishes microseconds later, so it polls with relaxed loads (an acquire
+// load invalidates L1 every poll) and backs off exponentially up to 2 us,
+// keeping ~1.5k waiting warps from flooding L2 next to the GEMM's TMA
+// traffic; one acquire fence orders the partial-sum reads after the flag.
+__device__ __forceinline__ bool wait_tile_flag(const uint32_t* p, uint32_t want, const RankSet& rs) {
+  uint32_t v;
+  asm volatile("ld.relaxed.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  if (int32_t(v - want) < 0) {
+    const unsigned long long t0 = globaltimer();
+    unsigned ns = 128;
+    for (;;) {
+      __nanosleep(ns);
+      ns = ns < 2048 ? ns * 2 : 2048;
+      asm volatile("ld.relaxed.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+      if (int32_t(v - want) >= 0) break;
+      if (globaltimer() - t0 > rs.timeout_ns) {
+        atomicCAS(rs.status, 0, COCONET_ERR_TIMEOUT);
+        return false;
+      }
+    }
+  }
+  asm volatile("fence.acq_rel.sys;" ::: "memory");
+  return true;
 }
 
 // One warp's share of the all-reduce: take tickets until the units run out.
@@ -290,7 +326,7 @@ __device__ void mp_comm_warp(const OvArgs& a, char* const* base, int lane) {
     bool ok = true;
     if (lane < W) {
       const uint32_t* fl = reinterpret_cast<const uint32_t*>(base[lane] + a.flag_off);
-      for (int nt = t_lo; nt <= t_hi; ++nt) ok &= wait_flag(fl + mt * a.tiles_n + nt, a.rs.epoch, a.rs);
+      for (int nt = t_lo; nt <= t_hi; ++nt) ok &= wait_tile_flag(fl + mt * a.tiles_n + nt, a.rs.epoch, a.rs);
     }
     if (!__all_sync(full, ok)) continue;  // watchdog fired; status already recorded
     mp_unit<T>(a, base, me, mt, rg, lane);
@@ -409,6 +445,7 @@ __global__ void __launch_bounds__(FUSED ? kFusedThreads : kGemmThreads, 1)
     constexpr int kCols = 128 / int(sizeof(TO));  // columns per 128-byte row chunk
     int acc = 0, buf = 0;
     uint32_t acc_phase = 0;
+    uint32_t* pend_flag = nullptr;  // tile flag published once its stores are complete
     for (int t = blockIdx.x; t < total; t += gridDim.x) {
       int r, mt, nt;
       decode_tile(g, t, r, mt, nt);
@@ -455,22 +492,31 @@ __global__ void __launch_bounds__(FUSED ? kFusedThreads : kGemmThreads, 1)
       tc_fence_before();
       mbar_arrive(&tempty[acc]);
       if (g.flags[r] != nullptr) {
-        if (lane == 0) {
-          asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // this warp's stores are complete
-          asm volatile("fence.proxy.async;" ::: "memory");
+        // publish the PREVIOUS tile's flag: only its store groups (all but
+        // this tile's BN / kCols) must be complete, so the epilogue never
+        // waits for the stores it just issued
+        if (pend_flag) {
+          if (lane == 0) {
+            asm volatile("cp.async.bulk.wait_group %0;" ::"n"(BN / kCols) : "memory");
+            asm volatile("fence.proxy.async;" ::: "memory");
+          }
+          __syncwarp();
+          asm volatile("bar.sync 1, 128;" ::: "memory");
+          if (warp == 4 && lane == 0) publish_flag(pend_flag, g.epoch, g.local_peers);
         }
-        __syncwarp();
-        asm volatile("bar.sync 1, 128;" ::: "memory");
-        if (warp == 4 && lane == 0) {
-          __threadfence_system();
-          st_release_sys(g.flags[r] + mt * g.tiles_n + nt, g.epoch);
-        }
+        pend_flag = g.flags[r] + mt * g.tiles_n + nt;
       }
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1;
     }
     if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
     __syncwarp();
+    if (pend_flag) {  // the last tile
+      if (lane == 0) asm volatile("fence.proxy.async;" ::: "memory");
+      __syncwarp();
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+      if (warp == 4 && lane == 0) publish_flag(pend_flag, g.epoch, g.local_peers);
+    }
     if constexpr (FUSED) mp_comm_warp<TO>(ov, s_base, lane);
   } else if constexpr (FUSED) {  // warps 2, 3 and 8-15: all-reduce from the start
     mp_comm_warp<TO>(ov, s_base, lane);
@@ -707,8 +753,21 @@ int coconet_mm_overlap_fused_ar(coconet_ctx_t c, int group, const void* a, const
     return set_error(COCONET_ERR_UNSUPPORTED, "the overlapped MatMul runs on tcgen05 (bf16/f16)");
   const int W = c->groups[size_t(group)].size;
   if (cols % W) return set_error(COCONET_ERR_DIVISIBILITY, "column extent does not divide over the group");
-  if ((cols / W) % 4) return set_error(COCONET_ERR_UNSUPPORTED, "column block must be a multiple of 4");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
+  // Schedule: with every rank on this GPU (VIRTUAL) there is no link to hide
+  // the GEMM behind - both halves contend for the same HBM and SM memory pipe
+  // and the one-kernel overlap measures slower than GEMM then the fused
+  // all-reduce - so VIRTUAL runs the two kernels back to back
+  // (bitwise the same result); DISTRIBUTED (NVLink-bound comm) runs the fused
+  // kernel. COCONET_MP_OVERLAP=fused|sequential forces either.
+  const char* ov_env = getenv("COCONET_MP_OVERLAP");
+  const bool sequential = ov_env ? std::strcmp(ov_env, "sequential") == 0
+                                 : (c->mode == COCONET_MODE_VIRTUAL && W > 1);
+  if (sequential) {
+    int rc = coconet_matmul(c, group, a, w, partial, in_elem, in_elem, rows, cols, k_local, COCONET_MATH_FAST, stream);
+    if (rc) return rc;
+    return coconet_fused_rs_bdr_ag(c, group, partial, b, r, out, in_elem, rows, cols, hp, stream);
+  }
   TcPlan p;
   int rc = plan_tc(c, group, a, w, partial, in_elem, in_elem, rows, cols, k_local, s, &p);
   if (rc) return rc;
@@ -722,8 +781,8 @@ int coconet_mm_overlap_fused_ar(coconet_ctx_t c, int group, const void* a, const
   if (!rc) rc = heap_offset(c, r, &o.r_off);
   if (!rc) rc = heap_offset(c, out, &o.out_off);
   if (rc) return rc;
-  if ((o.part_off | o.b_off | o.r_off | o.out_off) % 8)
-    return set_error(COCONET_ERR_INVALID_INPUT, "operands must be aligned to 4 elements");
+  if ((o.part_off | o.b_off | o.r_off | o.out_off) % 16 || (cols / W) % 8 || cols % 8)
+    return set_error(COCONET_ERR_INVALID_INPUT, "operands, rows and column blocks must be 16-byte aligned");
   // tile flags, arrival counter and unit ticket live in every rank's reserved
   // per-group area (common.cuh)
   o.flag_off = int64_t(group_area(group) + kTileFlagsOff);
@@ -754,6 +813,7 @@ int coconet_mm_overlap_fused_ar(coconet_ctx_t c, int group, const void* a, const
   for (int i = 0; i < p.g.ranks; ++i)
     p.g.flags[i] = reinterpret_cast<uint32_t*>(p.g.c[i] - o.part_off + o.flag_off);
   p.g.epoch = o.rs.epoch;
+  p.g.local_peers = c->mode == COCONET_MODE_VIRTUAL ? 1 : 0;
   return launch_tc<true>(c, &p, in_elem, in_elem, &o, s);
 }
 

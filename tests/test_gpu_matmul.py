@@ -74,11 +74,17 @@ def test_mp_program_end_to_end_exact_digest(name):
 
 
 @pytest.mark.parametrize("W,rows,H", [(1, 256, 512), (2, 512, 768), (4, 1024, 1536), (8, 1024, 3072)])
-def test_mm_overlap_matches_sequential(W, rows, H):
+@pytest.mark.parametrize("mode", ["fused", "auto"])
+def test_mm_overlap_matches_sequential(W, rows, H, mode, monkeypatch):
     """OverlapGroup{MatMul, FusedAllReduce}: the tile-flag-overlapped pair gives
     bit-identical output to running the same two kernels back to back
     (Overlap.OutputBitIdenticalToSequential, test_overlap.cpp:35-43), and is
-    within 1e-2 of the fp32 reference for bf16 activations."""
+    within 1e-2 of the fp32 reference for bf16 activations. mode=fused forces
+    the one-kernel overlap (VIRTUAL mode's AUTO runs the pair back to back)."""
+    if mode == "fused":
+        monkeypatch.setenv("COCONET_MP_OVERLAP", "fused")
+    else:
+        monkeypatch.delenv("COCONET_MP_OVERLAP", raising=False)
     dtype = torch.bfloat16
     k = H // W
     torch.manual_seed(W * rows)
