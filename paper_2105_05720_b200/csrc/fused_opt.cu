@@ -551,6 +551,55 @@ struct SegBatch {
   }
 };
 
+// The producer warp of a TMA-ring kernel: walks the CTA's segments
+// (batched descriptors) and, per chunk of ST::CHUNK_Q quads, waits for a free
+// stage and issues the bulk copies of g (when with_g), m, v and p into it.
+// Lane 0 issues; the warp returns the ring position it reached.
+template <typename G, int NW, int QPT>
+__device__ __forceinline__ void tma_produce(const OptArgs& a, char* const* s_base, int me, int64_t sb, int64_t se,
+                                            uint8_t* stage0, uint64_t* full, uint64_t* empty, int S, bool with_g,
+                                            int lane, uint32_t& st, uint32_t& ph) {
+  using ST = TmaStage<G, NW, QPT>;
+  const float* m = reinterpret_cast<const float*>(s_base[me] + a.m_off);
+  const float* v = reinterpret_cast<const float*>(s_base[me] + a.v_off);
+  const char* pme = s_base[me];
+  const int64_t st32 = int64_t(gridDim.x) * 32;
+  for (int64_t s0 = sb + blockIdx.x; s0 < se; s0 += st32) {
+    SegBatch batch;
+    batch.load(a, s0 + int64_t(lane) * gridDim.x, se);
+    for (int j = 0; j < 32; ++j) {
+      if (s0 + int64_t(j) * gridDim.x >= se) break;
+      const SegD d = batch.get(j, me);
+      if (lane != 0) continue;
+      const int64_t q0 = d.toff >> 2, q1 = (d.toff + d.len + 3) >> 2;
+      for (int64_t qa = q0; qa < q1; qa += ST::CHUNK_Q) {
+        const int64_t qb = min(qa + int64_t(ST::CHUNK_Q), q1);
+        mbar_wait(&empty[st], ph ^ 1u);
+        uint8_t* dst = stage0 + size_t(st) * ST::BYTES;
+        const uint32_t abytes = uint32_t(qb - qa) * 16u;
+        const char* ga = pme + d.aoff + qa * 4 * int64_t(sizeof(G));
+        const char* g0 = reinterpret_cast<const char*>(reinterpret_cast<uintptr_t>(ga) & ~uintptr_t(15));
+        const char* g1 = reinterpret_cast<const char*>(
+            (reinterpret_cast<uintptr_t>(pme + d.aoff + qb * 4 * int64_t(sizeof(G))) + 15) & ~uintptr_t(15));
+        const uint32_t gbytes = with_g ? uint32_t(g1 - g0) : 0u;
+        const int64_t si = d.sidx + (qa * 4 - d.toff);
+        mbar_expect_tx(&full[st], gbytes + 3u * abytes);
+        if (with_g) bulk_load(dst, g0, gbytes, &full[st]);
+        bulk_load(dst + ST::G_BYTES, m + si, abytes, &full[st]);
+        bulk_load(dst + ST::G_BYTES + ST::A_BYTES, v + si, abytes, &full[st]);
+        bulk_load(dst + ST::G_BYTES + 2 * ST::A_BYTES, pme + d.boff + qa * 16, abytes, &full[st]);
+        if (++st == uint32_t(S)) {
+          st = 0;
+          ph ^= 1u;
+        }
+      }
+    }
+  }
+  __syncwarp();
+  st = __shfl_sync(0xffffffffu, st, 0);
+  ph = __shfl_sync(0xffffffffu, ph, 0);
+}
+
 template <typename G, int NW, int QPT>
 __global__ void __launch_bounds__((NW + 1) * 32) lamb_tma_kernel(OptArgs a, LambK k, TmaArgs ta) {
   using ST = TmaStage<G, NW, QPT>;
@@ -614,42 +663,7 @@ __global__ void __launch_bounds__((NW + 1) * 32) lamb_tma_kernel(OptArgs a, Lamb
     }
     const double* xch_me = reinterpret_cast<const double*>(s_base[me] + group_area(rs.group));
     if (producer) {
-      const int64_t st32 = int64_t(gridDim.x) * 32;
-      for (int64_t s0 = sb + blockIdx.x; s0 < se; s0 += st32) {
-        SegBatch batch;
-        batch.load(a, s0 + int64_t(lane) * gridDim.x, se);
-        for (int j = 0; j < 32; ++j) {
-          if (s0 + int64_t(j) * gridDim.x >= se) break;
-          const SegD d = batch.get(j, me);
-          if (lane != 0) continue;
-          const int64_t q0 = d.toff >> 2, q1 = (d.toff + d.len + 3) >> 2;
-          for (int64_t qa = q0; qa < q1; qa += kTmaChunkQ) {
-            const int64_t qb = min(qa + int64_t(kTmaChunkQ), q1);
-            mbar_wait(&empty[st], ph ^ 1u);
-            uint8_t* dst = stage0 + size_t(st) * ST::BYTES;
-            const uint32_t abytes = uint32_t(qb - qa) * 16u;
-            const char* ga = s_base[me] + d.aoff + qa * 4 * int64_t(sizeof(G));
-            const char* g0 = reinterpret_cast<const char*>(reinterpret_cast<uintptr_t>(ga) & ~uintptr_t(15));
-            const char* g1 = reinterpret_cast<const char*>(
-                (reinterpret_cast<uintptr_t>(s_base[me] + d.aoff + qb * 4 * int64_t(sizeof(G))) + 15) &
-                ~uintptr_t(15));
-            const uint32_t gbytes = pass == 0 ? uint32_t(g1 - g0) : 0u;
-            const int64_t si = d.sidx + (qa * 4 - d.toff);
-            mbar_expect_tx(&full[st], gbytes + 3u * abytes);
-            if (pass == 0) bulk_load(dst, g0, gbytes, &full[st]);
-            bulk_load(dst + ST::G_BYTES, m + si, abytes, &full[st]);
-            bulk_load(dst + ST::G_BYTES + ST::A_BYTES, v + si, abytes, &full[st]);
-            bulk_load(dst + ST::G_BYTES + 2 * ST::A_BYTES, pme + d.boff + qa * 16, abytes, &full[st]);
-            if (++st == uint32_t(S)) {
-              st = 0;
-              ph ^= 1u;
-            }
-          }
-        }
-      }
-      __syncwarp();
-      st = __shfl_sync(0xffffffffu, st, 0);
-      ph = __shfl_sync(0xffffffffu, ph, 0);
+      tma_produce<G, NW, QPT>(a, s_base, me, sb, se, stage0, full, empty, S, pass == 0, lane, st, ph);
     } else {
       int red = 0;  // s_red buffer of the next segment reduction
       const int64_t st32 = int64_t(gridDim.x) * 32;
@@ -752,6 +766,96 @@ __global__ void __launch_bounds__((NW + 1) * 32) lamb_tma_kernel(OptArgs a, Lamb
           red ^= 1;
         }
        }
+      }
+    }
+  }
+  rank_barrier(rs, 1);
+}
+
+// ---- Adam, TMA schedule (W = 1): one pass, the producer of lamb_tma_kernel
+// streaming g, m, v, p into the shared-memory ring and NW consumer warps
+// applying adam_elem (EXACT or FAST) and writing m, v, p.
+template <typename G, int NW, int QPT, int MATH>
+__global__ void __launch_bounds__((NW + 1) * 32) adam_tma_kernel(OptArgs a, AdamK k, TmaArgs ta) {
+  using ST = TmaStage<G, NW, QPT>;
+  extern __shared__ __align__(128) uint8_t smem_raw[];
+  __shared__ char* s_base[kMaxRanks];
+  const RankSet& rs = a.rs;
+  if (threadIdx.x < kMaxRanks) s_base[threadIdx.x] = threadIdx.x < rs.world ? rs.base[threadIdx.x] : nullptr;
+  const int S = ta.stages;
+  uint8_t* stage0 = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
+  uint64_t* full = reinterpret_cast<uint64_t*>(stage0 + size_t(S) * ST::BYTES);
+  uint64_t* empty = full + S;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < S; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], NW);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  const int me = rs.rank();
+  const bool ok = rank_barrier(rs, 0);
+  const int64_t sb = a.seg_begin[me], se = ok ? a.seg_begin[me + 1] : sb;
+  float* m = reinterpret_cast<float*>(s_base[me] + a.m_off);
+  float* v = reinterpret_cast<float*>(s_base[me] + a.v_off);
+  char* pme = s_base[me];
+  uint32_t st = 0, ph = 0;
+  if (warp == NW) {
+    tma_produce<G, NW, QPT>(a, s_base, me, sb, se, stage0, full, empty, S, true, lane, st, ph);
+  } else {
+    const int ctid = threadIdx.x;
+    const int64_t st32 = int64_t(gridDim.x) * 32;
+    for (int64_t s0 = sb + blockIdx.x; s0 < se; s0 += st32) {
+      SegBatch batch;
+      batch.load(a, s0 + int64_t(lane) * gridDim.x, se);
+      for (int j = 0; j < 32; ++j) {
+        if (s0 + int64_t(j) * gridDim.x >= se) break;
+        const SegD d = batch.get(j, me);
+        const int64_t q0 = d.toff >> 2, q1 = (d.toff + d.len + 3) >> 2;
+        for (int64_t qa = q0; qa < q1; qa += ST::CHUNK_Q) {
+          const int64_t qb = min(qa + int64_t(ST::CHUNK_Q), q1);
+          mbar_wait(&full[st], ph);
+          const uint8_t* src = stage0 + size_t(st) * ST::BYTES;
+          const uintptr_t ga = reinterpret_cast<uintptr_t>(pme + d.aoff + qa * 4 * int64_t(sizeof(G)));
+#pragma unroll
+          for (int qq = 0; qq < QPT; ++qq) {
+            const int64_t q = qa + ctid + qq * (NW * 32);
+            if (q < qb) {
+              const int64_t e0 = q << 2;
+              int lo, hi;
+              quad_range(d, e0, lo, hi);
+              const int64_t si = d.sidx + (e0 - d.toff);
+              const float4 mq = *reinterpret_cast<const float4*>(src + ST::G_BYTES + (q - qa) * 16);
+              const float4 vq = *reinterpret_cast<const float4*>(src + ST::G_BYTES + ST::A_BYTES + (q - qa) * 16);
+              const float4 pq = *reinterpret_cast<const float4*>(src + ST::G_BYTES + 2 * ST::A_BYTES + (q - qa) * 16);
+              float mm[4] = {mq.x, mq.y, mq.z, mq.w}, vv[4] = {vq.x, vq.y, vq.z, vq.w}, pp[4] = {pq.x, pq.y, pq.z, pq.w};
+              const uintptr_t goff = (ga & 15u) + uintptr_t(q - qa) * 4u * sizeof(G);
+              float gs[4];
+              if constexpr (sizeof(G) == 4) {
+                const float4 gq = *reinterpret_cast<const float4*>(src + goff);
+                gs[0] = gq.x; gs[1] = gq.y; gs[2] = gq.z; gs[3] = gq.w;
+              } else {
+                const uint2 gq = *reinterpret_cast<const uint2*>(src + goff);
+                const G* h = reinterpret_cast<const G*>(&gq);
+#pragma unroll
+                for (int i = 0; i < 4; ++i) gs[i] = to_f32(h[i]);
+              }
+#pragma unroll
+              for (int i = 0; i < 4; ++i) adam_elem<MATH>(gs[i], mm[i], vv[i], pp[i], k);
+              st4m(m + si, mm, lo, hi);
+              st4m(v + si, vv, lo, hi);
+              st4m(reinterpret_cast<float*>(pme + d.boff) + e0, pp, lo, hi);
+            }
+          }
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&empty[st]);
+          if (++st == uint32_t(S)) {
+            st = 0;
+            ph ^= 1u;
+          }
+        }
       }
     }
   }
@@ -1145,14 +1249,7 @@ const void* ar_pick(int red, bool os, int W) {
 template <typename G>
 const void* lamb_pick(int W) {
   switch (W) {
-    case 1: {
-      // occupancy/unroll trade-off at W=1 (probe with COCONET_LAMB_VARIANT)
-      const char* v = getenv("COCONET_LAMB_VARIANT");
-      if (v && v[0] == '1') return reinterpret_cast<const void*>(&lamb_kernel<G, 1, 2, 3>);
-      if (v && v[0] == '2') return reinterpret_cast<const void*>(&lamb_kernel<G, 1, 3, 3>);
-      if (v && v[0] == '3') return reinterpret_cast<const void*>(&lamb_kernel<G, 1, 2, 4>);
-      return reinterpret_cast<const void*>(&lamb_kernel<G, 1, 4>);
-    }
+    case 1: return reinterpret_cast<const void*>(&lamb_kernel<G, 1, 4>);
     case 2: return reinterpret_cast<const void*>(&lamb_kernel<G, 2, 2>);
     case 4: return reinterpret_cast<const void*>(&lamb_kernel<G, 4, 2>);
     case 8: return reinterpret_cast<const void*>(&lamb_kernel<G, 8, 1>);
@@ -1175,6 +1272,13 @@ const void* lamb_stream_pick(int W) {
 // in-flight window (2 CTAs x 148 SMs x 4096-element items = 1.2M elements)
 // while tensor + lag stay inside the 126 MB L2 for tensors up to ~4M.
 constexpr int64_t kDefaultLag = int64_t(1) << 21;
+
+// The TMA ring pays off when a segment spans several 2048-element chunks: at
+// 1024-element buckets its per-segment cost dominates (LAMB 4.1 ms vs GRID
+// 2.4 ms), from 4096 up it wins (LAMB 2.06 vs 2.26 ms, Adam EXACT 2.0 vs
+// 2.5 ms at 16384). Group size 1 only (peer bulk copies untested).
+constexpr int64_t kTmaMinBucket = 4096;
+bool tma_eligible(const coconet_tlist* tl, int W) { return W == 1 && tl->bucket_cap >= kTmaMinBucket; }
 
 int check_state(coconet_ctx* c, const void* ptr, int64_t* off) {
   int rc = heap_offset(c, ptr, off);
@@ -1225,6 +1329,34 @@ int coconet_fused_rs_adam_ag(coconet_ctx_t c, coconet_tlist_t tl, const void* co
   if (rc) return rc;
   OptArgs a;
   fill_args(tl, &a, rs, m_off, v_off);
+  // W = 1 (two-shot tables) with large buckets: the TMA ring
+  // (COCONET_ADAM_TMA=0 keeps the LDG kernel)
+  const char* te = getenv("COCONET_ADAM_TMA");
+  if (!os && tma_eligible(tl, W) && !(te && te[0] == '0')) {
+    const void* fn = nullptr;
+    int sbytes = 0, threads = 0;
+    auto pick = [&](auto tag_g) {
+      using Gt = decltype(tag_g);
+      using ST = TmaStage<Gt, 8, 2>;
+      fn = hp->math == COCONET_MATH_EXACT ? reinterpret_cast<const void*>(&adam_tma_kernel<Gt, 8, 2, COCONET_MATH_EXACT>)
+                                          : reinterpret_cast<const void*>(&adam_tma_kernel<Gt, 8, 2, COCONET_MATH_FAST>);
+      sbytes = ST::BYTES;
+      threads = ST::THREADS;
+    };
+    if (g_elem == COCONET_F32) pick(float{});
+    else if (g_elem == COCONET_F16) pick(__half{});
+    else pick(__nv_bfloat16{});
+    const int per_sm = 3;
+    TmaArgs ta;
+    ta.stages = std::min(16, (200 << 10) / per_sm / sbytes);
+    const size_t smem = size_t(ta.stages) * size_t(sbytes) + size_t(ta.stages) * 16 + 128;
+    CN_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    int blocks = 0;
+    rc = coop_blocks(c, fn, threads, smem, tl->group, int64_t(c->sm_count) * per_sm, &blocks);
+    if (rc) return rc;
+    void* args[] = {&a, &k, &ta};
+    return coop_launch(c, fn, dim3(unsigned(blocks), 1u), dim3(unsigned(threads)), args, smem, stream);
+  }
   const void* fn = g_elem == COCONET_F32   ? adam_pick<float>(hp->math, os, W)
                    : g_elem == COCONET_F16 ? adam_pick<__half>(hp->math, os, W)
                                            : adam_pick<__nv_bfloat16>(hp->math, os, W);
@@ -1272,8 +1404,10 @@ int coconet_fused_rs_lamb_ag(coconet_ctx_t c, coconet_tlist_t tl, const void* co
   if (rc) return rc;
   OptArgs a;
   fill_args(tl, &a, rs, m_off, v_off);
-  // AUTO: TMA at W = 1, GRID otherwise
-  const int sched = hp->sched == COCONET_LAMB_AUTO ? (W == 1 ? COCONET_LAMB_TMA : COCONET_LAMB_GRID) : hp->sched;
+  // AUTO: the TMA ring at W = 1 with buckets of >= kTmaMinBucket elements,
+  // GRID otherwise
+  const int sched = hp->sched == COCONET_LAMB_AUTO ? (tma_eligible(tl, W) ? COCONET_LAMB_TMA : COCONET_LAMB_GRID)
+                                                   : hp->sched;
   if (sched == COCONET_LAMB_TMA) {
     if (W != 1) return set_error(COCONET_ERR_UNSUPPORTED, "the TMA LAMB schedule runs at group size 1");
     // COCONET_LAMB_TMA_CTAS / _SHAPE: CTAs per SM and consumer shape (probes)

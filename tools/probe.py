@@ -35,6 +35,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--only", default="")
+    ap.add_argument("--cap", type=int, default=1024)
     args = ap.parse_args()
     counts = bert_large_counts()
     N = sum(counts)
@@ -46,7 +47,7 @@ def main():
     del a, b
     for W in (1,):
         ctx = Context(W, heap_bytes=sum(counts) * 24 + (1 << 30))
-        tl = TensorList(ctx, counts)
+        tl = TensorList(ctx, counts, bucket_cap=args.cap)
         for gdt, gname in ((torch.float16, "f16"), (torch.float32, "f32")):
             grads = [ctx.alloc([n], gdt) for n in counts]
             params = [ctx.alloc([n]) for n in counts]
@@ -61,11 +62,10 @@ def main():
             gb = 2 if gdt == torch.float16 else 4
             hp = LambHParams(lr=1e-3, beta1=0.9, beta2=0.999, t=1.0)
             byt = (gb + 12 + 8 + 12 + 4) * N
-            for var in ("0", "1", "2", "3"):
-                os.environ["COCONET_LAMB_VARIANT"] = var
-                ms = timeit(lambda: fused_rs_lamb_ag(ctx, tl, grads, params, m, v, hp), args.steps)
-                out[f"lamb_W{W}_g{gname}_v{var}"] = {"ms": ms, "GBs": byt / ms / 1e6, "bytes": byt}
-            os.environ.pop("COCONET_LAMB_VARIANT", None)
+            for sched, sn in ((_lib.LAMB_GRID, "grid"), (_lib.LAMB_TMA, "tma")):
+                hps = LambHParams(lr=1e-3, beta1=0.9, beta2=0.999, t=1.0, sched=sched)
+                ms = timeit(lambda: fused_rs_lamb_ag(ctx, tl, grads, params, m, v, hps), args.steps)
+                out[f"lamb_W{W}_g{gname}_{sn}"] = {"ms": ms, "GBs": byt / ms / 1e6, "bytes": byt}
             for math, mn in ((_lib.MATH_FAST, "fast"), (_lib.MATH_EXACT, "exact")):
                 hpa = AdamHParams(lr=1e-3, beta1=0.9, beta2=0.999, t=1.0, eps=1e-8, math=math,
                                   algo=_lib.ALGO_TWO_SHOT)
