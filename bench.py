@@ -366,9 +366,9 @@ def run_coconet(args):
         # protocol cost; "NVLink" traffic is local HBM here) - see DESIGN.md
         try:
             ctx.close()
-            from tools.pattern_probe import c1, c3, c4
+            from tools.pattern_probe import c1, c3, c4, c5
             extras = {"note": "one GPU, virtual ranks: all ranks' traffic is local HBM"}
-            for f in (c1, c3, c4):
+            for f in (c1, c3, c4, c5):
                 f(extras)
         except Exception as e:
             extras = {"failed": repr(e)}

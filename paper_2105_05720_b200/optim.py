@@ -69,7 +69,7 @@ class FusedAdam(_FusedBase):
     gradient all-reduce."""
 
     def __init__(self, params, ctx: Context, lr=1e-3, betas=(0.9, 0.999), eps=1e-8,
-                 grad_dtype=torch.float32, math=_lib.MATH_FAST, bucket_cap=1024):
+                 grad_dtype=torch.float32, math=_lib.MATH_FAST, bucket_cap=16384):
         super().__init__(params, dict(lr=lr, betas=betas, eps=eps), ctx, grad_dtype, bucket_cap)
         self.math = math
 
@@ -88,7 +88,7 @@ class FusedLAMB(_FusedBase):
     """LAMB with per-tensor trust ratio, fused with the gradient all-reduce."""
 
     def __init__(self, params, ctx: Context, lr=1e-3, betas=(0.9, 0.999), eps=1e-6, weight_decay=0.01,
-                 grad_dtype=torch.float32, bucket_cap=4096):
+                 grad_dtype=torch.float32, bucket_cap=16384):
         super().__init__(params, dict(lr=lr, betas=betas, eps=eps, weight_decay=weight_decay), ctx,
                          grad_dtype, bucket_cap)
 

@@ -109,15 +109,36 @@ def c4(out):
     ctx.close()
 
 
+def c5(out, n=3_900_000_000):
+    """C5's optimizer step on ONE GPU: the whole 3.9e9-parameter fused Adam
+    (fp32 g, p, m, v: 62 GB resident, 16384-element buckets -> the TMA ring).
+    At W=8 each GPU applies 1/8 of it and pulls/pushes the rest over NVLink."""
+    ctx = Context(1, heap_bytes=n * 16 + (1 << 30))
+    tl = TensorList(ctx, [n], bucket_cap=16384)
+    g, p = ctx.alloc([n]), ctx.alloc([n])
+    m, v = ctx.alloc([tl.shard_elems]), ctx.alloc([tl.shard_elems])
+    gen_values(ctx, ctx.view(g, 0), 1, "g", "local", 0, [n], group_size=1)
+    gen_values(ctx, ctx.view(p, 0), 1, "p", "replicated", 0, [n], group_size=1)
+    ctx.view(m, 0).zero_()
+    ctx.view(v, 0).fill_(1e-3)
+    hp = AdamHParams(1e-3, 0.9, 0.999, 1.0, 1e-8, False, _lib.MATH_FAST, _lib.ALGO_TWO_SHOT)
+    ms = timeit(lambda: fused_rs_adam_ag(ctx, tl, [g], [p], m, v, hp), 5)
+    out["c5_adam_3.9e9_W1_fp32_ms"] = ms
+    out["c5_adam_3.9e9_W1_GBs"] = 28 * n / ms / 1e6  # g 4 + m, v, p 12 read + m, v, p 12 written
+    ctx.close()
+
+
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--only", default="c1,c3,c4")
+    ap.add_argument("--only", default="c1,c3,c4,c5")
     ap.add_argument("--gemm-only", action="store_true")
     a = ap.parse_args()
     out = {}
     sel = a.only.split(",")
     if "c1" in sel:
         c1(out)
+    if "c5" in sel:
+        c5(out)
     if "c3" in sel:
         c3(out, a.gemm_only)
     if "c4" in sel:
