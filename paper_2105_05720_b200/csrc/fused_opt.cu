@@ -51,6 +51,7 @@ struct OptArgs {
   int64_t seg_begin[kMaxRanks + 1];
   int64_t os_begin, os_end;
   int64_t m_off, v_off;
+  int parts;  // adam_kernel: quad ranges per segment (1 = whole segments)
 };
 
 // Adam constants in both arithmetics. Double values are exactly what
@@ -220,6 +221,54 @@ __device__ __forceinline__ void adam_elem(float g, float& m, float& v, float& p,
   }
 }
 
+// Quads [qs, qe) of one segment through Adam: U quads per lane in flight,
+// clamped unconditional loads, then the ring fold, the element update and the
+// stores (own m, v; p to every rank, or the own copy for ONE_SHOT).
+template <typename G, int MATH, bool ONE_SHOT, int WT, int U>
+__device__ __forceinline__ void adam_quads(char* const* s_base, const SegD& d, int64_t qs, int64_t qe, float* m,
+                                           float* v, const char* pme, int me, int W, int lane, const AdamK& k) {
+  for (int64_t qb = qs + lane; qb < qe; qb += 32 * U) {
+    float g[U][Ranks<WT>::kMax][4], mm[U][4], vv[U][4], pp[U][4];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      // clamped, unconditional loads: the compiler can batch all U of them
+      const int64_t q = min(qb + 32 * u, qe - 1);
+      const int64_t e0 = q << 2;
+      const int64_t si = d.sidx + (e0 - d.toff);
+      ring_load4<G, COCONET_SUM, WT>(s_base, d.aoff + e0 * int64_t(sizeof(G)), d.owner, W, g[u]);
+      ld4(m + si, mm[u]);
+      ld4(v + si, vv[u]);
+      ld4(reinterpret_cast<const float*>(pme + d.boff) + e0, pp[u]);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t q = qb + 32 * u;
+      if (q < qe) {
+        const int64_t e0 = q << 2;
+        int lo, hi;
+        quad_range(d, e0, lo, hi);
+        const int64_t si = d.sidx + (e0 - d.toff);
+        float gs[4];
+        ring_fold4<COCONET_SUM, WT>(g[u], W, gs);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) adam_elem<MATH>(gs[i], mm[u][i], vv[u][i], pp[u][i], k);
+        st4m(m + si, mm[u], lo, hi);
+        st4m(v + si, vv[u], lo, hi);
+        if (ONE_SHOT) {
+          st4m(reinterpret_cast<float*>(s_base[me] + d.boff) + e0, pp[u], lo, hi);
+        } else {
+#pragma unroll
+          for (int j = 0; j < Ranks<WT>::kMax; ++j)  // AG push, own copy included
+            if (Ranks<WT>::has(j, W)) st4m(reinterpret_cast<float*>(s_base[j] + d.boff) + e0, pp[u], lo, hi);
+        }
+      }
+    }
+  }
+}
+
+// a.parts > 1 (small lists): each segment is split into `parts` quad ranges
+// so the resident grid has work for every warp (C1: 256 segments per rank
+// would otherwise keep 32 of 74 CTAs per rank busy).
 template <typename G, int MATH, bool ONE_SHOT, int WT, int U>
 __global__ void __launch_bounds__(kThreads, 2) adam_kernel(OptArgs a, AdamK k) {
   __shared__ char* s_base[kMaxRanks];
@@ -234,51 +283,26 @@ __global__ void __launch_bounds__(kThreads, 2) adam_kernel(OptArgs a, AdamK k) {
   float* m = reinterpret_cast<float*>(s_base[me] + a.m_off);
   float* v = reinterpret_cast<float*>(s_base[me] + a.v_off);
   const char* pme = s_base[me];
-  for (SegIter it(a.segs, a.offs, a.n_tensors, sb + int64_t(blockIdx.x) * kWarps + warp, se,
-                  int64_t(gridDim.x) * kWarps);
-       it.valid(); it.next()) {
-         const SegD d = it.get();
-         const int64_t q0 = d.toff >> 2, q1 = (d.toff + d.len + 3) >> 2;
-         for (int64_t qb = q0 + lane; qb < q1; qb += 32 * U) {
-           float g[U][Ranks<WT>::kMax][4], mm[U][4], vv[U][4], pp[U][4];
-#pragma unroll
-           for (int u = 0; u < U; ++u) {
-             // clamped, unconditional loads: the compiler can batch all U of them
-             const int64_t q = min(qb + 32 * u, q1 - 1);
-             {
-               const int64_t e0 = q << 2;
-               const int64_t si = d.sidx + (e0 - d.toff);
-               ring_load4<G, COCONET_SUM, WT>(s_base, d.aoff + e0 * int64_t(sizeof(G)), d.owner, W, g[u]);
-               ld4(m + si, mm[u]);
-               ld4(v + si, vv[u]);
-               ld4(reinterpret_cast<const float*>(pme + d.boff) + e0, pp[u]);
-             }
-           }
-#pragma unroll
-           for (int u = 0; u < U; ++u) {
-             const int64_t q = qb + 32 * u;
-             if (q < q1) {
-               const int64_t e0 = q << 2;
-               int lo, hi;
-               quad_range(d, e0, lo, hi);
-               const int64_t si = d.sidx + (e0 - d.toff);
-               float gs[4];
-               ring_fold4<COCONET_SUM, WT>(g[u], W, gs);
-#pragma unroll
-               for (int i = 0; i < 4; ++i) adam_elem<MATH>(gs[i], mm[u][i], vv[u][i], pp[u][i], k);
-               st4m(m + si, mm[u], lo, hi);
-               st4m(v + si, vv[u], lo, hi);
-               if (ONE_SHOT) {
-                 st4m(reinterpret_cast<float*>(s_base[me] + d.boff) + e0, pp[u], lo, hi);
-               } else {
-#pragma unroll
-                 for (int j = 0; j < Ranks<WT>::kMax; ++j)  // AG push, own copy included
-                   if (Ranks<WT>::has(j, W)) st4m(reinterpret_cast<float*>(s_base[j] + d.boff) + e0, pp[u], lo, hi);
-               }
-             }
-           }
-         }
-       }
+  const int64_t wid = int64_t(blockIdx.x) * kWarps + warp, wstride = int64_t(gridDim.x) * kWarps;
+  if (a.parts > 1) {
+    const int P = a.parts;
+    for (int64_t it = wid; it < (se - sb) * P; it += wstride) {
+      const Seg sg = a.segs[sb + it / P];
+      const int part = int(it % P);
+      const int tens = meta_tensor(sg.meta);
+      const SegD d{sg.toff, sg.sidx, a.offs[tens], a.offs[a.n_tensors + tens], meta_len(sg.meta), meta_owner(sg.meta),
+                   tens};
+      const int64_t q0 = d.toff >> 2, nq = ((d.toff + d.len + 3) >> 2) - q0;
+      adam_quads<G, MATH, ONE_SHOT, WT, U>(s_base, d, q0 + nq * part / P, q0 + nq * (part + 1) / P, m, v, pme, me,
+                                           W, lane, k);
+    }
+  } else {
+    for (SegIter it(a.segs, a.offs, a.n_tensors, sb + wid, se, wstride); it.valid(); it.next()) {
+      const SegD d = it.get();
+      adam_quads<G, MATH, ONE_SHOT, WT, U>(s_base, d, d.toff >> 2, (d.toff + d.len + 3) >> 2, m, v, pme, me, W,
+                                           lane, k);
+    }
+  }
   rank_barrier(rs, 1);  // peers done reading our g and writing our p
 }
 
@@ -1169,6 +1193,7 @@ int fill_args(coconet_tlist* tl, OptArgs* a, const RankSet& rs, int64_t m_off, i
   a->os_end = tl->os_end;
   a->m_off = m_off;
   a->v_off = v_off;
+  a->parts = 1;
   return COCONET_OK;
 }
 
@@ -1180,9 +1205,9 @@ int64_t max_rank_segs(const coconet_tlist* tl, int W, bool one_shot) {
 }
 
 int launch_opt(coconet_ctx* c, coconet_tlist* tl, const void* func, void** args, bool one_shot,
-               cudaStream_t stream) {
+               cudaStream_t stream, int parts = 1) {
   int W = c->groups[size_t(tl->group)].size;
-  int64_t want = (max_rank_segs(tl, W, one_shot) + kWarps - 1) / kWarps;
+  int64_t want = (max_rank_segs(tl, W, one_shot) * parts + kWarps - 1) / kWarps;
   int blocks = 0;
   int rc = coop_blocks(c, func, kThreads, 0, tl->group, want, &blocks);
   if (rc) return rc;
@@ -1360,8 +1385,15 @@ int coconet_fused_rs_adam_ag(coconet_ctx_t c, coconet_tlist_t tl, const void* co
   const void* fn = g_elem == COCONET_F32   ? adam_pick<float>(hp->math, os, W)
                    : g_elem == COCONET_F16 ? adam_pick<__half>(hp->math, os, W)
                                            : adam_pick<__nv_bfloat16>(hp->math, os, W);
+  // split segments while the resident grid has idle warps (small lists)
+  int per_sm = 0;
+  CN_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kThreads, 0));
+  const int64_t warps = int64_t(per_sm) * c->sm_count / local_ranks(c, tl->group) * kWarps;
+  const int64_t segs = std::max<int64_t>(1, max_rank_segs(tl, W, os));
+  a.parts = 1;
+  while (a.parts < 8 && segs * a.parts * 2 <= warps) a.parts *= 2;
   void* args[] = {&a, &k};
-  return launch_opt(c, tl, fn, args, os, stream);
+  return launch_opt(c, tl, fn, args, os, stream, a.parts);
 }
 
 int coconet_fused_rs_lamb_ag(coconet_ctx_t c, coconet_tlist_t tl, const void* const* g, int g_elem,
