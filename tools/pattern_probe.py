@@ -148,3 +148,46 @@ def main():
 
 if __name__ == "__main__":
     main()
+
+
+def unfused_baselines(out, steps=5):
+    """The unfused GPU baseline at N=1 (north star: "NCCL plus separate
+    kernels"; one GPU has no collective): the same LAMB step written with
+    torch's multi-tensor _foreach kernels over the same 398 BERT-336M tensors
+    (fp16 grads widened, fp32 p/m/v), and torch._fused_adam_ for Adam."""
+    from paper_2105_05720_b200.workloads import bert_large_counts
+    counts = bert_large_counts()
+    dev = "cuda"
+    g16 = [torch.randn(n, device=dev, dtype=torch.float16) for n in counts]
+    p = [torch.rand(n, device=dev) for n in counts]
+    m = [torch.zeros(n, device=dev) for n in counts]
+    v = [torch.full((n,), 1e-3, device=dev) for n in counts]
+    lr, b1, b2, eps, wd, t = 1e-3, 0.9, 0.999, 1e-6, 0.01, 1.0
+    bc1, bc2 = 1 - b1 ** t, 1 - b2 ** t
+
+    def lamb_step():
+        g = [x.float() for x in g16]
+        torch._foreach_mul_(m, b1)
+        torch._foreach_add_(m, g, alpha=1 - b1)
+        torch._foreach_mul_(v, b2)
+        torch._foreach_addcmul_(v, g, g, value=1 - b2)
+        den = torch._foreach_div(v, bc2)
+        torch._foreach_sqrt_(den)
+        torch._foreach_add_(den, eps)
+        u = torch._foreach_div(m, bc1)
+        torch._foreach_div_(u, den)
+        torch._foreach_add_(u, p, alpha=wd)
+        pn = torch._foreach_norm(p)
+        un = torch._foreach_norm(u)
+        ratio = [lr * a / b for a, b in zip(pn, un)]
+        torch._foreach_mul_(u, ratio)
+        torch._foreach_sub_(p, u)
+
+    ms = timeit(lamb_step, steps)
+    out["unfused_torch_foreach_lamb_bert336m_ms"] = ms
+    del g16
+    g32 = [torch.randn(n, device=dev) for n in counts]
+    steps_t = [torch.tensor(1.0, device=dev) for _ in counts]
+    f = lambda: torch._fused_adam_(p, g32, m, v, [], steps_t, amsgrad=False, lr=1e-3, beta1=0.9, beta2=0.999,
+                                   weight_decay=0.0, eps=1e-8, maximize=False)
+    out["unfused_torch_fused_adam_bert336m_fp32_ms"] = timeit(f, steps)
