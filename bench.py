@@ -366,9 +366,9 @@ def run_coconet(args):
         # protocol cost; "NVLink" traffic is local HBM here) - see DESIGN.md
         try:
             ctx.close()
-            from tools.pattern_probe import c1, c3, c4, c5, unfused_baselines
+            from tools.pattern_probe import c1, c2_w8, c3, c4, c5, unfused_baselines
             extras = {"note": "one GPU, virtual ranks: all ranks' traffic is local HBM"}
-            for f in (c1, c3, c4, c5, unfused_baselines):
+            for f in (c1, c2_w8, c3, c4, c5, unfused_baselines):
                 f(extras)
             if "unfused_torch_foreach_lamb_bert336m_ms" in extras:
                 extras["fused_lamb_speedup_vs_unfused"] = extras["unfused_torch_foreach_lamb_bert336m_ms"] / ms

@@ -191,3 +191,33 @@ def unfused_baselines(out, steps=5):
     f = lambda: torch._fused_adam_(p, g32, m, v, [], steps_t, amsgrad=False, lr=1e-3, beta1=0.9, beta2=0.999,
                                    weight_decay=0.0, eps=1e-8, maximize=False)
     out["unfused_torch_fused_adam_bert336m_fp32_ms"] = timeit(f, steps)
+
+
+def c2_w8(out, steps=5):
+    """The headline step at W=8 with VIRTUAL ranks: the GRID LAMB kernel the
+    8-GPU run uses (RS pulls of fp16 g from 8 ranks, sharded m/v, AG pushes of
+    p into 8 ranks), with all traffic in this GPU's HBM. Bytes per global
+    element summed over ranks: every rank's g read once (8 x 2 B), pass 1
+    m, v, p read + m, v written (20 B), pass 2 m, v, p read (12 B), p pushed
+    into 8 copies (32 B) = 80 B."""
+    from paper_2105_05720_b200.collectives import LambHParams, fused_rs_lamb_ag
+    from paper_2105_05720_b200.workloads import bert_large_counts
+    W = 8
+    counts = bert_large_counts()
+    N = sum(counts)
+    ctx = Context(W, heap_bytes=N * 6 + 2 * (N // W + 64 * len(counts) + 4096) * 4 + (512 << 20))
+    tl = TensorList(ctx, counts, bucket_cap=16384)
+    grads = [ctx.alloc([n], torch.float16) for n in counts]
+    params = [ctx.alloc([n]) for n in counts]
+    m, v = ctx.alloc([tl.shard_elems]), ctx.alloc([tl.shard_elems])
+    for r in range(W):
+        for i, n in enumerate(counts):
+            ctx.view(grads[i], r).normal_()
+            ctx.view(params[i], r).uniform_(0.1, 0.9)
+        ctx.view(m, r).zero_()
+        ctx.view(v, r).fill_(1e-3)
+    hp = LambHParams(lr=1e-3, beta1=0.9, beta2=0.999, t=1.0)
+    ms = timeit(lambda: fused_rs_lamb_ag(ctx, tl, grads, params, m, v, hp), steps, warmup=2)
+    out["c2_lamb_W8_virtual_ms"] = ms
+    out["c2_lamb_W8_virtual_GBs"] = 80 * N / ms / 1e6
+    ctx.close()
