@@ -98,8 +98,13 @@ int coconet_world(coconet_ctx_t ctx, int* world, int* rank, int* mode);
 int coconet_heap_handle(coconet_ctx_t ctx, void* handle_out, size_t* len);
 int coconet_open_peers(coconet_ctx_t ctx, const void* all_handles, size_t len_per_rank);
 /* Symmetric allocation: same offset on every rank; 256-byte aligned. */
+/* Deterministic first-fit over a free list (256-byte granules, neighbours
+ * coalesced on free): alloc/free are collective - every rank issues the same
+ * sequence and gets the same offsets. */
 int coconet_symm_alloc(coconet_ctx_t ctx, size_t bytes, size_t* offset);
+int coconet_symm_free(coconet_ctx_t ctx, size_t offset); /* INVALID_INPUT if not live */
 int coconet_symm_reset(coconet_ctx_t ctx); /* frees every symmetric allocation */
+size_t coconet_symm_high_water(coconet_ctx_t ctx); /* highest offset ever allocated */
 size_t coconet_heap_bytes(coconet_ctx_t ctx); /* per-rank heap size incl. reserved pad */
 /* Device pointer of `offset` in `rank`'s heap (VIRTUAL: any rank;
  * DISTRIBUTED: own rank, or a mapped peer pointer). */

@@ -76,7 +76,9 @@ _SIGNATURES = {
     "coconet_heap_handle": (_I, [_P, _P, C.POINTER(_SZ)]),
     "coconet_open_peers": (_I, [_P, _P, _SZ]),
     "coconet_symm_alloc": (_I, [_P, _SZ, C.POINTER(_SZ)]),
+    "coconet_symm_free": (_I, [_P, _SZ]),
     "coconet_symm_reset": (_I, [_P]),
+    "coconet_symm_high_water": (_SZ, [_P]),
     "coconet_symm_ptr": (_P, [_P, _I, _SZ]),
     "coconet_heap_bytes": (_SZ, [_P]),
     "coconet_group_create": (_I, [_P, _I, _I, C.POINTER(_I)]),

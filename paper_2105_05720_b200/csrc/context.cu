@@ -230,21 +230,28 @@ int coconet_open_peers(coconet_ctx_t c, const void* all, size_t len_per_rank) {
 
 int coconet_symm_alloc(coconet_ctx_t c, size_t bytes, size_t* offset) {
   if (!c || !offset) return set_error(COCONET_ERR_INVALID_INPUT, "null argument");
-  size_t off = (c->heap_used + 255) & ~size_t(255);
-  size_t sz = (bytes + 255) & ~size_t(255);
-  if (off + sz > c->heap_bytes)
-    return set_error(COCONET_ERR_OOM, "symmetric heap exhausted: need " + std::to_string(off + sz) +
-                                          " of " + std::to_string(c->heap_bytes) + " bytes");
-  c->heap_used = off + sz;
-  *offset = off;
+  if (c->alloc.end == 0) c->alloc.init(kReservedBytes, c->heap_bytes);
+  if (!c->alloc.alloc(bytes, offset))
+    return set_error(COCONET_ERR_OOM, "symmetric heap exhausted: need " + std::to_string((bytes + 255) & ~size_t(255)) +
+                                          " bytes, largest free block " + std::to_string(c->alloc.largest_free()) +
+                                          " of " + std::to_string(c->heap_bytes));
+  return COCONET_OK;
+}
+
+int coconet_symm_free(coconet_ctx_t c, size_t offset) {
+  if (!c) return set_error(COCONET_ERR_INVALID_INPUT, "null ctx");
+  if (!c->alloc.release(offset))
+    return set_error(COCONET_ERR_INVALID_INPUT, "offset " + std::to_string(offset) + " is not a live symmetric allocation");
   return COCONET_OK;
 }
 
 int coconet_symm_reset(coconet_ctx_t c) {
   if (!c) return set_error(COCONET_ERR_INVALID_INPUT, "null ctx");
-  c->heap_used = kReservedBytes;
+  c->alloc.init(kReservedBytes, c->heap_bytes);
   return COCONET_OK;
 }
+
+size_t coconet_symm_high_water(coconet_ctx_t c) { return c ? c->alloc.high : 0; }
 
 size_t coconet_heap_bytes(coconet_ctx_t c) { return c ? c->heap_bytes : 0; }
 

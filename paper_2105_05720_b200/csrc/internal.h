@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <map>
 #include <string>
 #include <vector>
 
@@ -16,6 +17,8 @@ struct coconet_group_s {
   uint32_t epoch = 0;  // calls issued on this group (flag value)
 };
 
+#include "symm_heap.h"
+
 struct coconet_ctx {
   int mode = COCONET_MODE_VIRTUAL;
   int world = 1;
@@ -26,7 +29,7 @@ struct coconet_ctx {
   char* heap[coconet::kMaxRanks] = {};
   bool peer_mapped[coconet::kMaxRanks] = {};
   cudaIpcMemHandle_t my_handle{};
-  size_t heap_used = coconet::kReservedBytes;
+  SymmHeap alloc;  // user region [kReservedBytes, heap_bytes)
   int* status_host = nullptr;  // host-mapped watchdog word
   int* status_dev = nullptr;
   uint64_t timeout_ns = 20ull * 1000 * 1000 * 1000;

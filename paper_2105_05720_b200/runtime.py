@@ -152,8 +152,15 @@ class Context:
         check(self.lib.coconet_symm_alloc(self.handle, max(1, buf.nbytes), C.byref(off)))
         return SymmBuffer(off.value, shape, dtype)
 
+    def free(self, buf: SymmBuffer):
+        """Returns `buf` to the symmetric heap (collective, like alloc)."""
+        check(self.lib.coconet_symm_free(self.handle, buf.offset))
+
     def reset(self):
         check(self.lib.coconet_symm_reset(self.handle))
+
+    def high_water(self) -> int:
+        return int(self.lib.coconet_symm_high_water(self.handle))
 
     def view(self, buf: SymmBuffer, rank: int | None = None) -> torch.Tensor:
         r = self.rank if rank is None else rank
