@@ -6,6 +6,7 @@ between contexts that the driver time-slices. Results must equal the
 restated reference bit for bit (EXACT)."""
 import os
 import socket
+import time
 
 import numpy as np
 import pytest
@@ -149,6 +150,7 @@ def _worker_lamb_rooted(rank, world, port, counts, q):
             dist.barrier()
             first = None
             for step in range(3):
+                time.sleep(0.02 * ((rank + step) % world))  # skewed rank start times
                 fused_rs_lamb_ag(ctx, tl, gb, pb, mb, vb,
                                  LambHParams(lr=0.01, beta1=0.9, beta2=0.999, t=float(step + 1), sched=sched,
                                              lag_elems=2000))
@@ -345,3 +347,68 @@ def test_distributed_mp_and_pp_match_virtual(world):
         assert ok_seq, f"rank {rank}: MatMul + fused RS-BDR-AG differs from VIRTUAL mode"
         assert ok_ov, f"rank {rank}: overlapped MatMul+AR differs from VIRTUAL mode"
         assert ok_pp, f"rank {rank}: PP RS->send->AG differs from VIRTUAL mode"
+
+
+def _worker_missing_peer(rank, world, port, q):
+    """Fault injection: rank 1 never joins the collective. Rank 0's kernel must
+    give up on the flag barrier after its watchdog bound and report
+    COCONET_ERR_TIMEOUT through check() - not hang - and the GPU must stay
+    usable (a fresh context runs)."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2105_05720_b200 import _lib
+        from paper_2105_05720_b200.collectives import AdamHParams, TensorList, fused_rs_adam_ag
+        from paper_2105_05720_b200.runtime import Context
+
+        torch.cuda.set_device(0)
+        ctx = Context(world, mode="distributed", rank=rank, device=0, heap_bytes=16 << 20, timeout_ms=300)
+        counts = [4096, 77]
+        tl = TensorList(ctx, counts)
+        gb = [ctx.alloc([n]) for n in counts]
+        pb = [ctx.alloc([n]) for n in counts]
+        mb, vb = ctx.alloc([tl.shard_elems]), ctx.alloc([tl.shard_elems])
+        dist.barrier()
+        name, elapsed = None, 0.0
+        if rank == 0:
+            t0 = time.time()
+            fused_rs_adam_ag(ctx, tl, gb, pb, mb, vb,
+                             AdamHParams(0.01, 0.9, 0.999, 1.0, 0.0, True, _lib.MATH_FAST, _lib.ALGO_TWO_SHOT))
+            try:
+                ctx.check()
+            except _lib.CoconetError as e:
+                name = e.name
+            elapsed = time.time() - t0
+        dist.barrier()
+        ctx.close()
+        usable = True
+        if rank == 0:
+            c2 = Context(1, heap_bytes=16 << 20)
+            x = c2.alloc([16])
+            c2.view(x, 0).fill_(3.0)
+            usable = bool(torch.all(c2.view(x, 0) == 3.0))
+            c2.close()
+        q.put((rank, name, elapsed, usable, None))
+    except Exception as e:
+        q.put((rank, "exception", 0.0, False, repr(e)))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_watchdog_reports_a_missing_peer():
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_missing_peer, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=300) for _ in range(world))
+    for p in procs:
+        p.join(timeout=120)
+    rank0 = res[0]
+    assert rank0[4] is None, rank0[4]
+    assert rank0[1] == "Timeout", rank0
+    assert rank0[2] < 30, f"gave up after {rank0[2]:.1f} s"
+    assert rank0[3], "GPU unusable after the watchdog fired"
