@@ -28,6 +28,7 @@
 #pragma once
 
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
 #include <chrono>
@@ -92,6 +93,12 @@ class GpuEngine {
     cudaEventRecord(e0, stream_);
     for (size_t i = 0; i < pl.steps.size(); ++i) {
       const OpNode& n = *p_.find_node(pl.steps[i]);
+      // one NVTX range per plan step ("step i: id (kind)") for ncu / nsys
+      const std::string tag = "step " + std::to_string(i) + ": " + n.id + " (" + op_kind_name(n.kind) + ")";
+      nvtxRangePushA(tag.c_str());
+      struct PopRange {
+        ~PopRange() { nvtxRangePop(); }
+      } pop_range;
       try {
         exec(n);
         clock += clock_model.step_time(n);
