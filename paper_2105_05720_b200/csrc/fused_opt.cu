@@ -377,8 +377,8 @@ __device__ __forceinline__ float lamb_u(float m, float v, float p, const LambK& 
 //  deterministic) -> pushed into every peer's exchange area -> flag barrier
 //  -> totals combined in rank order (state.hpp:163-167)
 //  pass 2: trust ratio -> p update -> AG push.
-template <typename G, int WT, int U, int MINB = 2>
-__global__ void __launch_bounds__(kThreads, MINB) lamb_kernel(OptArgs a, LambK k) {
+template <typename G, int WT, int U>
+__global__ void __launch_bounds__(kThreads, 2) lamb_kernel(OptArgs a, LambK k) {
   __shared__ char* s_base[kMaxRanks];
   const RankSet& rs = a.rs;
   if (threadIdx.x < kMaxRanks) s_base[threadIdx.x] = threadIdx.x < rs.world ? rs.base[threadIdx.x] : nullptr;
@@ -1442,38 +1442,23 @@ int coconet_fused_rs_lamb_ag(coconet_ctx_t c, coconet_tlist_t tl, const void* co
                                                    : hp->sched;
   if (sched == COCONET_LAMB_TMA) {
     if (W != 1) return set_error(COCONET_ERR_UNSUPPORTED, "the TMA LAMB schedule runs at group size 1");
-    // COCONET_LAMB_TMA_CTAS / _SHAPE: CTAs per SM and consumer shape (probes)
+    // 8 consumer warps x 2 quads per thread (2048-element chunks), 3 CTAs
+    // per SM: the best of the sweep in profiles/r01_lamb_tma_sweep.json
+    // (COCONET_LAMB_TMA_CTAS overrides the CTAs per SM)
     const char* ce = getenv("COCONET_LAMB_TMA_CTAS");
-    const char* sh = getenv("COCONET_LAMB_TMA_SHAPE");
-    // defaults measured on B200 (profiles/r01_lamb_tma_sweep.json): 8 consumer warps x 2 quads
-    // per thread (2048-element chunks), 3 CTAs per SM
     const int per_sm = ce ? std::max(1, std::min(4, atoi(ce))) : 3;
-    const int shape = sh ? atoi(sh) : 1;  // 0: 8 warps x 1 quad, 1: 8 x 2, 2: 16 x 1, 3: 4 x 2
     const void* fn = nullptr;
     int sbytes = 0, threads = 0;
-    auto pick = [&](auto tag_g, auto tag_nw, auto tag_q) {
+    auto pick = [&](auto tag_g) {
       using Gt = decltype(tag_g);
-      constexpr int NW = decltype(tag_nw)::value, Q = decltype(tag_q)::value;
-      fn = reinterpret_cast<const void*>(&lamb_tma_kernel<Gt, NW, Q>);
-      sbytes = TmaStage<Gt, NW, Q>::BYTES;
-      threads = TmaStage<Gt, NW, Q>::THREADS;
+      using ST = TmaStage<Gt, 8, 2>;
+      fn = reinterpret_cast<const void*>(&lamb_tma_kernel<Gt, 8, 2>);
+      sbytes = ST::BYTES;
+      threads = ST::THREADS;
     };
-    auto pick_g = [&](auto tag_g) {
-      using I8 = std::integral_constant<int, 8>;
-      using I16 = std::integral_constant<int, 16>;
-      using I4 = std::integral_constant<int, 4>;
-      using Q1 = std::integral_constant<int, 1>;
-      using Q2 = std::integral_constant<int, 2>;
-      switch (shape) {
-        case 0: pick(tag_g, I8{}, Q1{}); break;
-        case 2: pick(tag_g, I16{}, Q1{}); break;
-        case 3: pick(tag_g, I4{}, Q2{}); break;
-        default: pick(tag_g, I8{}, Q2{}); break;
-      }
-    };
-    if (g_elem == COCONET_F32) pick_g(float{});
-    else if (g_elem == COCONET_F16) pick_g(__half{});
-    else pick_g(__nv_bfloat16{});
+    if (g_elem == COCONET_F32) pick(float{});
+    else if (g_elem == COCONET_F16) pick(__half{});
+    else pick(__nv_bfloat16{});
     TmaArgs ta;
     ta.stages = std::min(16, (200 << 10) / per_sm / sbytes);
     if (ta.stages < 2) return set_error(COCONET_ERR_UNSUPPORTED, "TMA ring does not fit");
