@@ -36,7 +36,10 @@ sys.path.insert(0, str(ROOT))
 METRIC = "fused AR+Adam/LAMB step time & NVLink-roofline fraction, 1/2/4/8 B200"
 UNIT = "Gelem/s"
 NVLINK_GBS = 770.0  # measured peer copy per direction (B200_PROFILING.md)
-BUCKET_CAP = 16384  # segments of the TMA LAMB schedule
+BUCKET_CAP = 16384  # N=1: segments of the TMA LAMB schedule
+BUCKET_CAP_MULTI = 4096  # N>1: the GRID kernel has one warp per segment; with the
+# whole GPU per rank, 16384-element buckets leave ~2600 segments for ~2400 warps
+# (makespan 2 segments), 4096 gives ~10400 (4.4 per warp)
 E2E_GROUPS = 16  # tensor groups pipelined against PCIe in the e2e measurement
 CPU_SAMPLE = 1 << 22  # elements per core for cpu_baseline: ~10-30 s of CPU work
 
@@ -210,7 +213,8 @@ def run_coconet(args):
     # bucket capacity: the reference's 2^10 (runtime.hpp:579) fixes the flat order
     # the parity tests pin; for this workload 4096-element buckets amortise the
     # per-segment cost (descriptor + per-segment norm reduction), DESIGN.md §3
-    tl = TensorList(ctx, counts, bucket_cap=BUCKET_CAP)
+    cap = BUCKET_CAP if world == 1 else BUCKET_CAP_MULTI
+    tl = TensorList(ctx, counts, bucket_cap=cap)
     # one flat buffer per dtype (tensors at 64-element aligned offsets) so the
     # unfused baseline can hand all gradients to ONE NCCL all_reduce
     from paper_2105_05720_b200.runtime import SymmBuffer
@@ -275,7 +279,7 @@ def run_coconet(args):
     if distributed and not share:
         try:  # the baseline is reported, never allowed to sink the bench line
             g1 = ctx.group(rank, 1)
-            tl1 = TensorList(ctx, counts, group=g1, bucket_cap=BUCKET_CAP)
+            tl1 = TensorList(ctx, counts, group=g1, bucket_cap=BUCKET_CAP)  # size-1 group: the TMA path
             m1 = ctx.alloc([tl1.shard_elems], torch.float32)
             v1 = ctx.alloc([tl1.shard_elems], torch.float32)
             ctx.view(m1).zero_()
@@ -311,7 +315,7 @@ def run_coconet(args):
     offsets = [0]
     for pn in padded[:-1]:
         offsets.append(offsets[-1] + pn)
-    pipe = LambHostPipeline(ctx, counts, flat_g, flat_p, offsets, groups=E2E_GROUPS, bucket_cap=BUCKET_CAP)
+    pipe = LambHostPipeline(ctx, counts, flat_g, flat_p, offsets, groups=E2E_GROUPS, bucket_cap=cap)
     for (pm, pv) in pipe.state():
         ctx.view(pm).uniform_(-1e-3, 1e-3)
         ctx.view(pv).uniform_(1e-4, 1e-3)
@@ -398,7 +402,7 @@ def run_coconet(args):
                                    "fp32 master weights + m/v, fused ReduceScatter+LAMB+AllGather",
                        "global_batch": None, "seq_len": None, "parallelism": f"dp{world}",
                        "l2": "per-step traffic ~13 GB >> 126 MB L2 (no flush needed)",
-                       "math": "FAST (fp32 element math, fp64 norms)", "bucket_cap": BUCKET_CAP},
+                       "math": "FAST (fp32 element math, fp64 norms)", "bucket_cap": cap},
             "roofline": roof, "cpu_baseline": cpu,
             "e2e": {"value": W * N / e2e_s / 1e9, "unit": UNIT, "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h,
