@@ -62,6 +62,7 @@ template <int BN> struct Cfg {
 
 struct RankMaps {
   CUtensorMap a[kMaxRanks];
+  CUtensorMap a_half[kMaxRanks];  // 64-row boxes: the multicast halves of A (MC)
   CUtensorMap b[kMaxRanks];
   CUtensorMap c[kMaxRanks];  // output, stored by TMA from swizzled staging tiles
 };
@@ -82,6 +83,25 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, i
           smem_u32(dst)),
       "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
       : "memory");
+}
+
+// TMA load multicast to every CTA of the cluster in `mask` (same smem offset
+// and the barrier at the same offset in each destination CTA).
+__device__ __forceinline__ void tma_load_2d_mc(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar,
+                                               uint16_t mask) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster [%0], [%1, {%2, "
+      "%3}], [%4], %5;" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar)), "h"(mask)
+      : "memory");
+}
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 
 __device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void* src, int c0, int c1) {
@@ -128,6 +148,14 @@ __device__ __forceinline__ void mma_f16(uint32_t d, uint64_t a, uint64_t b, uint
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
                : "memory");
+}
+// arrive on `bar` in both CTAs of a 2-CTA cluster once these MMAs retire
+__device__ __forceinline__ void mma_commit_both(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          smem_u32(bar)),
+      "h"(uint16_t(3))
+      : "memory");
 }
 
 __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
@@ -190,6 +218,21 @@ __device__ __forceinline__ void decode_tile(const GemmArgs& g, int t, int& r, in
   const int j = t - mt * per_m;
   nt = j / g.ranks;
   r = j - nt * g.ranks;
+}
+
+// MC: tile t of the pair sequence; CTA crank of the cluster takes column tile 2j + crank
+template <bool MC>
+__device__ __forceinline__ void decode_tile2(const GemmArgs& g, int t, uint32_t crank, int& r, int& mt, int& nt) {
+  if constexpr (MC) {
+    const int per_m = (g.tiles_n / 2) * g.ranks;
+    mt = t / per_m;
+    const int j = t - mt * per_m;
+    const int np = j / g.ranks;
+    r = j - np * g.ranks;
+    nt = 2 * np + int(crank);
+  } else {
+    decode_tile(g, t, r, mt, nt);
+  }
 }
 
 // ---- fused all-reduce epilogue of the overlapped MatMul (mp_overlap.json) ----
@@ -338,9 +381,15 @@ __device__ void mp_comm_warp(const OvArgs& a, char* const* base, int lane) {
   }
 }
 
-template <int BN, typename TO, bool FUSED>
+// MC (plain GEMM only): clusters of 2 CTAs compute column tiles 2j and 2j+1
+// of the same row tile; each CTA loads one 64-row half of the shared A tile
+// and multicasts it into both CTAs, so A crosses L2 once per pair. The stage
+// barriers then count both CTAs' MMAs (either CTA's producer writes into both
+// CTAs' stages).
+template <int BN, typename TO, bool FUSED, bool MC>
 __global__ void __launch_bounds__(FUSED ? kFusedThreads : kGemmThreads, 1)
     gemm_tc_kernel(const __grid_constant__ RankMaps maps, GemmArgs g, uint32_t in_fmt, OvArgs ov) {
+  static_assert(!(MC && FUSED), "multicast is for the plain GEMM");
   __shared__ char* s_base[kMaxRanks];
   if (FUSED && threadIdx.x < kMaxRanks)
     s_base[threadIdx.x] = threadIdx.x < ov.rs.world ? ov.rs.base[threadIdx.x] : nullptr;
@@ -356,7 +405,7 @@ __global__ void __launch_bounds__(FUSED ? kFusedThreads : kGemmThreads, 1)
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < Cfg<BN>::STAGES; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
+      mbar_init(&empty[s], MC ? 2 : 1);
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
@@ -373,23 +422,32 @@ __global__ void __launch_bounds__(FUSED ? kFusedThreads : kGemmThreads, 1)
   }
   tc_fence_before();
   __syncthreads();
+  if constexpr (MC) cluster_sync();  // the peer multicasts into our barriers: they must exist
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  const int total = g.ranks * g.tiles_m * g.tiles_n;
+  const uint32_t crank = MC ? cluster_ctarank() : 0u;
+  // MC: the cluster walks pair tiles (column tiles 2j, 2j+1), CTA crank takes 2j + crank
+  const int total = MC ? g.ranks * g.tiles_m * (g.tiles_n / 2) : g.ranks * g.tiles_m * g.tiles_n;
+  const int tile0 = MC ? int(blockIdx.x >> 1) : int(blockIdx.x);
+  const int tstride = MC ? int(gridDim.x >> 1) : int(gridDim.x);
   const int kblocks = g.K / BK;
 
   if (warp == 0) {
     if (lane == 0) {  // ---- TMA producer
       int stage = 0;
       uint32_t phase = 0;
-      for (int t = blockIdx.x; t < total; t += gridDim.x) {
+      for (int t = tile0; t < total; t += tstride) {
         int r, mt, nt;
-        decode_tile(g, t, r, mt, nt);
+        decode_tile2<MC>(g, t, crank, r, mt, nt);
         for (int kb = 0; kb < kblocks; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* sa = smem + stage * Cfg<BN>::STAGE_BYTES;
           mbar_expect_tx(&full[stage], Cfg<BN>::STAGE_BYTES);
-          tma_load_2d(sa, &maps.a[r], kb * BK, mt * BM, &full[stage]);
+          if constexpr (MC)  // our 64-row half of A into both CTAs
+            tma_load_2d_mc(sa + crank * (Cfg<BN>::A_BYTES / 2), &maps.a_half[r], kb * BK, mt * BM + int(crank) * 64,
+                           &full[stage], uint16_t(3));
+          else
+            tma_load_2d(sa, &maps.a[r], kb * BK, mt * BM, &full[stage]);
 #pragma unroll
           for (int j = 0; j < BN / 64; ++j)  // B [K, N] row-major: 64 n x 64 k boxes
             tma_load_2d(sa + Cfg<BN>::A_BYTES + j * kMnBlockBytes, &maps.b[r], nt * BN + j * 64, kb * BK,
@@ -412,7 +470,7 @@ __global__ void __launch_bounds__(FUSED ? kFusedThreads : kGemmThreads, 1)
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
-      for (int t = blockIdx.x; t < total; t += gridDim.x) {
+      for (int t = tile0; t < total; t += tstride) {
         mbar_wait(&tempty[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d = tmem + uint32_t(acc * kAccStride);
@@ -424,7 +482,10 @@ __global__ void __launch_bounds__(FUSED ? kFusedThreads : kGemmThreads, 1)
 #pragma unroll
           for (int k = 0; k < BK / 16; ++k)  // per UMMA_K = 16: A +32 bytes along K, B +16 k-rows (2 KB)
             mma_f16(d, da + 2 * k, db + uint64_t(k) * ((16 * 128) >> 4), idesc, (kb | k) != 0);
-          mma_commit(&empty[stage]);  // frees the smem stage once these MMAs retire
+          if constexpr (MC)
+            mma_commit_both(&empty[stage]);  // both CTAs' producers write into this stage
+          else
+            mma_commit(&empty[stage]);  // frees the smem stage once these MMAs retire
           if (++stage == Cfg<BN>::STAGES) {
             stage = 0;
             phase ^= 1;
@@ -446,9 +507,9 @@ __global__ void __launch_bounds__(FUSED ? kFusedThreads : kGemmThreads, 1)
     int acc = 0, buf = 0;
     uint32_t acc_phase = 0;
     uint32_t* pend_flag = nullptr;  // tile flag published once its stores are complete
-    for (int t = blockIdx.x; t < total; t += gridDim.x) {
+    for (int t = tile0; t < total; t += tstride) {
       int r, mt, nt;
-      decode_tile(g, t, r, mt, nt);
+      decode_tile2<MC>(g, t, crank, r, mt, nt);
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
       const uint32_t tbase = tmem + (uint32_t(q * 32) << 16) + uint32_t(acc * kAccStride);
@@ -523,6 +584,7 @@ __global__ void __launch_bounds__(FUSED ? kFusedThreads : kGemmThreads, 1)
   }
   tc_fence_before();
   __syncthreads();
+  if constexpr (MC) cluster_sync();  // no CTA leaves while its peer may still multicast into it
   tc_fence_after();
   if (warp == 2)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols) : "memory");
@@ -636,6 +698,7 @@ int plan_tc(coconet_ctx* c, int group, const void* a, const void* b, void* cc, i
     const int wr = c->mode == COCONET_MODE_VIRTUAL ? grp.first + i : c->rank;
     char* heap = c->heap[wr];
     rc = make_map(&p->maps.a[i], heap + ao, in_elem, uint64_t(k), uint64_t(m), BK, BM);
+    if (!rc) rc = make_map(&p->maps.a_half[i], heap + ao, in_elem, uint64_t(k), uint64_t(m), BK, BM / 2);
     // B in its natural row-major [K, N] layout, read MN-major (64 n x 64 k boxes)
     if (!rc) rc = make_map(&p->maps.b[i], heap + bo, in_elem, uint64_t(n), uint64_t(k), 64, BK);
     if (!rc)
@@ -656,20 +719,42 @@ int plan_tc(coconet_ctx* c, int group, const void* a, const void* b, void* cc, i
 
 template <int BN, typename TO, bool FUSED>
 int launch_tc_t(coconet_ctx* c, TcPlan* p, uint32_t in_fmt, const OvArgs* ov, cudaStream_t s) {
-  auto fn = gemm_tc_kernel<BN, TO, FUSED>;
   const int smem = Cfg<BN>::SMEM;
-  CN_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   const int total = p->g.ranks * p->g.tiles_m * p->g.tiles_n;
   OvArgs none{};
   const OvArgs& o = ov ? *ov : none;
-  if (!FUSED) {
-    const int grid = std::min(total, c->sm_count);
-    fn<<<grid, kGemmThreads, smem, s>>>(p->maps, p->g, in_fmt, o);
-    CN_CUDA(cudaGetLastError());
+  if constexpr (!FUSED) {
+    const char* e = getenv("COCONET_GEMM_MC");
+    const bool mc = p->g.tiles_n % 2 == 0 && !(e && e[0] == '0');
+    if (mc) {  // 2-CTA clusters sharing A by multicast
+      auto fn = gemm_tc_kernel<BN, TO, false, true>;
+      CN_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+      cudaLaunchConfig_t cfg{};
+      cfg.gridDim = dim3(unsigned(2 * std::min(total / 2, c->sm_count / 2)));
+      cfg.blockDim = dim3(kGemmThreads);
+      cfg.dynamicSmemBytes = size_t(smem);
+      cfg.stream = s;
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeClusterDimension;
+      attr[0].val.clusterDim.x = 2;
+      attr[0].val.clusterDim.y = 1;
+      attr[0].val.clusterDim.z = 1;
+      cfg.attrs = attr;
+      cfg.numAttrs = 1;
+      CN_CUDA(cudaLaunchKernelEx(&cfg, fn, p->maps, p->g, in_fmt, o));
+    } else {
+      auto fn = gemm_tc_kernel<BN, TO, false, false>;
+      CN_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+      const int grid = std::min(total, c->sm_count);
+      fn<<<grid, kGemmThreads, smem, s>>>(p->maps, p->g, in_fmt, o);
+      CN_CUDA(cudaGetLastError());
+    }
   } else {
     // every CTA both computes tiles and all-reduces: co-residency (one CTA
     // per SM) is guaranteed by the cooperative launch, so comm warps spinning
     // on tile flags can never starve the CTAs that publish them
+    auto fn = gemm_tc_kernel<BN, TO, true, false>;
+    CN_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     const int grid = c->sm_count;
     void* args[] = {const_cast<RankMaps*>(&p->maps), &p->g, &in_fmt, const_cast<OvArgs*>(&o)};
     CN_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(fn), dim3(grid), dim3(kFusedThreads), args, smem, s));
