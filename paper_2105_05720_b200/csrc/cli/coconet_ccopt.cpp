@@ -12,6 +12,11 @@
 //                                      by measured device time); sim: ccopt::tune
 //
 // CUDA-only options: --device D, --math exact|fast, --reps R (tune), --no-fused.
+// Tensor files (the reference's write_tensor_file / read_tensor_file format,
+// json_io.hpp:580-608: little-endian f32 + JSON sidecar), run only:
+//   --input NAME=BASE   decl NAME's global tensor from BASE.{bin,json} instead
+//                       of gen_decl_values (sliced decls take their slice)
+//   --dump DIR          every result array as DIR/<key>_r<rank>.{bin,json}
 #include <cstdio>
 #include <cstdlib>
 #include <iostream>
@@ -34,6 +39,8 @@ namespace {
 struct Opts {
   std::string cmd, program_path, schedule_path, out_path, other_path;
   std::vector<std::string> sizes;
+  std::vector<std::string> inputs;  // NAME=BASE
+  std::string dump_dir;
   int ranks = 4, channels = 2;
   std::string protocol = "simple";
   double alpha = 0.5, beta = 2000.0, gamma = 2000.0, lambda = 0.5;
@@ -55,7 +62,8 @@ struct Opts {
                "  [--schedule S.json] [--ranks W] [--size NAME=VALUE]... [--seed N] [--tol T] [--out F]\n"
                "  [--channels C] [--protocol ll|simple] [--alpha A] [--beta B] [--gamma G] [--lambda L]\n"
                "  [--tile T] [--threaded] [--wall-time]\n"
-               "  [--backend cuda|sim] [--device D] [--math exact|fast] [--reps R] [--no-fused]\n";
+               "  [--backend cuda|sim] [--device D] [--math exact|fast] [--reps R] [--no-fused]\n"
+               "  [--input NAME=BASE]... [--dump DIR]\n";
   std::exit(2);
 }
 
@@ -98,6 +106,8 @@ Opts parse(int argc, char** argv) {
       else if (m == "fast") o.math = COCONET_MATH_FAST;
       else usage("--math must be exact or fast");
     } else if (a == "--no-fused") o.fused = false;
+    else if (a == "--input") o.inputs.push_back(val());
+    else if (a == "--dump") o.dump_dir = val();
     else if (!a.empty() && a[0] == '-') usage("unknown option " + a);
     else pos.push_back(a);
   }
@@ -239,16 +249,51 @@ int cmd_transform(const Opts& o) {
   return 0;
 }
 
+// gen_decl_values with --input overrides: each rank's storage of decl NAME
+// takes the file's global tensor through its DistView (state.hpp:17-50).
+ValueMap decl_values(const Opts& o, const Program& p) {
+  ValueMap vals = gen_decl_values(p, o.seed);
+  for (auto& spec : o.inputs) {
+    const auto eq = spec.find('=');
+    if (eq == std::string::npos) throw Error(ErrCode::ParseError, "--input expects NAME=BASE, got '" + spec + "'");
+    const std::string name = spec.substr(0, eq), base = spec.substr(eq + 1);
+    auto it = vals.find(name);
+    if (it == vals.end()) throw Error(ErrCode::UnknownId, "--input: no decl '" + name + "'");
+    Shape shape;
+    std::vector<float> data = read_tensor_file(base, nullptr, &shape);
+    TensorVal& t = it->second;
+    if (shape != t.view.global) throw Error(ErrCode::ShapeMismatch, "--input " + name + ": shape differs from the decl");
+    for (size_t r = 0; r < t.per_rank.size(); ++r)
+      for (int64_t li = 0; li < t.view.local_elems(); ++li)
+        t.per_rank[r][size_t(li)] = t.view.layout.is_sliced() ? data[size_t(t.view.to_global(int(r), li))]
+                                                              : data[size_t(li)];
+  }
+  return vals;
+}
+
+void dump_results(const Opts& o, const std::map<std::string, Collected>& res) {
+  if (o.dump_dir.empty()) return;
+  for (auto& [key, c] : res)
+    for (size_t r = 0; r < c.data.size(); ++r) {
+      std::string stem = key;
+      for (auto& ch : stem)
+        if (ch == ':' || ch == '/') ch = '_';
+      const Shape shape = int64_t(c.data[r].size()) == num_elems(c.shape) ? c.shape : Shape{int64_t(c.data[r].size())};
+      write_tensor_file(o.dump_dir + "/" + stem + "_r" + std::to_string(r), key, shape, Elem::F32, c.data[r]);
+    }
+}
+
 int cmd_run(const Opts& o) {
   Program base = load_program(o, o.program_path);
   Program p = transformed(o, o.program_path);
-  auto oracle_ref = oracle_results(base, gen_decl_values(base, o.seed), o.seed);
+  auto oracle_ref = oracle_results(base, decl_values(o, base), o.seed);
   Json j;
   double dev = 0;
   if (o.backend == "cuda") {
     coconet::GpuEngine eng(p, comm_config(o), o.seed, gpu_options(o));
-    RunReport rep = eng.run(gen_decl_values(p, o.seed));
+    RunReport rep = eng.run(decl_values(o, p));
     dev = compare_results(oracle_ref, rep.results);
+    dump_results(o, rep.results);
     j = run_report_json(o, rep, dev);
     j["backend"] = "cuda";
     j["device_ms"] = eng.device_ms();
@@ -256,8 +301,9 @@ int cmd_run(const Opts& o) {
     j["math"] = o.math == COCONET_MATH_EXACT ? "exact" : "fast";
   } else {
     Engine eng(p, comm_config(o), o.seed);
-    RunReport rep = eng.run(gen_decl_values(p, o.seed));
+    RunReport rep = eng.run(decl_values(o, p));
     dev = compare_results(oracle_ref, rep.results);
+    dump_results(o, rep.results);
     j = run_report_json(o, rep, dev);
     j["backend"] = "sim";
   }

@@ -3,6 +3,7 @@ subcommands that never touch the data path, the simulated backend reproducing
 the reference Engine's golden digests, argument errors (exit 2), and that the
 CUDA backend fails loudly without a device instead of falling back."""
 import json
+from pathlib import Path
 
 from tests.cli_util import GOLD, cli, dims_args, need_cli, program_file
 
@@ -53,3 +54,48 @@ def test_cuda_backend_fails_loudly_without_a_device(tmp_path):
     f, rec = program_file(tmp_path, "adam_W4_N4096", "sched_program")
     p = cli("run", f, *dims_args(rec))
     assert p.returncode == 2 and "error" in p.stderr.lower()
+
+
+def _write_tensor(base, name, arr):
+    """The reference's tensor file (json_io.hpp:580-593): f32 .bin + JSON sidecar."""
+    import numpy as np
+    np.asarray(arr, dtype="<f4").tofile(str(base) + ".bin")
+    (Path(str(base) + ".json")).write_text(json.dumps({"name": name, "shape": list(arr.shape), "elem": "f32"}))
+
+
+def test_tensor_file_io_round_trip(tmp_path):
+    """--input reads decls from tensor files, --dump writes every result array:
+    feeding the values gen_decl_values would make reproduces the golden digest,
+    and the dumped arrays hash to the report's per-key digests."""
+    need_cli()
+    import numpy as np
+
+    from oracle import coconet_oracle as co
+    f, rec = program_file(tmp_path, "adam_W4_N4096", "sched_program")
+    W, N = rec["dims"]["W"], rec["dims"]["N"]
+    p = co.gen_decl(1, "p", [N], "replicated", 0, W)
+    m = co.gen_decl(1, "m", [N], "replicated", 0, W)  # global view of the sliced decl
+    _write_tensor(tmp_path / "p", "p", np.asarray(p))
+    _write_tensor(tmp_path / "m", "m", np.asarray(m))
+    out = tmp_path / "dump"
+    out.mkdir()
+    j = json.loads(cli("run", f, *dims_args(rec), "--backend", "sim", "--input", f"p={tmp_path / 'p'}",
+                       "--input", f"m={tmp_path / 'm'}", "--dump", out, check_rc=0).stdout)
+    assert j["digest"] == rec["engine_sched_digest"]
+    for key, summ in j["results"].items():
+        stem = key.replace(":", "_").replace("/", "_")
+        files = sorted(out.glob(f"{stem}_r*.bin"), key=lambda x: int(x.stem.rsplit("_r", 1)[1]))
+        assert files, key
+        h = co.FNV_OFFSET
+        for fb in files:
+            side = json.loads(fb.with_suffix(".json").read_text())
+            assert side["name"] == key and side["elem"] == "f32"
+            h = co.fnv1a(np.fromfile(fb, dtype="<f4").tobytes(), h)
+        assert "%016x" % h == summ["digest"], key
+    # a different p changes the result; a wrong shape is rejected
+    _write_tensor(tmp_path / "p2", "p", np.asarray(p) * 2)
+    j2 = json.loads(cli("run", f, *dims_args(rec), "--backend", "sim", "--input", f"p={tmp_path / 'p2'}",
+                        check_rc=0).stdout)
+    assert j2["digest"] != rec["engine_sched_digest"]
+    _write_tensor(tmp_path / "bad", "p", np.zeros(7, np.float32))
+    assert cli("run", f, *dims_args(rec), "--backend", "sim", "--input", f"p={tmp_path / 'bad'}").returncode == 2

@@ -65,3 +65,28 @@ def test_engine_gpu_tune_python_binding():
         pytest.skip("libcoconet_engine.so not built")
     j = engine.gpu_tune(ref["program"], dims={"W": 4, "N": 4096}, reps=2)
     _check_tune(j, ref)
+
+
+def test_run_cuda_tensor_files_match_sim(tmp_path):
+    """--input / --dump on the CUDA backend: the same tensor-file inputs give
+    the reference Engine's digest, and the dumped result files are byte-equal
+    to the simulated backend's."""
+    need_cli()
+    import numpy as np
+
+    from oracle import coconet_oracle as co
+    f, rec = program_file(tmp_path, "adam_W4_N4096", "sched_program")
+    W, N = rec["dims"]["W"], rec["dims"]["N"]
+    for name in ("p", "m"):
+        arr = np.asarray(co.gen_decl(1, name, [N], "replicated", 0, W), dtype="<f4")
+        arr.tofile(str(tmp_path / name) + ".bin")
+        (tmp_path / f"{name}.json").write_text(json.dumps({"name": name, "shape": [N], "elem": "f32"}))
+    dumps = {}
+    for backend in ("cuda", "sim"):
+        out = tmp_path / f"dump_{backend}"
+        out.mkdir()
+        j = json.loads(cli("run", f, *dims_args(rec), "--backend", backend, "--input", f"p={tmp_path / 'p'}",
+                           "--input", f"m={tmp_path / 'm'}", "--dump", out, check_rc=0).stdout)
+        assert j["digest"] == rec["engine_sched_digest"], backend
+        dumps[backend] = {x.name: x.read_bytes() for x in out.iterdir()}
+    assert dumps["cuda"] == dumps["sim"]
