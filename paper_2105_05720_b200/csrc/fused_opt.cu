@@ -1220,9 +1220,12 @@ int elem_bytes(int e) { return e == COCONET_F32 ? 4 : 2; }
 bool resolve_one_shot(int algo, const coconet_tlist* tl, int W) {
   if (algo == COCONET_ALGO_ONE_SHOT) return true;
   if (algo == COCONET_ALGO_TWO_SHOT) return false;
-  // AUTO: the paper's crossover (AR-Opt best up to 2^16 elements,
-  // PAPER.md:1558-1565); at W == 1 both are the same local update.
-  return W > 1 && tl->total <= (int64_t(1) << 16);
+  // AUTO: the crossover measured on B200 (profiles/r01_oneshot_twoshot_crossover.json):
+  // up to 2^14 elements both variants sit on the launch + flag-barrier floor,
+  // from 2^16 two-shot wins, so one-shot only for tiny lists (the paper's V100
+  // crossover was 2^16); at W == 1 both are the same
+  // local update.
+  return W > 1 && tl->total <= (int64_t(1) << 12);
 }
 
 // ---- instantiation tables: group size specialised for 1, 2, 4, 8 ranks,
