@@ -151,10 +151,7 @@ def check(status: int) -> None:
 
 
 def ptr_array(ptrs) -> C.Array:
-    arr = (C.c_void_p * len(ptrs))()
-    for i, p in enumerate(ptrs):
-        arr[i] = p
-    return arr
+    return (C.c_void_p * len(ptrs))(*ptrs)
 
 
 def i64_array(vals) -> C.Array:

@@ -175,6 +175,10 @@ __device__ __forceinline__ bool wait_flag(const uint32_t* p, uint32_t want, cons
 // every other rank of the group: thread q < W signals rank q and waits for
 // rank q. `fence` orders this CTA's prior (remote) writes before the signal.
 __device__ __forceinline__ bool rank_barrier(const RankSet& rs, int phase) {
+  if (rs.world == 1) {  // no peer to meet
+    __syncthreads();
+    return true;
+  }
   __syncthreads();
   bool ok = true;
   const int me = rs.rank();
@@ -185,6 +189,20 @@ __device__ __forceinline__ bool rank_barrier(const RankSet& rs, int phase) {
     ok = wait_flag(flag_slot(rs.base[me], rs.group, phase, q, blockIdx.x), rs.epoch, rs);
   }
   return __syncthreads_and(ok);
+}
+
+// Entry / exit barrier of a kernel whose ranks touch disjoint data inside the
+// launch (each rank reads every peer's input chunk r and writes chunk r of
+// every peer's output). It orders the launch against the peers' producers
+// before and consumers after it, which only separate processes need: in
+// VIRTUAL mode every rank is a slice of this grid and stream order already
+// does it, so the CTA only syncs its own threads.
+__device__ __forceinline__ bool edge_barrier(const RankSet& rs, int phase) {
+  if (rs.me < 0) {
+    __syncthreads();
+    return true;
+  }
+  return rank_barrier(rs, phase);
 }
 
 __device__ __forceinline__ bool failed(const RankSet& rs) {

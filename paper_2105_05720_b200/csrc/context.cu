@@ -70,10 +70,31 @@ int heap_offset(const coconet_ctx* c, const void* p, int64_t* off) {
   return COCONET_OK;
 }
 
+int occupancy(coconet_ctx* c, const void* func, int threads, size_t smem, int* per_sm) {
+  const auto key = std::make_tuple(func, threads, smem);
+  auto it = c->occupancy.find(key);
+  if (it == c->occupancy.end()) {
+    int n = 0;
+    CN_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, func, threads, smem));
+    it = c->occupancy.emplace(key, n).first;
+  }
+  *per_sm = it->second;
+  return COCONET_OK;
+}
+
+int ensure_smem(coconet_ctx* c, const void* func, size_t smem) {
+  auto it = c->smem_set.find(func);
+  if (it != c->smem_set.end() && size_t(it->second) >= smem) return COCONET_OK;
+  CN_CUDA(cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+  c->smem_set[func] = int(smem);
+  return COCONET_OK;
+}
+
 int coop_blocks(coconet_ctx* c, const void* func, int threads, size_t smem, int group,
                 int64_t want, int* blocks) {
   int per_sm = 0;
-  CN_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, func, threads, smem));
+  int rc = occupancy(c, func, threads, smem, &per_sm);
+  if (rc) return rc;
   if (per_sm < 1) return set_error(COCONET_ERR_CUDA, "kernel cannot be resident (occupancy 0)");
   int64_t cap = int64_t(per_sm) * c->sm_count / local_ranks(c, group);
   if (cap > kMaxBlocks) cap = kMaxBlocks;

@@ -276,7 +276,7 @@ __global__ void __launch_bounds__(kThreads, 2) adam_kernel(OptArgs a, AdamK k) {
   if (threadIdx.x < kMaxRanks) s_base[threadIdx.x] = threadIdx.x < rs.world ? rs.base[threadIdx.x] : nullptr;
   const int W = WT > 0 ? WT : rs.world;
   const int me = rs.rank();
-  if (!rank_barrier(rs, 0)) return;  // peers' gradients are complete
+  if (!edge_barrier(rs, 0)) return;  // peers' gradients are complete
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t sb = ONE_SHOT ? a.os_begin : a.seg_begin[me];
   const int64_t se = ONE_SHOT ? a.os_end : a.seg_begin[me + 1];
@@ -303,7 +303,7 @@ __global__ void __launch_bounds__(kThreads, 2) adam_kernel(OptArgs a, AdamK k) {
                                            lane, k);
     }
   }
-  rank_barrier(rs, 1);  // peers done reading our g and writing our p
+  edge_barrier(rs, 1);  // peers done reading our g and writing our p
 }
 
 // Tensor-list AllReduce (x -> out). TWO_SHOT = pull-RS of the own chunk +
@@ -315,7 +315,7 @@ __global__ void __launch_bounds__(kThreads, 2) allreduce_kernel(OptArgs a) {
   if (threadIdx.x < kMaxRanks) s_base[threadIdx.x] = threadIdx.x < rs.world ? rs.base[threadIdx.x] : nullptr;
   const int W = WT > 0 ? WT : rs.world;
   const int me = rs.rank();
-  if (!rank_barrier(rs, 0)) return;
+  if (!edge_barrier(rs, 0)) return;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t sb = ONE_SHOT ? a.os_begin : a.seg_begin[me];
   const int64_t se = ONE_SHOT ? a.os_end : a.seg_begin[me + 1];
@@ -351,7 +351,7 @@ __global__ void __launch_bounds__(kThreads, 2) allreduce_kernel(OptArgs a) {
            }
          }
        }
-  rank_barrier(rs, 1);
+  edge_barrier(rs, 1);
 }
 
 __device__ __forceinline__ float warp_sumf(float x) {
@@ -386,7 +386,7 @@ __global__ void __launch_bounds__(kThreads, 2) lamb_kernel(OptArgs a, LambK k) {
   const int me = rs.rank();
   // No early return before the grid syncs: a CTA whose barrier timed out
   // skips its work but still arrives, so the grid cannot deadlock.
-  const bool ok = rank_barrier(rs, 0);
+  const bool ok = edge_barrier(rs, 0);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t sb = a.seg_begin[me], se = ok ? a.seg_begin[me + 1] : sb;
   float* m = reinterpret_cast<float*>(s_base[me] + a.m_off);
@@ -519,7 +519,7 @@ __global__ void __launch_bounds__(kThreads, 2) lamb_kernel(OptArgs a, LambK k) {
       }
     }
   }
-  rank_barrier(rs, 1);
+  edge_barrier(rs, 1);
 }
 
 // ---- LAMB, TMA schedule (W = 1): the GRID algorithm with its two streaming
@@ -649,7 +649,7 @@ __global__ void __launch_bounds__((NW + 1) * 32) lamb_tma_kernel(OptArgs a, Lamb
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   }
   const int me = rs.rank();
-  const bool ok = rank_barrier(rs, 0);  // also publishes the barrier inits to the CTA
+  const bool ok = edge_barrier(rs, 0);  // also publishes the barrier inits to the CTA
   const int64_t sb = a.seg_begin[me], se = ok ? a.seg_begin[me + 1] : sb;
   float* m = reinterpret_cast<float*>(s_base[me] + a.m_off);
   float* v = reinterpret_cast<float*>(s_base[me] + a.v_off);
@@ -793,7 +793,7 @@ __global__ void __launch_bounds__((NW + 1) * 32) lamb_tma_kernel(OptArgs a, Lamb
       }
     }
   }
-  rank_barrier(rs, 1);
+  edge_barrier(rs, 1);
 }
 
 // ---- Adam, TMA schedule (W = 1): one pass, the producer of lamb_tma_kernel
@@ -820,7 +820,7 @@ __global__ void __launch_bounds__((NW + 1) * 32) adam_tma_kernel(OptArgs a, Adam
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   }
   const int me = rs.rank();
-  const bool ok = rank_barrier(rs, 0);
+  const bool ok = edge_barrier(rs, 0);
   const int64_t sb = a.seg_begin[me], se = ok ? a.seg_begin[me + 1] : sb;
   float* m = reinterpret_cast<float*>(s_base[me] + a.m_off);
   float* v = reinterpret_cast<float*>(s_base[me] + a.v_off);
@@ -883,7 +883,7 @@ __global__ void __launch_bounds__((NW + 1) * 32) adam_tma_kernel(OptArgs a, Adam
       }
     }
   }
-  rank_barrier(rs, 1);
+  edge_barrier(rs, 1);
 }
 
 // STREAMED-LAMB bookkeeping (tlist_stream_plan).
@@ -1009,7 +1009,7 @@ __global__ void __launch_bounds__(NT, 512 / NT) lamb_stream_kernel(OptArgs a, La
   if (threadIdx.x < kMaxRanks) s_base[threadIdx.x] = threadIdx.x < rs.world ? rs.base[threadIdx.x] : nullptr;
   const int W = WT > 0 ? WT : rs.world;
   const int me = rs.rank();
-  const bool ok = rank_barrier(rs, 0);
+  const bool ok = edge_barrier(rs, 0);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int n = a.n_tensors;
   const int64_t ib = ls.item_begin[me], ie = ok ? ls.item_begin[me + 1] : ib;
@@ -1180,7 +1180,7 @@ __global__ void __launch_bounds__(NT, 512 / NT) lamb_stream_kernel(OptArgs a, La
       stream_reduce(s_base, ls.part, p1_first[pend_t], ptr[pend_t + 1] - ptr[pend_t], xch_off, ls.rdy_off,
                     rs.epoch, n, W, me, pend_t);
   }
-  rank_barrier(rs, 1);
+  edge_barrier(rs, 1);
 }
 
 int fill_args(coconet_tlist* tl, OptArgs* a, const RankSet& rs, int64_t m_off, int64_t v_off) {
@@ -1378,7 +1378,8 @@ int coconet_fused_rs_adam_ag(coconet_ctx_t c, coconet_tlist_t tl, const void* co
     TmaArgs ta;
     ta.stages = std::min(16, (200 << 10) / per_sm / sbytes);
     const size_t smem = size_t(ta.stages) * size_t(sbytes) + size_t(ta.stages) * 16 + 128;
-    CN_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    rc = ensure_smem(c, fn, smem);
+    if (rc) return rc;
     int blocks = 0;
     rc = coop_blocks(c, fn, threads, smem, tl->group, int64_t(c->sm_count) * per_sm, &blocks);
     if (rc) return rc;
@@ -1390,7 +1391,8 @@ int coconet_fused_rs_adam_ag(coconet_ctx_t c, coconet_tlist_t tl, const void* co
                                            : adam_pick<__nv_bfloat16>(hp->math, os, W);
   // split segments while the resident grid has idle warps (small lists)
   int per_sm = 0;
-  CN_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kThreads, 0));
+  rc = occupancy(c, fn, kThreads, 0, &per_sm);
+  if (rc) return rc;
   const int64_t warps = int64_t(per_sm) * c->sm_count / local_ranks(c, tl->group) * kWarps;
   const int64_t segs = std::max<int64_t>(1, max_rank_segs(tl, W, os));
   a.parts = 1;
@@ -1466,7 +1468,8 @@ int coconet_fused_rs_lamb_ag(coconet_ctx_t c, coconet_tlist_t tl, const void* co
     ta.stages = std::min(16, (200 << 10) / per_sm / sbytes);
     if (ta.stages < 2) return set_error(COCONET_ERR_UNSUPPORTED, "TMA ring does not fit");
     const size_t smem = size_t(ta.stages) * size_t(sbytes) + size_t(ta.stages) * 16 + 128;
-    CN_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    rc = ensure_smem(c, fn, smem);
+    if (rc) return rc;
     int blocks = 0;
     rc = coop_blocks(c, fn, threads, smem, tl->group, int64_t(c->sm_count) * per_sm, &blocks);
     if (rc) return rc;

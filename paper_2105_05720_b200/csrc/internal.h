@@ -41,6 +41,11 @@ struct coconet_ctx {
   uint32_t mp_arrivals[coconet::kMaxGroups] = {};
   uint32_t mp_tickets[coconet::kMaxGroups] = {};  // unit tickets handed out so far
   std::vector<coconet_group_s> groups;
+  // per-kernel launch facts queried once (the driver queries cost
+  // microseconds, more than a small collective's kernel): resident CTAs per
+  // SM by (func, threads, smem), and the dynamic smem limit already set
+  std::map<std::tuple<const void*, int, size_t>, int> occupancy;
+  std::map<const void*, int> smem_set;
 };
 
 namespace coconet {
@@ -66,6 +71,10 @@ int make_rankset(coconet_ctx* c, int group, RankSet* rs);
 int heap_offset(const coconet_ctx* c, const void* p, int64_t* off);
 
 // Blocks per rank for a cooperative launch of `func`.
+// Resident CTAs per SM of `func` (cached per context).
+int occupancy(coconet_ctx* c, const void* func, int threads, size_t smem, int* per_sm);
+// cudaFuncAttributeMaxDynamicSharedMemorySize >= smem (set once per kernel).
+int ensure_smem(coconet_ctx* c, const void* func, size_t smem);
 int coop_blocks(coconet_ctx* c, const void* func, int threads, size_t smem, int group,
                 int64_t want, int* blocks);
 

@@ -103,6 +103,7 @@ class Context:
             self._open_peers(process_group)
         self._heap_bytes = None
         self._heaps: dict[int, torch.Tensor] = {}
+        self._bases: dict[int, int] = {}
         self.groups = {0: (0, self.world)}
 
     # -- bootstrap -------------------------------------------------------------
@@ -169,7 +170,10 @@ class Context:
 
     def ptr(self, buf: SymmBuffer, rank: int | None = None) -> int:
         r = (0 if self.mode == "virtual" else self.rank) if rank is None else rank
-        return int(self.lib.coconet_symm_ptr(self.handle, r, buf.offset))
+        base = self._bases.get(r)
+        if base is None:  # heap bases are fixed for the context's lifetime
+            base = self._bases[r] = int(self.lib.coconet_symm_ptr(self.handle, r, 0) or 0)
+        return base + buf.offset if base else int(self.lib.coconet_symm_ptr(self.handle, r, buf.offset) or 0)
 
     # -- groups / sync -------------------------------------------------------------
     def group(self, first_rank: int, size: int) -> int:
@@ -180,8 +184,9 @@ class Context:
 
     @staticmethod
     def stream_ptr(stream=None) -> int:
-        s = stream if stream is not None else torch.cuda.current_stream()
-        return int(s.cuda_stream)
+        if stream is None:  # the raw handle without building a Stream object
+            return torch._C._cuda_getCurrentRawStream(torch.cuda.current_device())
+        return int(stream.cuda_stream)
 
     def check(self, stream=None):
         check(self.lib.coconet_check(self.handle, C.c_void_p(self.stream_ptr(stream))))

@@ -35,6 +35,27 @@ def timeit(fn, steps=20, warmup=3):
     return e0.elapsed_time(e1) / steps
 
 
+def devtime(fn, steps=20, warmup=3, flush_bytes=0):
+    """Device time of one call, without the host's launch gaps: each call is
+    queued behind a ~25 us device sleep, so the kernel starts the moment its
+    start event completes. flush_bytes > 0 writes that many bytes between
+    calls (outside the events) so every call starts with a cold L2."""
+    for _ in range(warmup):
+        fn()
+    scratch = torch.empty(flush_bytes // 4, dtype=torch.float32, device="cuda") if flush_bytes else None
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    torch.cuda.synchronize()
+    for e0, e1 in ev:
+        if scratch is not None:
+            scratch.zero_()
+        torch.cuda._sleep(50_000)
+        e0.record()
+        fn()
+        e1.record()
+    torch.cuda.synchronize()
+    return sum(e0.elapsed_time(e1) for e0, e1 in ev) / steps
+
+
 def c1(out):
     W, N = 4, 1 << 20
     ctx = Context(W, heap_bytes=64 << 20)
@@ -49,8 +70,16 @@ def c1(out):
     for math, name in ((_lib.MATH_EXACT, "exact"), (_lib.MATH_FAST, "fast")):
         for algo, an in ((_lib.ALGO_TWO_SHOT, "two_shot"),):
             hp = AdamHParams(1e-3, 0.9, 0.999, 1.0, 0.0, True, math, algo)
-            ms = timeit(lambda: fused_rs_adam_ag(ctx, tl, [g], [p], m, v, hp), 50)
-            out[f"c1_adam_W4_N2^20_{name}_{an}_us"] = ms * 1e3
+            f = lambda: fused_rs_adam_ag(ctx, tl, [g], [p], m, v, hp)  # noqa: E731
+            # per call from Python, back to back (host-bound at this size)
+            out[f"c1_adam_W4_N2^20_{name}_{an}_us"] = timeit(f, 50) * 1e3
+            # the kernel alone, L2 flushed before each call (512 MB write)
+            dev = devtime(f, 20, flush_bytes=512 << 20)
+            out[f"c1_adam_W4_N2^20_{name}_{an}_device_cold_us"] = dev * 1e3
+            # HBM bytes of all W ranks here: each pulls its chunk of g from W
+            # ranks and pushes p to W ranks (8N), plus m, v, p read and m, v
+            # written on its own chunk (20N/W): (8W + 20) N in total
+            out[f"c1_adam_W4_N2^20_{name}_{an}_device_cold_GBs"] = (8 * W + 20) * N / (dev * 1e-3) / 1e9
     ctx.close()
 
 
