@@ -67,7 +67,7 @@ __global__ void __launch_bounds__(kThreads) reduce_kernel(RootArgs a) {
   const RankSet& rs = a.rs;
   if (threadIdx.x < kMaxRanks) s_base[threadIdx.x] = threadIdx.x < rs.world ? rs.base[threadIdx.x] : nullptr;
   const int W = rs.world, me = rs.rank();
-  if (!rank_barrier(rs, 0)) return;
+  if (!edge_barrier(rs, 0)) return;
   const int64_t nq = a.n / VEC;
   const int64_t st = int64_t(gridDim.x) * kThreads;
   if (me == a.root) {
@@ -87,10 +87,14 @@ __global__ void __launch_bounds__(kThreads) reduce_kernel(RootArgs a) {
       else out[q] = from_f32<T>(acc[0]);
     }
   }
+  // pairwise with the root's CTA of the same index: this CTA then zeroes
+  // exactly the vectors that CTA read
   if (!rank_barrier(rs, 1)) return;
   if (me != a.root) {
     T* out = reinterpret_cast<T*>(s_base[me] + a.out_off);
-    for (int64_t i = int64_t(blockIdx.x) * kThreads + threadIdx.x; i < a.n; i += st) out[i] = from_f32<T>(0.f);
+    for (int64_t q = int64_t(blockIdx.x) * kThreads + threadIdx.x; q < nq; q += st)
+#pragma unroll
+      for (int i = 0; i < VEC; ++i) out[q * VEC + i] = from_f32<T>(0.f);
   }
 }
 
@@ -101,7 +105,7 @@ __global__ void __launch_bounds__(kThreads) bcast_kernel(RootArgs a) {
   const RankSet& rs = a.rs;
   if (threadIdx.x < kMaxRanks) s_base[threadIdx.x] = threadIdx.x < rs.world ? rs.base[threadIdx.x] : nullptr;
   const int me = rs.rank();
-  if (!rank_barrier(rs, 0)) return;
+  if (!edge_barrier(rs, 0)) return;
   const bool same = me == a.root && a.x_off == a.out_off;
   if (!same) {
     const T* src = reinterpret_cast<const T*>(s_base[a.root] + a.x_off);
@@ -117,7 +121,7 @@ __global__ void __launch_bounds__(kThreads) bcast_kernel(RootArgs a) {
       }
     }
   }
-  rank_barrier(rs, 1);  // nobody overwrites the root's x while peers still read it
+  edge_barrier(rs, 1);  // nobody overwrites the root's x while peers still read it (across processes)
 }
 
 template <typename T, int RED, int VEC>
@@ -126,7 +130,7 @@ __global__ void __launch_bounds__(kThreads) rs_kernel(AxisArgs a) {
   const RankSet& rs = a.rs;
   if (threadIdx.x < kMaxRanks) s_base[threadIdx.x] = threadIdx.x < rs.world ? rs.base[threadIdx.x] : nullptr;
   const int W = rs.world, me = rs.rank();
-  if (!rank_barrier(rs, 0)) return;
+  if (!edge_barrier(rs, 0)) return;
   T* out = reinterpret_cast<T*>(s_base[me] + a.out_off);
   const int64_t nq = a.n_local / VEC;
   for (int64_t q = int64_t(blockIdx.x) * kThreads + threadIdx.x; q < nq; q += int64_t(gridDim.x) * kThreads) {
@@ -148,7 +152,7 @@ __global__ void __launch_bounds__(kThreads) rs_kernel(AxisArgs a) {
     if (VEC == 4) store4(out + li, acc);
     else out[li] = from_f32<T>(acc[0]);
   }
-  rank_barrier(rs, 1);
+  edge_barrier(rs, 1);
 }
 
 // AG: out_q[to_global(r, li)] = x_r[li] for every q (push). in_place: the
@@ -159,7 +163,7 @@ __global__ void __launch_bounds__(kThreads) ag_kernel(AxisArgs a) {
   const RankSet& rs = a.rs;
   if (threadIdx.x < kMaxRanks) s_base[threadIdx.x] = threadIdx.x < rs.world ? rs.base[threadIdx.x] : nullptr;
   const int W = rs.world, me = rs.rank();
-  if (!rank_barrier(rs, 0)) return;
+  if (!edge_barrier(rs, 0)) return;
   const int64_t nq = a.n_local / VEC;
   for (int64_t q = int64_t(blockIdx.x) * kThreads + threadIdx.x; q < nq; q += int64_t(gridDim.x) * kThreads) {
     const int64_t li = q * VEC;
@@ -178,7 +182,7 @@ __global__ void __launch_bounds__(kThreads) ag_kernel(AxisArgs a) {
       else dst[0] = from_f32<T>(x[0]);
     }
   }
-  rank_barrier(rs, 1);
+  edge_barrier(rs, 1);
 }
 
 template <typename T, int VEC>

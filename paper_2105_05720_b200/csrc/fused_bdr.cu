@@ -94,7 +94,7 @@ __global__ void __launch_bounds__(kThreads) rs_bdr_ag_kernel(BdrArgs a, BdrK k) 
   const RankSet& rs = a.rs;
   if (threadIdx.x < kMaxRanks) s_base[threadIdx.x] = threadIdx.x < rs.world ? rs.base[threadIdx.x] : nullptr;
   const int W = rs.world, me = rs.rank();
-  if (!rank_barrier(rs, 0)) return;
+  if (!edge_barrier(rs, 0)) return;
   const int64_t vpr = a.per / V;  // vectors per row block
   const int64_t nv = a.rows * vpr;
   const T* bb = reinterpret_cast<const T*>(s_base[me] + a.b_off);
@@ -128,7 +128,7 @@ __global__ void __launch_bounds__(kThreads) rs_bdr_ag_kernel(BdrArgs a, BdrK k) 
       store16(reinterpret_cast<T*>(s_base[j] + a.out_off) + gi, o);
     }
   }
-  rank_barrier(rs, 1);
+  edge_barrier(rs, 1);
 }
 
 // PP: union ranks [0, S) form the source stage, [S, 2S) the destination.
@@ -141,7 +141,7 @@ __global__ void __launch_bounds__(kThreads) rs_send_ag_kernel(BdrArgs a, BdrK k)
   const RankSet& rs = a.rs;
   if (threadIdx.x < kMaxRanks) s_base[threadIdx.x] = threadIdx.x < rs.world ? rs.base[threadIdx.x] : nullptr;
   const int U = rs.world, me = rs.rank(), S = a.src_ranks;
-  if (!rank_barrier(rs, 0)) return;
+  if (!edge_barrier(rs, 0)) return;
   if (me < S) {
     const int64_t per = a.n / S;
     const int64_t nq = per >> 2;
@@ -176,7 +176,7 @@ __global__ void __launch_bounds__(kThreads) rs_send_ag_kernel(BdrArgs a, BdrK k)
       }
     }
   }
-  rank_barrier(rs, 1);
+  edge_barrier(rs, 1);
 }
 
 BdrK make_k(const coconet_bdr_params* hp) {

@@ -37,6 +37,29 @@ def test_reduce_rank_order(W, n, red):
     ctx.close()
 
 
+@pytest.mark.parametrize("W", [2, 4, 8])
+def test_reduce_in_place_many_ctas(W):
+    """x aliases out over a multi-CTA grid: a non-root CTA zeroes only the
+    vectors the root's CTA of the same index has finished reading."""
+    n = 1 << 22
+    rng = np.random.default_rng(W)
+    xs = rng.uniform(-1, 1, (W, n)).astype(np.float32)
+    ctx = new_ctx(W)
+    x = ctx.alloc([n])
+    for r in range(W):
+        ctx.view(x, r).copy_(torch.from_numpy(xs[r]))
+    root = 1
+    reduce(ctx, x, x, root=root)
+    ctx.check()
+    acc = xs[0].copy()
+    for r in range(1, W):
+        acc = (acc + xs[r]).astype(np.float32)
+    for r in range(W):
+        got = ctx.view(x, r).cpu().numpy()
+        assert np.array_equal(got, acc if r == root else np.zeros(n, np.float32)), r
+    ctx.close()
+
+
 def test_reduce_in_place_and_bf16():
     W, n = 4, 4096
     ctx = new_ctx(W)
