@@ -90,3 +90,24 @@ def test_run_cuda_tensor_files_match_sim(tmp_path):
         assert j["digest"] == rec["engine_sched_digest"], backend
         dumps[backend] = {x.name: x.read_bytes() for x in out.iterdir()}
     assert dumps["cuda"] == dumps["sim"]
+
+
+@pytest.mark.parametrize("case", ["adam_W4_N4096", "mp_W4_B2_S8_H64", "pp_W4_N1024"])
+@pytest.mark.parametrize("math", ["exact", "fast"])
+def test_run_cuda_is_deterministic(tmp_path, case, math):
+    """acceptance.cpp:380-416 runs the CLI twice and byte-compares the JSON.
+    On the GPU everything but the measured device time must repeat exactly,
+    in FAST math too (fixed reduction order, no atomics in the data path)."""
+    need_cli()
+    from tests.dp_util import golden
+    try:
+        golden(case)
+    except KeyError:
+        pytest.skip(f"no fixture {case}")
+    f, rec = program_file(tmp_path, case, "sched_program")
+    outs = []
+    for _ in range(2):
+        j = json.loads(cli("run", f, *dims_args(rec), "--math", math, check_rc=0).stdout)
+        j.pop("device_ms")
+        outs.append(json.dumps(j, sort_keys=True))
+    assert outs[0] == outs[1]
