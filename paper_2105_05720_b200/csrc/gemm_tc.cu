@@ -760,9 +760,11 @@ int launch_tc_t(coconet_ctx* c, TcPlan* p, uint32_t in_fmt, const OvArgs* ov, cu
   OvArgs none{};
   const OvArgs& o = ov ? *ov : none;
   if constexpr (!FUSED) {
-    // COCONET_GEMM_MC: 0 = no clusters, a = pairs share A, b = pairs share B
+    // COCONET_GEMM_MC: 0 = no clusters, a = pairs share A (default), b = pairs
+    // share B (less L2 -> SM traffic, but no faster end to end at C3's shape:
+    // profiles/r01_gemm_diag.json)
     const char* e = getenv("COCONET_GEMM_MC");
-    const char want = e ? e[0] : 'b';
+    const char want = e ? e[0] : 'a';
     const bool mc_b = (want == 'b') && p->g.tiles_m % 2 == 0 && (BN / 64) % 2 == 0;
     const bool mc_a = !mc_b && want != '0' && p->g.tiles_n % 2 == 0;
     if (mc_a || mc_b) {  // 2-CTA clusters sharing an operand by multicast
