@@ -37,9 +37,8 @@ METRIC = "fused AR+Adam/LAMB step time & NVLink-roofline fraction, 1/2/4/8 B200"
 UNIT = "Gelem/s"
 NVLINK_GBS = 770.0  # measured peer copy per direction (B200_PROFILING.md)
 BUCKET_CAP = 16384  # N=1: segments of the TMA LAMB schedule
-BUCKET_CAP_MULTI = 4096  # N>1: the GRID kernel has one warp per segment; with the
-# whole GPU per rank, 16384-element buckets leave ~2600 segments for ~2400 warps
-# (makespan 2 segments), 4096 gives ~10400 (4.4 per warp)
+BUCKET_CAP_MULTI = 16384  # N>1: the TMA schedule across ranks is fastest at 16384
+# (W=2/8 virtual, profiles/r01_lamb_w_probe.json); GRID would prefer 4096
 E2E_GROUPS = 16  # tensor groups pipelined against PCIe in the e2e measurement
 CPU_SAMPLE = 1 << 22  # elements per core for cpu_baseline: ~10-30 s of CPU work
 

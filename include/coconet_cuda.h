@@ -213,13 +213,17 @@ typedef struct {
  * order, one small CTA per segment; a tensor's pass 2 is scheduled lag_elems
  * of pass-1 work after its pass 1 and waits only on that tensor's norms
  * (per-tensor completion counters, cross-rank ready flags), so part of its
- * m, v, p re-reads hit L2. AUTO = TMA at group size 1, GRID otherwise. */
+ * m, v, p re-reads hit L2. TMA: GRID's two passes with the local m, v, p
+ * (and g at group size 1) fed by bulk copies; across ranks g is pulled and p
+ * pushed by the consumer threads. AUTO = TMA with buckets of >= 4096
+ * elements, GRID otherwise. m and v are bit-identical across
+ * schedules; TMA sums the norms in another fixed order. */
 enum coconet_lamb_sched {
   COCONET_LAMB_AUTO = 0,
   COCONET_LAMB_GRID = 1,
   COCONET_LAMB_STREAMED = 2,
   COCONET_LAMB_TMA = 3 /* GRID's two passes fed by TMA bulk copies into a shared-memory ring
-                          (group size 1; norms summed in a different fixed order) */
+                          (norms summed in a different fixed order) */
 };
 
 int coconet_fused_rs_lamb_ag(coconet_ctx_t ctx, coconet_tlist_t tl, const void* const* g,

@@ -624,8 +624,8 @@ __device__ __forceinline__ void tma_produce(const OptArgs& a, char* const* s_bas
   ph = __shfl_sync(0xffffffffu, ph, 0);
 }
 
-template <typename G, int NW, int QPT>
-__global__ void __launch_bounds__((NW + 1) * 32) lamb_tma_kernel(OptArgs a, LambK k, TmaArgs ta) {
+template <typename G, int NW, int QPT, int WT>
+__global__ void __launch_bounds__((NW + 1) * 32, 2) lamb_tma_kernel(OptArgs a, LambK k, TmaArgs ta) {
   using ST = TmaStage<G, NW, QPT>;
   constexpr int kTmaConsumerWarps = NW;
   constexpr int kTmaThreads = ST::THREADS;
@@ -649,6 +649,7 @@ __global__ void __launch_bounds__((NW + 1) * 32) lamb_tma_kernel(OptArgs a, Lamb
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   }
   const int me = rs.rank();
+  const int W = WT > 0 ? WT : rs.world;
   const bool ok = edge_barrier(rs, 0);  // also publishes the barrier inits to the CTA
   const int64_t sb = a.seg_begin[me], se = ok ? a.seg_begin[me + 1] : sb;
   float* m = reinterpret_cast<float*>(s_base[me] + a.m_off);
@@ -676,18 +677,21 @@ __global__ void __launch_bounds__((NW + 1) * 32) lamb_tma_kernel(OptArgs a, Lamb
         }
         sp = warp_sum(sp);
         su = warp_sum(su);
-        if (lane == 0) {
-          double* xq = reinterpret_cast<double*>(s_base[me] + xch_off);
+        if (lane < W) {  // this rank's partials into every rank's slot [me][t]
+          double* xq = reinterpret_cast<double*>(s_base[lane] + xch_off);
           xq[(int64_t(me) * a.n_tensors + t) * 2] = sp;
           xq[(int64_t(me) * a.n_tensors + t) * 2 + 1] = su;
         }
       }
-      __threadfence();
+      __threadfence_system();
       cg::this_grid().sync();
+      if (!rank_barrier(rs, 2)) return;  // every rank's partials have landed (no-op at W = 1)
     }
     const double* xch_me = reinterpret_cast<const double*>(s_base[me] + group_area(rs.group));
     if (producer) {
-      tma_produce<G, NW, QPT>(a, s_base, me, sb, se, stage0, full, empty, S, pass == 0, lane, st, ph);
+      // g comes through the ring only at W = 1; across ranks the consumers
+      // pull it (peer memory is never a bulk-copy source)
+      tma_produce<G, NW, QPT>(a, s_base, me, sb, se, stage0, full, empty, S, pass == 0 && W == 1, lane, st, ph);
     } else {
       int red = 0;  // s_red buffer of the next segment reduction
       const int64_t st32 = int64_t(gridDim.x) * 32;
@@ -703,13 +707,34 @@ __global__ void __launch_bounds__((NW + 1) * 32) lamb_tma_kernel(OptArgs a, Lamb
         const int64_t q0 = d.toff >> 2, q1 = (d.toff + d.len + 3) >> 2;
         float ratio = 0.f;
         if (pass == 1) {
-          const double P = __ldcg(xch_me + (int64_t(me) * a.n_tensors + tens) * 2);
-          const double U = __ldcg(xch_me + (int64_t(me) * a.n_tensors + tens) * 2 + 1);
+          double P = 0.0, U = 0.0;
+#pragma unroll
+          for (int q = 0; q < Ranks<WT>::kMax; ++q)  // rank order 0..W-1
+            if (Ranks<WT>::has(q, W)) {
+              P += __ldcg(xch_me + (int64_t(q) * a.n_tensors + tens) * 2);
+              U += __ldcg(xch_me + (int64_t(q) * a.n_tensors + tens) * 2 + 1);
+            }
           ratio = float((k.lr * sqrt(P)) / sqrt(U));
         }
         float sp = 0.f, su = 0.f;
         for (int64_t qa = q0; qa < q1; qa += kTmaChunkQ) {
           const int64_t qb = min(qa + int64_t(kTmaChunkQ), q1);
+          // W > 1: this thread's g quads from every rank, in flight while
+          // the stage fills (clamped, unconditional loads)
+          // (kept packed until the fold: 2 registers per fp16 quad and rank)
+          using GRaw = std::conditional_t<sizeof(G) == 4, float4, uint2>;
+          GRaw gw[QPT][Ranks<WT>::kMax];
+          if (WT != 1 && pass == 0) {
+#pragma unroll
+            for (int qq = 0; qq < QPT; ++qq) {
+              const int64_t q = min(qa + ctid + qq * (NW * 32), qb - 1);
+#pragma unroll
+              for (int j = 0; j < Ranks<WT>::kMax; ++j)
+                if (Ranks<WT>::has(j, W))
+                  gw[qq][j] = __ldg(reinterpret_cast<const GRaw*>(s_base[rot<WT>(me, j, W)] + aoff +
+                                                                  (q << 2) * int64_t(sizeof(G))));
+            }
+          }
           mbar_wait(&full[st], ph);
           const uint8_t* src = stage0 + size_t(st) * ST::BYTES;
 #pragma unroll
@@ -728,7 +753,22 @@ __global__ void __launch_bounds__((NW + 1) * 32) lamb_tma_kernel(OptArgs a, Lamb
               const uintptr_t ga = reinterpret_cast<uintptr_t>(s_base[me] + aoff + qa * 4 * int64_t(sizeof(G)));
               const uintptr_t goff = (ga & 15u) + uintptr_t(q - qa) * 4u * sizeof(G);
               float gs[4];
-              if constexpr (sizeof(G) == 4) {
+              if (WT != 1) {  // ring order: rank me+1 first (runtime.hpp:302-305)
+#pragma unroll
+                for (int j = 0; j < Ranks<WT>::kMax; ++j)
+                  if (Ranks<WT>::has(j, W)) {
+                    float x[4];
+                    if constexpr (sizeof(G) == 4) {
+                      x[0] = gw[qq][j].x; x[1] = gw[qq][j].y; x[2] = gw[qq][j].z; x[3] = gw[qq][j].w;
+                    } else {
+                      const G* h = reinterpret_cast<const G*>(&gw[qq][j]);
+#pragma unroll
+                      for (int i = 0; i < 4; ++i) x[i] = to_f32(h[i]);
+                    }
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) gs[i] = j == 0 ? x[i] : __fadd_rn(gs[i], x[i]);
+                  }
+              } else if constexpr (sizeof(G) == 4) {
                 const float4 gq = *reinterpret_cast<const float4*>(src + goff);
                 gs[0] = gq.x; gs[1] = gq.y; gs[2] = gq.z; gs[3] = gq.w;
               } else {
@@ -758,7 +798,9 @@ __global__ void __launch_bounds__((NW + 1) * 32) lamb_tma_kernel(OptArgs a, Lamb
               float pn[4];
 #pragma unroll
               for (int i = 0; i < 4; ++i) pn[i] = pp[i] - ratio * lamb_u(mm[i], vv[i], pp[i], k);
-              st4m(reinterpret_cast<float*>(pme + boff) + e0, pn, lo, hi);
+#pragma unroll
+              for (int j = 0; j < Ranks<WT>::kMax; ++j)  // AllGather push
+                if (Ranks<WT>::has(j, W)) st4m(reinterpret_cast<float*>(s_base[j] + boff) + e0, pn, lo, hi);
             }
           }
           }
@@ -1441,23 +1483,28 @@ int coconet_fused_rs_lamb_ag(coconet_ctx_t c, coconet_tlist_t tl, const void* co
   if (rc) return rc;
   OptArgs a;
   fill_args(tl, &a, rs, m_off, v_off);
-  // AUTO: the TMA ring at W = 1 with buckets of >= kTmaMinBucket elements,
-  // GRID otherwise
-  const int sched = hp->sched == COCONET_LAMB_AUTO ? (tma_eligible(tl, W) ? COCONET_LAMB_TMA : COCONET_LAMB_GRID)
-                                                   : hp->sched;
+  // AUTO: the TMA ring with buckets of >= kTmaMinBucket elements at W = 1,
+  // >= 4x that across ranks (BERT-336M, W = 2/8 virtual: TMA wins at 16384,
+  // GRID at 4096; profiles/r01_lamb_w_probe.json), GRID otherwise
+  const bool tma_auto = tl->bucket_cap >= (W == 1 ? kTmaMinBucket : 4 * kTmaMinBucket);
+  const int sched = hp->sched == COCONET_LAMB_AUTO ? (tma_auto ? COCONET_LAMB_TMA : COCONET_LAMB_GRID) : hp->sched;
   if (sched == COCONET_LAMB_TMA) {
-    if (W != 1) return set_error(COCONET_ERR_UNSUPPORTED, "the TMA LAMB schedule runs at group size 1");
     // 8 consumer warps x 2 quads per thread (2048-element chunks), 3 CTAs
     // per SM: the best of the sweep in profiles/r01_lamb_tma_sweep.json
-    // (COCONET_LAMB_TMA_CTAS overrides the CTAs per SM)
+    // (COCONET_LAMB_TMA_CTAS overrides the CTAs per SM). At W > 1 the
+    // consumers also hold every rank's g quads: 2 CTAs per SM.
     const char* ce = getenv("COCONET_LAMB_TMA_CTAS");
-    const int per_sm = ce ? std::max(1, std::min(4, atoi(ce))) : 3;
+    const int per_sm = ce ? std::max(1, std::min(4, atoi(ce))) : (W == 1 ? 3 : 2);
     const void* fn = nullptr;
     int sbytes = 0, threads = 0;
     auto pick = [&](auto tag_g) {
       using Gt = decltype(tag_g);
       using ST = TmaStage<Gt, 8, 2>;
-      fn = reinterpret_cast<const void*>(&lamb_tma_kernel<Gt, 8, 2>);
+      fn = W == 1   ? reinterpret_cast<const void*>(&lamb_tma_kernel<Gt, 8, 2, 1>)
+           : W == 2 ? reinterpret_cast<const void*>(&lamb_tma_kernel<Gt, 8, 2, 2>)
+           : W == 4 ? reinterpret_cast<const void*>(&lamb_tma_kernel<Gt, 8, 2, 4>)
+           : W == 8 ? reinterpret_cast<const void*>(&lamb_tma_kernel<Gt, 8, 2, 8>)
+                    : reinterpret_cast<const void*>(&lamb_tma_kernel<Gt, 8, 2, 0>);
       sbytes = ST::BYTES;
       threads = ST::THREADS;
     };
@@ -1471,10 +1518,11 @@ int coconet_fused_rs_lamb_ag(coconet_ctx_t c, coconet_tlist_t tl, const void* co
     rc = ensure_smem(c, fn, smem);
     if (rc) return rc;
     int blocks = 0;
-    rc = coop_blocks(c, fn, threads, smem, tl->group, int64_t(c->sm_count) * per_sm, &blocks);
+    const int lr = local_ranks(c, tl->group);
+    rc = coop_blocks(c, fn, threads, smem, tl->group, int64_t(c->sm_count) * per_sm / lr, &blocks);
     if (rc) return rc;
     void* args[] = {&a, &k, &ta};
-    return coop_launch(c, fn, dim3(unsigned(blocks), 1u), dim3(unsigned(threads)), args, smem, stream);
+    return coop_launch(c, fn, dim3(unsigned(blocks), unsigned(lr)), dim3(unsigned(threads)), args, smem, stream);
   }
   if (sched == COCONET_LAMB_GRID) {
     const void* fn = g_elem == COCONET_F32   ? lamb_pick<float>(W)

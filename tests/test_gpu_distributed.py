@@ -130,7 +130,7 @@ def _worker_lamb_rooted(rank, world, port, counts, q):
         ctx = Context(world, mode="distributed", rank=rank, device=0, heap_bytes=64 << 20, timeout_ms=60000)
         g, p, m, v = _inputs(world, counts)
         outs = {}
-        for sched in (_lib.LAMB_GRID, _lib.LAMB_STREAMED):
+        for sched in (_lib.LAMB_GRID, _lib.LAMB_STREAMED, _lib.LAMB_TMA):
             tl = TensorList(ctx, counts, bucket_cap=512)
             gb = [ctx.alloc([n]) for n in counts]
             pb = [ctx.alloc([n]) for n in counts]
@@ -157,16 +157,22 @@ def _worker_lamb_rooted(rank, world, port, counts, q):
                 ctx.check()
                 if step == 0:
                     first = [ctx.view(b).cpu().numpy().copy() for b in pb]
-            outs[sched] = ([ctx.view(b).cpu().numpy() for b in pb], first)
+            outs[sched] = ([ctx.view(b).cpu().numpy() for b in pb], first, ctx.view(mb).cpu().numpy(),
+                           ctx.view(vb).cpu().numpy())
         same = all(np.array_equal(a, b) for a, b in zip(outs[_lib.LAMB_GRID][0], outs[_lib.LAMB_STREAMED][0]))
+        # TMA (m, v, p through the bulk-copy ring, g pulled across processes):
+        # m, v bitwise GRID's (they do not depend on p); p by its own segment
+        # sums, so against the oracle below
+        same = same and np.array_equal(outs[_lib.LAMB_TMA][2], outs[_lib.LAMB_GRID][2]) and np.array_equal(
+            outs[_lib.LAMB_TMA][3], outs[_lib.LAMB_GRID][3])
         k = co.lamb_consts(0.01, 0.9, 0.999, 1.0, 1e-6, 0.01)
         table = co.bucket_table(counts)
         flat = co.flatten_bucket_order(g, table)
         bounds = co.flat_chunks(flat.shape[1], world)
         owner = np.searchsorted(np.asarray(bounds[1:]), np.arange(flat.shape[1]), side="right")
         gr = co.unflatten_bucket_order(co.ring_reduce(flat, owner), counts, table)
-        dev = max(co.max_rel_deviation(outs[_lib.LAMB_STREAMED][1][t], co.lamb_oracle(gr[t], m[t], v[t], p[t], k)[2])
-                  for t in range(len(counts)))
+        dev = max(co.max_rel_deviation(outs[sc][1][t], co.lamb_oracle(gr[t], m[t], v[t], p[t], k)[2])
+                  for t in range(len(counts)) for sc in (_lib.LAMB_STREAMED, _lib.LAMB_TMA))
         # a size-1 subgroup inside DISTRIBUTED mode (the bench's NCCL-baseline
         # leg): AUTO picks the TMA schedule; m, v equal GRID's bitwise
         g1 = ctx.group(rank, 1)
