@@ -114,6 +114,37 @@ __device__ __forceinline__ void ring_fold4(const float x[][4], int W, float acc[
     }
 }
 
+// The same pull and fold with the quads kept packed until the fold (2
+// registers per fp16 quad and rank instead of 4): the TMA kernels hold every
+// rank's quads in flight while their stage fills.
+template <typename G>
+using GRaw = std::conditional_t<sizeof(G) == 4, float4, uint2>;
+
+template <typename G, int WT>
+__device__ __forceinline__ void ring_load_raw(char* const* base, int64_t off, int owner, int W, GRaw<G> x[]) {
+#pragma unroll
+  for (int j = 0; j < Ranks<WT>::kMax; ++j)
+    if (Ranks<WT>::has(j, W)) x[j] = __ldg(reinterpret_cast<const GRaw<G>*>(base[rot<WT>(owner, j, W)] + off));
+}
+
+template <typename G, int WT>
+__device__ __forceinline__ void ring_fold_raw(const GRaw<G> x[], int W, float acc[4]) {
+#pragma unroll
+  for (int j = 0; j < Ranks<WT>::kMax; ++j)
+    if (Ranks<WT>::has(j, W)) {
+      float y[4];
+      if constexpr (sizeof(G) == 4) {
+        y[0] = x[j].x; y[1] = x[j].y; y[2] = x[j].z; y[3] = x[j].w;
+      } else {
+        const G* h = reinterpret_cast<const G*>(&x[j]);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) y[i] = to_f32(h[i]);
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i) acc[i] = j == 0 ? y[i] : __fadd_rn(acc[i], y[i]);  // as ring_fold4
+    }
+}
+
 __device__ __forceinline__ void ld4(const float* p, float o[4]) {
   float4 x = *reinterpret_cast<const float4*>(p);
   o[0] = x.x; o[1] = x.y; o[2] = x.z; o[3] = x.w;
@@ -721,18 +752,12 @@ __global__ void __launch_bounds__((NW + 1) * 32, 2) lamb_tma_kernel(OptArgs a, L
           const int64_t qb = min(qa + int64_t(kTmaChunkQ), q1);
           // W > 1: this thread's g quads from every rank, in flight while
           // the stage fills (clamped, unconditional loads)
-          // (kept packed until the fold: 2 registers per fp16 quad and rank)
-          using GRaw = std::conditional_t<sizeof(G) == 4, float4, uint2>;
-          GRaw gw[QPT][Ranks<WT>::kMax];
+          GRaw<G> gw[QPT][Ranks<WT>::kMax];
           if (WT != 1 && pass == 0) {
 #pragma unroll
             for (int qq = 0; qq < QPT; ++qq) {
               const int64_t q = min(qa + ctid + qq * (NW * 32), qb - 1);
-#pragma unroll
-              for (int j = 0; j < Ranks<WT>::kMax; ++j)
-                if (Ranks<WT>::has(j, W))
-                  gw[qq][j] = __ldg(reinterpret_cast<const GRaw*>(s_base[rot<WT>(me, j, W)] + aoff +
-                                                                  (q << 2) * int64_t(sizeof(G))));
+              ring_load_raw<G, WT>(s_base, aoff + (q << 2) * int64_t(sizeof(G)), me, W, gw[qq]);
             }
           }
           mbar_wait(&full[st], ph);
@@ -754,20 +779,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, 2) lamb_tma_kernel(OptArgs a, L
               const uintptr_t goff = (ga & 15u) + uintptr_t(q - qa) * 4u * sizeof(G);
               float gs[4];
               if (WT != 1) {  // ring order: rank me+1 first (runtime.hpp:302-305)
-#pragma unroll
-                for (int j = 0; j < Ranks<WT>::kMax; ++j)
-                  if (Ranks<WT>::has(j, W)) {
-                    float x[4];
-                    if constexpr (sizeof(G) == 4) {
-                      x[0] = gw[qq][j].x; x[1] = gw[qq][j].y; x[2] = gw[qq][j].z; x[3] = gw[qq][j].w;
-                    } else {
-                      const G* h = reinterpret_cast<const G*>(&gw[qq][j]);
-#pragma unroll
-                      for (int i = 0; i < 4; ++i) x[i] = to_f32(h[i]);
-                    }
-#pragma unroll
-                    for (int i = 0; i < 4; ++i) gs[i] = j == 0 ? x[i] : __fadd_rn(gs[i], x[i]);
-                  }
+                ring_fold_raw<G, WT>(gw[qq], W, gs);
               } else if constexpr (sizeof(G) == 4) {
                 const float4 gq = *reinterpret_cast<const float4*>(src + goff);
                 gs[0] = gq.x; gs[1] = gq.y; gs[2] = gq.z; gs[3] = gq.w;
@@ -841,8 +853,8 @@ __global__ void __launch_bounds__((NW + 1) * 32, 2) lamb_tma_kernel(OptArgs a, L
 // ---- Adam, TMA schedule (W = 1): one pass, the producer of lamb_tma_kernel
 // streaming g, m, v, p into the shared-memory ring and NW consumer warps
 // applying adam_elem (EXACT or FAST) and writing m, v, p.
-template <typename G, int NW, int QPT, int MATH>
-__global__ void __launch_bounds__((NW + 1) * 32) adam_tma_kernel(OptArgs a, AdamK k, TmaArgs ta) {
+template <typename G, int NW, int QPT, int MATH, int WT>
+__global__ void __launch_bounds__((NW + 1) * 32, 2) adam_tma_kernel(OptArgs a, AdamK k, TmaArgs ta) {
   using ST = TmaStage<G, NW, QPT>;
   extern __shared__ __align__(128) uint8_t smem_raw[];
   __shared__ char* s_base[kMaxRanks];
@@ -862,6 +874,7 @@ __global__ void __launch_bounds__((NW + 1) * 32) adam_tma_kernel(OptArgs a, Adam
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   }
   const int me = rs.rank();
+  const int W = WT > 0 ? WT : rs.world;
   const bool ok = edge_barrier(rs, 0);
   const int64_t sb = a.seg_begin[me], se = ok ? a.seg_begin[me + 1] : sb;
   float* m = reinterpret_cast<float*>(s_base[me] + a.m_off);
@@ -869,7 +882,8 @@ __global__ void __launch_bounds__((NW + 1) * 32) adam_tma_kernel(OptArgs a, Adam
   char* pme = s_base[me];
   uint32_t st = 0, ph = 0;
   if (warp == NW) {
-    tma_produce<G, NW, QPT>(a, s_base, me, sb, se, stage0, full, empty, S, true, lane, st, ph);
+    // across ranks g is pulled by the consumers (never a bulk copy from peer memory)
+    tma_produce<G, NW, QPT>(a, s_base, me, sb, se, stage0, full, empty, S, W == 1, lane, st, ph);
   } else {
     const int ctid = threadIdx.x;
     const int64_t st32 = int64_t(gridDim.x) * 32;
@@ -882,6 +896,14 @@ __global__ void __launch_bounds__((NW + 1) * 32) adam_tma_kernel(OptArgs a, Adam
         const int64_t q0 = d.toff >> 2, q1 = (d.toff + d.len + 3) >> 2;
         for (int64_t qa = q0; qa < q1; qa += ST::CHUNK_Q) {
           const int64_t qb = min(qa + int64_t(ST::CHUNK_Q), q1);
+          GRaw<G> gw[QPT][Ranks<WT>::kMax];  // W > 1: every rank's quads, in flight while the stage fills
+          if (WT != 1) {
+#pragma unroll
+            for (int qq = 0; qq < QPT; ++qq) {
+              const int64_t q = min(qa + ctid + qq * (NW * 32), qb - 1);
+              ring_load_raw<G, WT>(s_base, d.aoff + (q << 2) * int64_t(sizeof(G)), me, W, gw[qq]);
+            }
+          }
           mbar_wait(&full[st], ph);
           const uint8_t* src = stage0 + size_t(st) * ST::BYTES;
           const uintptr_t ga = reinterpret_cast<uintptr_t>(pme + d.aoff + qa * 4 * int64_t(sizeof(G)));
@@ -899,7 +921,9 @@ __global__ void __launch_bounds__((NW + 1) * 32) adam_tma_kernel(OptArgs a, Adam
               float mm[4] = {mq.x, mq.y, mq.z, mq.w}, vv[4] = {vq.x, vq.y, vq.z, vq.w}, pp[4] = {pq.x, pq.y, pq.z, pq.w};
               const uintptr_t goff = (ga & 15u) + uintptr_t(q - qa) * 4u * sizeof(G);
               float gs[4];
-              if constexpr (sizeof(G) == 4) {
+              if (WT != 1) {
+                ring_fold_raw<G, WT>(gw[qq], W, gs);
+              } else if constexpr (sizeof(G) == 4) {
                 const float4 gq = *reinterpret_cast<const float4*>(src + goff);
                 gs[0] = gq.x; gs[1] = gq.y; gs[2] = gq.z; gs[3] = gq.w;
               } else {
@@ -912,7 +936,9 @@ __global__ void __launch_bounds__((NW + 1) * 32) adam_tma_kernel(OptArgs a, Adam
               for (int i = 0; i < 4; ++i) adam_elem<MATH>(gs[i], mm[i], vv[i], pp[i], k);
               st4m(m + si, mm, lo, hi);
               st4m(v + si, vv, lo, hi);
-              st4m(reinterpret_cast<float*>(pme + d.boff) + e0, pp, lo, hi);
+#pragma unroll
+              for (int jr = 0; jr < Ranks<WT>::kMax; ++jr)  // AllGather push
+                if (Ranks<WT>::has(jr, W)) st4m(reinterpret_cast<float*>(s_base[jr] + d.boff) + e0, pp, lo, hi);
             }
           }
           __syncwarp();
@@ -1348,7 +1374,6 @@ constexpr int64_t kDefaultLag = int64_t(1) << 21;
 // 2.4 ms), from 4096 up it wins (LAMB 2.06 vs 2.26 ms, Adam EXACT 2.0 vs
 // 2.5 ms at 16384). Group size 1 only (peer bulk copies untested).
 constexpr int64_t kTmaMinBucket = 4096;
-bool tma_eligible(const coconet_tlist* tl, int W) { return W == 1 && tl->bucket_cap >= kTmaMinBucket; }
 
 int check_state(coconet_ctx* c, const void* ptr, int64_t* off) {
   int rc = heap_offset(c, ptr, off);
@@ -1399,34 +1424,45 @@ int coconet_fused_rs_adam_ag(coconet_ctx_t c, coconet_tlist_t tl, const void* co
   if (rc) return rc;
   OptArgs a;
   fill_args(tl, &a, rs, m_off, v_off);
-  // W = 1 (two-shot tables) with large buckets: the TMA ring
-  // (COCONET_ADAM_TMA=0 keeps the LDG kernel)
+  // two-shot tables with large buckets: the TMA ring (local m, v, p and, at
+  // W = 1, g; across ranks the consumers pull g and push p). COCONET_ADAM_TMA:
+  // 0 keeps the LDG kernel, 1 forces the ring whatever the bucket size.
   const char* te = getenv("COCONET_ADAM_TMA");
-  if (!os && tma_eligible(tl, W) && !(te && te[0] == '0')) {
+  const bool tma = te ? te[0] == '1' : tl->bucket_cap >= (W == 1 ? kTmaMinBucket : 4 * kTmaMinBucket);
+  if (!os && tma) {
     const void* fn = nullptr;
     int sbytes = 0, threads = 0;
     auto pick = [&](auto tag_g) {
       using Gt = decltype(tag_g);
       using ST = TmaStage<Gt, 8, 2>;
-      fn = hp->math == COCONET_MATH_EXACT ? reinterpret_cast<const void*>(&adam_tma_kernel<Gt, 8, 2, COCONET_MATH_EXACT>)
-                                          : reinterpret_cast<const void*>(&adam_tma_kernel<Gt, 8, 2, COCONET_MATH_FAST>);
+      auto by_w = [&](auto math_tag) -> const void* {
+        constexpr int M = decltype(math_tag)::value;
+        return W == 1   ? reinterpret_cast<const void*>(&adam_tma_kernel<Gt, 8, 2, M, 1>)
+               : W == 2 ? reinterpret_cast<const void*>(&adam_tma_kernel<Gt, 8, 2, M, 2>)
+               : W == 4 ? reinterpret_cast<const void*>(&adam_tma_kernel<Gt, 8, 2, M, 4>)
+               : W == 8 ? reinterpret_cast<const void*>(&adam_tma_kernel<Gt, 8, 2, M, 8>)
+                        : reinterpret_cast<const void*>(&adam_tma_kernel<Gt, 8, 2, M, 0>);
+      };
+      fn = hp->math == COCONET_MATH_EXACT ? by_w(std::integral_constant<int, COCONET_MATH_EXACT>{})
+                                          : by_w(std::integral_constant<int, COCONET_MATH_FAST>{});
       sbytes = ST::BYTES;
       threads = ST::THREADS;
     };
     if (g_elem == COCONET_F32) pick(float{});
     else if (g_elem == COCONET_F16) pick(__half{});
     else pick(__nv_bfloat16{});
-    const int per_sm = 3;
+    const int per_sm = W == 1 ? 3 : 2;
     TmaArgs ta;
     ta.stages = std::min(16, (200 << 10) / per_sm / sbytes);
     const size_t smem = size_t(ta.stages) * size_t(sbytes) + size_t(ta.stages) * 16 + 128;
     rc = ensure_smem(c, fn, smem);
     if (rc) return rc;
+    const int lr = local_ranks(c, tl->group);
     int blocks = 0;
-    rc = coop_blocks(c, fn, threads, smem, tl->group, int64_t(c->sm_count) * per_sm, &blocks);
+    rc = coop_blocks(c, fn, threads, smem, tl->group, int64_t(c->sm_count) * per_sm / lr, &blocks);
     if (rc) return rc;
     void* args[] = {&a, &k, &ta};
-    return coop_launch(c, fn, dim3(unsigned(blocks), 1u), dim3(unsigned(threads)), args, smem, stream);
+    return coop_launch(c, fn, dim3(unsigned(blocks), unsigned(lr)), dim3(unsigned(threads)), args, smem, stream);
   }
   const void* fn = g_elem == COCONET_F32   ? adam_pick<float>(hp->math, os, W)
                    : g_elem == COCONET_F16 ? adam_pick<__half>(hp->math, os, W)

@@ -66,6 +66,24 @@ def _worker(rank, world, port, counts, q):
         for _ in range(2):  # twice: epochs advance consistently across processes
             fused_rs_adam_ag(ctx, tl, gb, pb, mb, vb, hp)
             ctx.check()
+        # the same two steps through the TMA ring (g pulled from the other
+        # processes by the consumers, p pushed into them)
+        pb_t = [ctx.alloc([n]) for n in counts]
+        mb_t, vb_t = ctx.alloc([tl.shard_elems]), ctx.alloc([tl.shard_elems])
+        for t in range(len(counts)):
+            ctx.view(pb_t[t]).copy_(torch.from_numpy(p[t]))
+        ctx.view(mb_t).copy_(torch.from_numpy(ms))
+        ctx.view(vb_t).copy_(torch.from_numpy(vs))
+        torch.cuda.synchronize()
+        dist.barrier()
+        os.environ["COCONET_ADAM_TMA"] = "1"
+        try:
+            for _ in range(2):
+                fused_rs_adam_ag(ctx, tl, gb, pb_t, mb_t, vb_t, hp)
+                ctx.check()
+        finally:
+            os.environ.pop("COCONET_ADAM_TMA")
+        got_p_tma = [ctx.view(b).cpu().numpy() for b in pb_t]
         # AllReduce of the (original) gradients, out of place
         ob = [ctx.alloc([n]) for n in counts]
         for t in range(len(counts)):
@@ -85,7 +103,7 @@ def _worker(rank, world, port, counts, q):
         bounds = co.flat_chunks(flat.shape[1], world)
         owner = np.searchsorted(np.asarray(bounds[1:]), np.arange(flat.shape[1]), side="right")
         ar = co.unflatten_bucket_order(co.ring_reduce(flat, owner), counts, table)
-        ok_p = all(np.array_equal(got_p[t], p2[t]) for t in range(len(counts)))
+        ok_p = all(np.array_equal(got_p[t], p2[t]) and np.array_equal(got_p_tma[t], p2[t]) for t in range(len(counts)))
         ok_ar = all(np.array_equal(got_ar[t], ar[t]) for t in range(len(counts)))
         dist.barrier()
         ctx.close()
