@@ -1,5 +1,6 @@
 """Small instances of every kernel family for compute-sanitizer (memcheck,
-racecheck, synccheck): LAMB (GRID, TMA, STREAMED), Adam (LDG, TMA, one-shot),
+racecheck, synccheck): LAMB (GRID, TMA, STREAMED; W = 1..4), Adam (LDG, TMA
+at W = 1..3),
 tensor-list AllReduce, Reduce/Broadcast, RS/AG, the MP epilogue, the
 overlapped tcgen05 GEMM + all-reduce, the plain GEMM, and the PP send.
 Usage: compute-sanitizer --tool TOOL python tools/sanitize_cases.py"""
@@ -32,7 +33,7 @@ def dp(W, cap):
             ctx.view(p[i], r).uniform_(0.1, 0.9)
         ctx.view(m, r).zero_()
         ctx.view(v, r).fill_(1e-3)
-    scheds = [_lib.LAMB_GRID, _lib.LAMB_STREAMED] + ([_lib.LAMB_TMA] if W == 1 else [])
+    scheds = [_lib.LAMB_GRID, _lib.LAMB_STREAMED, _lib.LAMB_TMA]
     for sched in scheds:
         fused_rs_lamb_ag(ctx, tl, g, p, m, v, LambHParams(1e-3, 0.9, 0.999, 1.0, sched=sched, lag_elems=3000))
     for math in (_lib.MATH_EXACT, _lib.MATH_FAST):
@@ -86,7 +87,7 @@ def mp_pp(W):
 
 
 if __name__ == "__main__":
-    for W, cap in ((1, 1024), (1, 4096), (2, 1024), (4, 512)):
+    for W, cap in ((1, 1024), (1, 4096), (2, 1024), (4, 512), (2, 16384), (3, 16384)):  # 16384: Adam TMA at W>1
         dp(W, cap)
     for W in (2, 4):
         rooted_axis(W)
