@@ -44,10 +44,21 @@ CPU_SAMPLE = 1 << 22  # elements per core for cpu_baseline: ~10-30 s of CPU work
 
 
 def peaks():
+    """Roofline denominators: the driver-measured HBM copy GB/s and burst bf16
+    TFLOP/s (MEASURED_PEAKS.json), else B200_PROFILING.md's fallback."""
     p = ROOT / "MEASURED_PEAKS.json"
+
+    def num(x):
+        if isinstance(x, dict):  # tolerate {"value": ...} entries
+            x = x.get("value", x.get("median"))
+        return float(x)
+
     if p.exists():
-        d = json.loads(p.read_text())
-        return float(d["hbm_gbs"]), float(d["bf16_tflops"]), "measured"
+        try:
+            d = json.loads(p.read_text())
+            return num(d["hbm_gbs"]), num(d["bf16_tflops"]), "measured"
+        except (KeyError, TypeError, ValueError) as e:
+            print(f"bench: MEASURED_PEAKS.json unreadable ({e!r}); using the fallback peaks", file=sys.stderr)
     return 6650.0, 1590.0, "fallback"
 
 
