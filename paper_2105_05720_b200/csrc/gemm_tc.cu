@@ -339,16 +339,22 @@ __device__ __forceinline__ void mp_unit(const OvArgs& a, char* const* base, int 
 // load invalidates L1 every poll) and backs off exponentially up to 2 us,
 // keeping ~1.5k waiting warps from flooding L2 next to the GEMM's TMA
 // traffic; one acquire fence orders the partial-sum reads after the flag.
-__device__ __forceinline__ bool wait_tile_flag(const uint32_t* p, uint32_t want, const RankSet& rs) {
+__device__ __forceinline__ bool wait_tile_flag(const uint32_t* p, uint32_t want, const RankSet& rs, bool local) {
   uint32_t v;
-  asm volatile("ld.relaxed.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  if (local)
+    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  else
+    asm volatile("ld.relaxed.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   if (int32_t(v - want) < 0) {
     const unsigned long long t0 = globaltimer();
     unsigned ns = 128;
     for (;;) {
       __nanosleep(ns);
       ns = ns < 2048 ? ns * 2 : 2048;
-      asm volatile("ld.relaxed.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+      if (local)
+        asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+      else
+        asm volatile("ld.relaxed.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
       if (int32_t(v - want) >= 0) break;
       if (globaltimer() - t0 > rs.timeout_ns) {
         atomicCAS(rs.status, 0, COCONET_ERR_TIMEOUT);
@@ -356,7 +362,6 @@ __device__ __forceinline__ bool wait_tile_flag(const uint32_t* p, uint32_t want,
       }
     }
   }
-  asm volatile("fence.acq_rel.sys;" ::: "memory");
   return true;
 }
 
@@ -376,17 +381,30 @@ __device__ void mp_comm_warp(const OvArgs& a, char* const* base, int lane) {
     const int lr = rem >> 2, rg = rem & 3;
     const int me = a.rs.me >= 0 ? a.rs.me : lr;
     const int t_lo = (me * a.per) / a.bn, t_hi = ((me + 1) * a.per - 1) / a.bn;
+    // VIRTUAL (every rank in this grid): gpu-scope flags, fences and
+    // arrivals; across processes, system scope. One acquire fence per lane
+    // after all its flags.
+    const bool local = a.rs.me < 0;
     bool ok = true;
     if (lane < W) {
       const uint32_t* fl = reinterpret_cast<const uint32_t*>(base[lane] + a.flag_off);
-      for (int nt = t_lo; nt <= t_hi; ++nt) ok &= wait_tile_flag(fl + mt * a.tiles_n + nt, a.rs.epoch, a.rs);
+      for (int nt = t_lo; nt <= t_hi; ++nt) ok &= wait_tile_flag(fl + mt * a.tiles_n + nt, a.rs.epoch, a.rs, local);
+      if (local)
+        asm volatile("fence.acq_rel.gpu;" ::: "memory");
+      else
+        asm volatile("fence.acq_rel.sys;" ::: "memory");
     }
     if (!__all_sync(full, ok)) continue;  // watchdog fired; status already recorded
     mp_unit<T>(a, base, me, mt, rg, lane);
     __syncwarp();
     if (lane < W) {  // one arrival per (unit, destination rank)
-      __threadfence_system();
-      atomicAdd_system(reinterpret_cast<unsigned int*>(base[lane] + a.cnt_off), 1u);
+      if (local) {
+        __threadfence();
+        atomicAdd(reinterpret_cast<unsigned int*>(base[lane] + a.cnt_off), 1u);
+      } else {
+        __threadfence_system();
+        atomicAdd_system(reinterpret_cast<unsigned int*>(base[lane] + a.cnt_off), 1u);
+      }
     }
   }
 }
