@@ -1451,7 +1451,8 @@ int coconet_fused_rs_adam_ag(coconet_ctx_t c, coconet_tlist_t tl, const void* co
     if (g_elem == COCONET_F32) pick(float{});
     else if (g_elem == COCONET_F16) pick(__half{});
     else pick(__nv_bfloat16{});
-    const int per_sm = W == 1 ? 3 : 2;
+    const char* ce = getenv("COCONET_ADAM_TMA_CTAS");  // ring sized as for this many CTAs per SM
+    const int per_sm = ce ? std::max(1, std::min(4, atoi(ce))) : 3;
     TmaArgs ta;
     ta.stages = std::min(16, (200 << 10) / per_sm / sbytes);
     const size_t smem = size_t(ta.stages) * size_t(sbytes) + size_t(ta.stages) * 16 + 128;
@@ -1527,10 +1528,12 @@ int coconet_fused_rs_lamb_ag(coconet_ctx_t c, coconet_tlist_t tl, const void* co
   if (sched == COCONET_LAMB_TMA) {
     // 8 consumer warps x 2 quads per thread (2048-element chunks), 3 CTAs
     // per SM: the best of the sweep in profiles/r01_lamb_tma_sweep.json
-    // (COCONET_LAMB_TMA_CTAS overrides the CTAs per SM). At W > 1 the
-    // consumers also hold every rank's g quads: 2 CTAs per SM.
+    // (COCONET_LAMB_TMA_CTAS overrides the CTAs per SM the ring is sized
+    // for). Registers keep 2 resident, so this is a 2-stage ring of 2048-
+    // element chunks, which also measured best at W = 2/4/8
+    // (profiles/r01_lamb_w_probe.json: a 3-stage ring is 1-4% slower).
     const char* ce = getenv("COCONET_LAMB_TMA_CTAS");
-    const int per_sm = ce ? std::max(1, std::min(4, atoi(ce))) : (W == 1 ? 3 : 2);
+    const int per_sm = ce ? std::max(1, std::min(4, atoi(ce))) : 3;
     const void* fn = nullptr;
     int sbytes = 0, threads = 0;
     auto pick = [&](auto tag_g) {

@@ -36,11 +36,13 @@ for W in [int(x) for x in sys.argv[1:]] or [1, 2, 4, 8]:
     row = {}
     for math, mn in ((_lib.MATH_FAST, "fast"), (_lib.MATH_EXACT, "exact")):
         hp = AdamHParams(1e-3, 0.9, 0.999, 1.0, 1e-8, False, math, _lib.ALGO_TWO_SHOT)
-        for impl, env in (("ldg", "0"), ("tma", "1")):
+        for impl, env, ctas in (("ldg", "0", "3"), ("tma", "1", "3"), ("tma_ring3", "1", "2")):
             os.environ["COCONET_ADAM_TMA"] = env
+            os.environ["COCONET_ADAM_TMA_CTAS"] = ctas
             ms = timeit(lambda: fused_rs_adam_ag(ctx, tl, grads, params, m, v, hp), 5, warmup=2)
             row[f"{mn}_{impl}_ms"] = round(ms, 3)
             row[f"{mn}_{impl}_GBs"] = round((20 + 6 * W) * N / ms / 1e6, 1)
     os.environ.pop("COCONET_ADAM_TMA", None)
+    os.environ.pop("COCONET_ADAM_TMA_CTAS", None)
     print(json.dumps({f"W{W}": row}), flush=True)
     ctx.close()

@@ -33,8 +33,10 @@ for W in [int(x) for x in sys.argv[1:]] or [2, 4, 8]:
         ctx.view(m, r).zero_()
         ctx.view(v, r).fill_(1e-3)
     row = {}
+    # COCONET_LAMB_TMA_CTAS sizes the ring as for that many CTAs per SM
+    # (2 stay resident at W > 1: registers): 1 -> 7 stages, 2 -> 3, 3 -> 2
     for name, sched, ctas in (("grid", _lib.LAMB_GRID, None), ("tma", _lib.LAMB_TMA, None),
-                              ("tma_1cta", _lib.LAMB_TMA, "1")):
+                              ("tma_1cta", _lib.LAMB_TMA, "1"), ("tma_ring2", _lib.LAMB_TMA, "3")):
         if ctas:
             os.environ["COCONET_LAMB_TMA_CTAS"] = ctas
         hp = LambHParams(lr=1e-3, beta1=0.9, beta2=0.999, t=1.0, sched=sched)

@@ -223,9 +223,10 @@ def unfused_baselines(out, steps=5):
 
 
 def c2_w8(out, steps=5):
-    """The headline step at W=8 with VIRTUAL ranks: the GRID LAMB kernel the
-    8-GPU run uses (RS pulls of fp16 g from 8 ranks, sharded m/v, AG pushes of
-    p into 8 ranks), with all traffic in this GPU's HBM. Bytes per global
+    """The headline step at W=8 with VIRTUAL ranks: the LAMB kernel the
+    8-GPU run uses (AUTO = the TMA ring for the local m/v/p, RS pulls of fp16
+    g from 8 ranks, sharded m/v, AG pushes of p into 8 ranks), with all
+    traffic in this GPU's HBM. Bytes per global
     element summed over ranks: every rank's g read once (8 x 2 B), pass 1
     m, v, p read + m, v written (20 B), pass 2 m, v, p read (12 B), p pushed
     into 8 copies (32 B) = 80 B."""
