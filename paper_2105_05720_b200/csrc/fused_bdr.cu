@@ -134,45 +134,82 @@ __global__ void __launch_bounds__(kThreads) rs_bdr_ag_kernel(BdrArgs a, BdrK k) 
 // PP: union ranks [0, S) form the source stage, [S, 2S) the destination.
 // Sender i pulls chunk i of `x` from the source ranks (ring order within the
 // source stage), applies the epilogue and stores the chunk into `out` of every
-// destination rank.
-template <typename T, int MATH>
+// destination rank. V16: 16-byte vectors (8 elements at 16-bit types) when
+// every operand and the chunk allow it, else 4-element quads.
+template <typename T, int MATH, bool V16, int SS>
 __global__ void __launch_bounds__(kThreads) rs_send_ag_kernel(BdrArgs a, BdrK k) {
+  constexpr int kS = SS > 0 ? SS : kMaxRanks;  // stage size: compile-time when specialised
   __shared__ char* s_base[kMaxRanks];
   const RankSet& rs = a.rs;
   if (threadIdx.x < kMaxRanks) s_base[threadIdx.x] = threadIdx.x < rs.world ? rs.base[threadIdx.x] : nullptr;
-  const int U = rs.world, me = rs.rank(), S = a.src_ranks;
+  const int S = SS > 0 ? SS : a.src_ranks;
+  const int U = 2 * S, me = rs.rank();
   if (!edge_barrier(rs, 0)) return;
   if (me < S) {
     const int64_t per = a.n / S;
-    const int64_t nq = per >> 2;
-    for (int64_t q = int64_t(blockIdx.x) * kThreads + threadIdx.x; q < nq; q += int64_t(gridDim.x) * kThreads) {
-      const int64_t gi = int64_t(me) * per + q * 4;
-      // every source rank's quad, b and r in flight before the fold
-      float acc[4], x[kMaxRanks][4], b4[4], r4[4], o[4];
+    if constexpr (V16) {
+      // 8 elements per 16-byte vector, kept packed until the fold
+      constexpr int VN = Vec16<T>::V;
+      const int64_t nv = per / VN;
+      for (int64_t q = int64_t(blockIdx.x) * kThreads + threadIdx.x; q < nv; q += int64_t(gridDim.x) * kThreads) {
+        const int64_t gi = int64_t(me) * per + q * VN;
+        Vec16<T> x[kS], bv, rv;
 #pragma unroll
-      for (int j = 0; j < kMaxRanks; ++j) {
-        if (j >= S) break;
-        int src = me + 1 + j;
-        src -= src >= S ? S : 0;
-        src -= src >= S ? S : 0;
-        load4(reinterpret_cast<const T*>(s_base[src] + a.x_off) + gi, x[j]);
+        for (int j = 0; j < kS; ++j) {
+          if (j >= S) break;
+          int src = me + 1 + j;
+          src -= src >= S ? S : 0;
+          src -= src >= S ? S : 0;
+          x[j].load(reinterpret_cast<const T*>(s_base[src] + a.x_off) + gi);
+        }
+        bv.load(reinterpret_cast<const T*>(s_base[me] + a.b_off) + gi);
+        rv.load(reinterpret_cast<const T*>(s_base[me] + a.r_off) + gi);
+        float o[VN];
+#pragma unroll
+        for (int i = 0; i < VN; ++i) {
+          float acc = x[0].get(i);
+#pragma unroll
+          for (int j = 1; j < kS; ++j)
+            if (j < S) acc = __fadd_rn(acc, x[j].get(i));
+          o[i] = bdr<MATH>(acc, bv.get(i), rv.get(i), uint64_t(gi + i), k);
+        }
+#pragma unroll
+        for (int j = 0; j < kS; ++j) {
+          if (j >= U - S) break;
+          store16(reinterpret_cast<T*>(s_base[S + j] + a.out_off) + gi, o);
+        }
       }
-      load4(reinterpret_cast<const T*>(s_base[me] + a.b_off) + gi, b4);
-      load4(reinterpret_cast<const T*>(s_base[me] + a.r_off) + gi, r4);
+    } else {
+      const int64_t nq = per >> 2;
+      for (int64_t q = int64_t(blockIdx.x) * kThreads + threadIdx.x; q < nq; q += int64_t(gridDim.x) * kThreads) {
+        const int64_t gi = int64_t(me) * per + q * 4;
+        // every source rank's quad, b and r in flight before the fold
+        float acc[4], x[kS][4], b4[4], r4[4], o[4];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) acc[i] = x[0][i];
+        for (int j = 0; j < kS; ++j) {
+          if (j >= S) break;
+          int src = me + 1 + j;
+          src -= src >= S ? S : 0;
+          src -= src >= S ? S : 0;
+          load4(reinterpret_cast<const T*>(s_base[src] + a.x_off) + gi, x[j]);
+        }
+        load4(reinterpret_cast<const T*>(s_base[me] + a.b_off) + gi, b4);
+        load4(reinterpret_cast<const T*>(s_base[me] + a.r_off) + gi, r4);
 #pragma unroll
-      for (int j = 1; j < kMaxRanks; ++j) {
-        if (j >= S) break;
+        for (int i = 0; i < 4; ++i) acc[i] = x[0][i];
 #pragma unroll
-        for (int i = 0; i < 4; ++i) acc[i] = __fadd_rn(acc[i], x[j][i]);
-      }
+        for (int j = 1; j < kS; ++j) {
+          if (j >= S) break;
 #pragma unroll
-      for (int i = 0; i < 4; ++i) o[i] = bdr<MATH>(acc[i], b4[i], r4[i], uint64_t(gi + i), k);
+          for (int i = 0; i < 4; ++i) acc[i] = __fadd_rn(acc[i], x[j][i]);
+        }
 #pragma unroll
-      for (int j = 0; j < kMaxRanks; ++j) {
-        if (j >= U - S) break;
-        store4(reinterpret_cast<T*>(s_base[S + j] + a.out_off) + gi, o);
+        for (int i = 0; i < 4; ++i) o[i] = bdr<MATH>(acc[i], b4[i], r4[i], uint64_t(gi + i), k);
+#pragma unroll
+        for (int j = 0; j < kS; ++j) {
+          if (j >= U - S) break;
+          store4(reinterpret_cast<T*>(s_base[S + j] + a.out_off) + gi, o);
+        }
       }
     }
   }
@@ -201,12 +238,21 @@ const void* mp_fn(int elem) {
   }
 }
 
+// stage size specialised for 2 and 4 (the paper's 2 x 4 boundary), generic otherwise
+template <typename T, int MATH, bool V16>
+const void* pp_fn_s(int S) {
+  return S == 4   ? reinterpret_cast<const void*>(&rs_send_ag_kernel<T, MATH, V16, 4>)
+         : S == 2 ? reinterpret_cast<const void*>(&rs_send_ag_kernel<T, MATH, V16, 2>)
+                  : reinterpret_cast<const void*>(&rs_send_ag_kernel<T, MATH, V16, 0>);
+}
+
 template <int MATH>
-const void* pp_fn(int elem) {
+const void* pp_fn(int elem, bool v16, int S) {
   switch (elem) {
-    case COCONET_F16: return reinterpret_cast<const void*>(&rs_send_ag_kernel<__half, MATH>);
-    case COCONET_BF16: return reinterpret_cast<const void*>(&rs_send_ag_kernel<__nv_bfloat16, MATH>);
-    default: return reinterpret_cast<const void*>(&rs_send_ag_kernel<float, MATH>);
+    case COCONET_F16: return v16 ? pp_fn_s<__half, MATH, true>(S) : pp_fn_s<__half, MATH, false>(S);
+    case COCONET_BF16:
+      return v16 ? pp_fn_s<__nv_bfloat16, MATH, true>(S) : pp_fn_s<__nv_bfloat16, MATH, false>(S);
+    default: return pp_fn_s<float, MATH, false>(S);  // fp32 quads are 16 bytes already
   }
 }
 
@@ -290,9 +336,16 @@ int coconet_rs_fused_send_ag(coconet_ctx_t c, int src_group, int dst_group, cons
   rc = union_group(c, gs.first, gs.size + gd.size, &ug);
   if (rc) return rc;
   BdrK k = make_k(hp);
-  const void* fn = hp->math == COCONET_MATH_EXACT ? pp_fn<COCONET_MATH_EXACT>(elem) : pp_fn<COCONET_MATH_FAST>(elem);
+  // 16-bit types: 8-element vectors when every operand is 16-byte aligned and
+  // the chunk is a multiple of 8 elements
+  const bool v16 = elem != COCONET_F32 && (n / gs.size) % 8 == 0 &&
+                   ((a.x_off | a.b_off | a.r_off | a.out_off) % 16) == 0;
+  const void* fn =
+      hp->math == COCONET_MATH_EXACT ? pp_fn<COCONET_MATH_EXACT>(elem, v16, gs.size)
+                                     : pp_fn<COCONET_MATH_FAST>(elem, v16, gs.size);
+  const int vn = v16 ? 8 : 4;
   int blocks = 0;
-  rc = coop_blocks(c, fn, kThreads, 0, ug, (n / gs.size / 4 + kThreads - 1) / kThreads, &blocks);
+  rc = coop_blocks(c, fn, kThreads, 0, ug, (n / gs.size / vn + kThreads - 1) / kThreads, &blocks);
   if (!rc) rc = make_rankset(c, ug, &a.rs);
   if (rc) return rc;
   void* args[] = {&a, &k};

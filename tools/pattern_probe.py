@@ -135,6 +135,16 @@ def c4(out):
         # HBM bytes on this device: each sender reads its chunk from 4 ranks + b + r,
         # writes it to 4 receivers: (4 + 2 + 4) * N/4 * 4B per sender, 4 senders
         out[f"c4_pp_{name}_GBs"] = 10 * N * 4 / (ms * 1e-3) / 1e9
+    # fp16 activations (the paper's C4 runs fp16 as well)
+    xh, bh, rh, oh = (ctx.alloc([N], torch.float16) for _ in range(4))
+    for r in range(S):
+        ctx.view(xh, r).copy_(ctx.view(x, r))
+        ctx.view(bh, r).copy_(ctx.view(bb, r))
+        ctx.view(rh, r).copy_(ctx.view(rr, r))
+    hp = BdrHParams(0.1, 1, 3251584743947114031, _lib.MATH_FAST)
+    ms = timeit(lambda: rs_fused_send_ag(ctx, g0, g1, xh, bh, rh, oh, hp))
+    out["c4_pp_2x4_N25M_fp16_fast_us"] = ms * 1e3
+    out["c4_pp_fp16_fast_GBs"] = 10 * N * 2 / (ms * 1e-3) / 1e9
     ctx.close()
 
 
