@@ -103,6 +103,8 @@ def c3(out, gemm_only=False):
     if gemm_only:
         return
     ar = timeit(lambda: fused_rs_bdr_ag(ctx, part, bb, rr, o1, hp))
+    out["c3_fused_rs_bdr_ag_exact_8ranks_us"] = timeit(
+        lambda: fused_rs_bdr_ag(ctx, part, bb, rr, o1, BdrHParams(0.1, 1, 11617925594314093840, _lib.MATH_EXACT))) * 1e3
     ov = timeit(lambda: mm_overlap_fused_ar(ctx, x, w, bb, rr, part, o1, hp))
     os.environ["COCONET_MP_OVERLAP"] = "fused"  # the one-kernel overlap, forced
     ovf = timeit(lambda: mm_overlap_fused_ar(ctx, x, w, bb, rr, part, o1, hp))
