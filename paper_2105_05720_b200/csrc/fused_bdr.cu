@@ -87,13 +87,14 @@ __device__ __forceinline__ void store16(T* p, const float (&o)[16 / sizeof(T)]) 
 
 // MP: rank c owns column block c of every row. One 16-byte vector per thread
 // per rank; all W + 2 loads issued before the ring-order fold.
-template <typename T, int MATH>
+template <typename T, int MATH, int WT>
 __global__ void __launch_bounds__(kThreads) rs_bdr_ag_kernel(BdrArgs a, BdrK k) {
   constexpr int V = Vec16<T>::V;
+  constexpr int kW = WT > 0 ? WT : kMaxRanks;  // group size: compile-time when specialised
   __shared__ char* s_base[kMaxRanks];
   const RankSet& rs = a.rs;
   if (threadIdx.x < kMaxRanks) s_base[threadIdx.x] = threadIdx.x < rs.world ? rs.base[threadIdx.x] : nullptr;
-  const int W = rs.world, me = rs.rank();
+  const int W = WT > 0 ? WT : rs.world, me = rs.rank();
   if (!edge_barrier(rs, 0)) return;
   const int64_t vpr = a.per / V;  // vectors per row block
   const int64_t nv = a.rows * vpr;
@@ -102,9 +103,9 @@ __global__ void __launch_bounds__(kThreads) rs_bdr_ag_kernel(BdrArgs a, BdrK k) 
     const int64_t row = q / vpr;
     const int64_t col = int64_t(me) * a.per + (q - row * vpr) * V;
     const int64_t gi = row * a.cols + col;
-    Vec16<T> x[kMaxRanks], bv, rv;
+    Vec16<T> x[kW], bv, rv;
 #pragma unroll
-    for (int j = 0; j < kMaxRanks; ++j) {
+    for (int j = 0; j < kW; ++j) {
       if (j >= W) break;
       int src = me + 1 + j;
       src -= src >= W ? W : 0;
@@ -118,12 +119,12 @@ __global__ void __launch_bounds__(kThreads) rs_bdr_ag_kernel(BdrArgs a, BdrK k) 
     for (int i = 0; i < V; ++i) {
       float acc = x[0].get(i);
 #pragma unroll
-      for (int j = 1; j < kMaxRanks; ++j)
+      for (int j = 1; j < kW; ++j)
         if (j < W) acc = __fadd_rn(acc, x[j].get(i));  // ring order (runtime.hpp:302-305)
       o[i] = bdr<MATH>(acc, bv.get(i), rv.get(i), uint64_t(gi + i), k);
     }
 #pragma unroll
-    for (int j = 0; j < kMaxRanks; ++j) {
+    for (int j = 0; j < kW; ++j) {
       if (j >= W) break;
       store16(reinterpret_cast<T*>(s_base[j] + a.out_off) + gi, o);
     }
@@ -229,12 +230,24 @@ BdrK make_k(const coconet_bdr_params* hp) {
   return k;
 }
 
+// EXACT: group size specialised for 2, 4 and 8 (C3 W=8: 151 -> 144 us).
+// FAST keeps the generic kernel: specialised, the 8-rank fold measured
+// slower (141 -> 166 us) at the same register count.
+template <typename T, int MATH>
+const void* mp_fn_w(int W) {
+  if (MATH == COCONET_MATH_FAST) return reinterpret_cast<const void*>(&rs_bdr_ag_kernel<T, MATH, 0>);
+  return W == 8   ? reinterpret_cast<const void*>(&rs_bdr_ag_kernel<T, MATH, 8>)
+         : W == 4 ? reinterpret_cast<const void*>(&rs_bdr_ag_kernel<T, MATH, 4>)
+         : W == 2 ? reinterpret_cast<const void*>(&rs_bdr_ag_kernel<T, MATH, 2>)
+                  : reinterpret_cast<const void*>(&rs_bdr_ag_kernel<T, MATH, 0>);
+}
+
 template <int MATH>
-const void* mp_fn(int elem) {
+const void* mp_fn(int elem, int W) {
   switch (elem) {
-    case COCONET_F16: return reinterpret_cast<const void*>(&rs_bdr_ag_kernel<__half, MATH>);
-    case COCONET_BF16: return reinterpret_cast<const void*>(&rs_bdr_ag_kernel<__nv_bfloat16, MATH>);
-    default: return reinterpret_cast<const void*>(&rs_bdr_ag_kernel<float, MATH>);
+    case COCONET_F16: return mp_fn_w<__half, MATH>(W);
+    case COCONET_BF16: return mp_fn_w<__nv_bfloat16, MATH>(W);
+    default: return mp_fn_w<float, MATH>(W);
   }
 }
 
@@ -304,7 +317,8 @@ int coconet_fused_rs_bdr_ag(coconet_ctx_t c, int group, const void* x, const voi
   a.cols = cols;
   a.per = cols / W;
   BdrK k = make_k(hp);
-  const void* fn = hp->math == COCONET_MATH_EXACT ? mp_fn<COCONET_MATH_EXACT>(elem) : mp_fn<COCONET_MATH_FAST>(elem);
+  const void* fn = hp->math == COCONET_MATH_EXACT ? mp_fn<COCONET_MATH_EXACT>(elem, W)
+                                                  : mp_fn<COCONET_MATH_FAST>(elem, W);
   int blocks = 0;
   rc = coop_blocks(c, fn, kThreads, 0, group, (rows * (a.per / (16 / esz(elem))) + kThreads - 1) / kThreads, &blocks);
   if (!rc) rc = make_rankset(c, group, &a.rs);
