@@ -112,3 +112,13 @@ def test_run_cuda_is_deterministic(tmp_path, case, math):
             j.pop(k)
         outs.append(json.dumps(j, sort_keys=True))
     assert outs[0] == outs[1]
+
+
+def test_run_cuda_reps_reports_warm_median(tmp_path):
+    """`run --reps R` executes R fresh engines (same digest every time, or
+    the CLI fails) and reports the median device time after the first."""
+    need_cli()
+    f, rec = program_file(tmp_path, "adam_W4_N4096", "sched_program")
+    j = json.loads(cli("run", f, *dims_args(rec), "--reps", 3, check_rc=0).stdout)
+    assert j["runs"] == 3 and j["device_ms"] > 0 and j["device_ms_first"] > 0
+    assert j["digest"] == rec["engine_sched_digest"]
