@@ -25,10 +25,11 @@ ROOT = Path(__file__).resolve().parent.parent
 REF = Path("/root/reference/proj")
 OUT = ROOT / "tests" / "golden"
 
-ADAM_CASES = [(w, n) for w in (1, 2, 4, 8) for n in (1024, 4096)] + [(4, 1 << 20), (8, 1 << 16)]
+ADAM_CASES = [(w, n) for w in (1, 2, 4, 8) for n in (1024, 4096)] + [(4, 1 << 20), (8, 1 << 16)] + [
+    (3, 3000), (5, 4100), (6, 6000), (7, 7007)]  # odd world sizes; 7007/7 = 1001 takes the generic lowering
 MP_CASES = [(w, dims) for w in (1, 2, 4) for dims in ({"B": 2, "S": 8, "H": 64},)] + [
     (8, {"B": 2, "S": 16, "H": 128})]
-PP_CASES = [(w, n) for w in (2, 4, 8) for n in (1024, 4096)]
+PP_CASES = [(w, n) for w in (2, 4, 8) for n in (1024, 4096)] + [(6, 6000)]
 # Reduce / Broadcast (runtime.hpp:415-436) + reorder_broadcast (transform.hpp:265-330):
 # no reference golden uses them, so the program is authored in the reference
 # format (tests/golden/rooted_*.json, reducer substituted) and evaluated here.
