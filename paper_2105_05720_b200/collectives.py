@@ -105,7 +105,16 @@ class TensorList:
 
 
 def _ptrs(ctx: Context, bufs):
-    return ptr_array([ctx.ptr(b) for b in bufs])
+    """The C pointer array of `bufs` (rank 0's heap in VIRTUAL mode), built
+    once per buffer list: a training loop passes the same list every step."""
+    key = tuple(b.offset for b in bufs)
+    cache = ctx.__dict__.setdefault("_ptr_arrays", {})
+    arr = cache.get(key)
+    if arr is None:
+        if len(cache) > 256:
+            cache.clear()
+        arr = cache[key] = ptr_array([ctx.ptr(b) for b in bufs])
+    return arr
 
 
 @dataclass
