@@ -221,8 +221,8 @@ def run_coconet(args):
     ctx = Context(W, mode="distributed" if distributed else "virtual", rank=rank, device=local_rank,
                   heap_bytes=need)
     # bucket capacity: the reference's 2^10 (runtime.hpp:579) fixes the flat order
-    # the parity tests pin; for this workload 4096-element buckets amortise the
-    # per-segment cost (descriptor + per-segment norm reduction), DESIGN.md §3
+    # the parity tests pin; for this workload 16384-element buckets amortise the
+    # per-segment cost of the TMA ring (descriptor + per-segment norm), DESIGN.md §3
     cap = BUCKET_CAP if world == 1 else BUCKET_CAP_MULTI
     tl = TensorList(ctx, counts, bucket_cap=cap)
     # one flat buffer per dtype (tensors at 64-element aligned offsets) so the
