@@ -82,6 +82,9 @@ def mp_pp(W):
         N = 1024 * S
         xs, b2, r2, o2 = (ctx.alloc([N]) for _ in range(4))
         rs_fused_send_ag(ctx, g0, g1, xs, b2, r2, o2, BdrHParams(0.1, 1, 3251584743947114031, _lib.MATH_EXACT))
+        xh, bh, rh, oh = (ctx.alloc([N], torch.float16) for _ in range(4))  # 16-byte vector path
+        rs_fused_send_ag(ctx, g0, g1, xh, bh, rh, oh, BdrHParams(0.1, 1, 3251584743947114031, _lib.MATH_FAST))
+    fused_rs_bdr_ag(ctx, part, bb, rr, out, BdrHParams(0.1, 1, 11617925594314093840, _lib.MATH_EXACT))
     ctx.check()
     ctx.close()
 
