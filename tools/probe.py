@@ -91,7 +91,7 @@ def extra_probes(steps=10):
     counts = bert_large_counts()
     N = sum(counts)
     ctx = Context(1, heap_bytes=N * 24 + (1 << 30))
-    for cap in (1024, 4096, 16384):
+    for cap in (1024, 4096, 16384, 32768, 65536):
         tl = TensorList(ctx, counts, bucket_cap=cap)
         grads = [ctx.alloc([n], torch.float16) for n in counts]
         params = [ctx.alloc([n]) for n in counts]
