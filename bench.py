@@ -261,24 +261,34 @@ def run_coconet(args):
         step()
     ctx.check()
     barrier()
-    sampler = ClockSampler(local_rank)
-    sampler.start()
-    launches0 = ctx.launch_count()
-    e0 = torch.cuda.Event(enable_timing=True)
-    e1 = torch.cuda.Event(enable_timing=True)
-    torch.cuda.nvtx.range_push("timed")  # ncu --nvtx-include "timed/" captures exactly these launches
-    e0.record(stream)
-    for _ in range(args.steps):
-        step()
-    e1.record(stream)
-    torch.cuda.nvtx.range_pop()
-    barrier()
-    clocks = sampler.stop()
-    ctx.check()
-    launches = ctx.launch_count() - launches0
-    ms = e0.elapsed_time(e1) / args.steps
-    if distributed:
-        ms = max_over_ranks(ms)
+    def timed():
+        sampler = ClockSampler(local_rank)
+        sampler.start()
+        launches0 = ctx.launch_count()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        torch.cuda.nvtx.range_push("timed")  # ncu --nvtx-include "timed/" captures exactly these launches
+        e0.record(stream)
+        for _ in range(args.steps):
+            step()
+        e1.record(stream)
+        torch.cuda.nvtx.range_pop()
+        barrier()
+        clocks = sampler.stop()
+        ctx.check()
+        t = e0.elapsed_time(e1) / args.steps
+        return (max_over_ranks(t) if distributed else t), clocks, ctx.launch_count() - launches0
+
+    ms, clocks, launches = timed()
+    # the recipe's rejection rule: a slowdown reason, or SM clocks well below
+    # max with no reason (a leftover lock), re-measures once (on every rank)
+    bad = bool(set(clocks["reasons"]) & {"hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown"}) or (
+        clocks["sm_mhz"] is not None and clocks["sm_max_mhz"] and not clocks["reasons"]
+        and clocks["sm_mhz"] < 0.85 * clocks["sm_max_mhz"])
+    if (max_over_ranks(float(bad)) if distributed else float(bad)) > 0:
+        first = clocks
+        ms, clocks, launches = timed()
+        clocks = dict(clocks, remeasured_after=first)
     N = BERT_LARGE_PARAMS
     value = W * N / (ms * 1e-3) / 1e9
 
