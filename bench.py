@@ -78,24 +78,39 @@ class ClockSampler:
         self.stop_flag = threading.Event()
         self.thread = None
         self.max_mhz = None
+        self.error = None
 
     def start(self):
+        self.error = None
         try:
             import pynvml
             pynvml.nvmlInit()
-            h = pynvml.nvmlDeviceGetHandleByIndex(self.device)
+            # NVML numbers GPUs ignoring CUDA_VISIBLE_DEVICES: resolve the
+            # handle of THIS CUDA device by its PCI bus id
+            h = None
+            try:
+                import torch
+                bus = torch.cuda.get_device_properties(self.device).pci_bus_id
+                if bus:
+                    h = pynvml.nvmlDeviceGetHandleByPciBusId_v2(bus.encode() if isinstance(bus, str) else bus)
+            except Exception:
+                h = None
+            if h is None:
+                h = pynvml.nvmlDeviceGetHandleByIndex(self.device)
             self.max_mhz = float(pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM))
-        except Exception:
+            reasons_fn = getattr(pynvml, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+                getattr(pynvml, "nvmlDeviceGetCurrentClocksThrottleReasons")
+        except Exception as e:
+            self.error = repr(e)
             return
 
         def run():
             while not self.stop_flag.is_set():
                 try:
                     mhz = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
-                    reasons = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
-                    self.samples.append((float(mhz), int(reasons)))
-                except Exception:
-                    pass
+                    self.samples.append((float(mhz), int(reasons_fn(h))))
+                except Exception as e:
+                    self.error = repr(e)
                 time.sleep(0.01)
 
         self.thread = threading.Thread(target=run, daemon=True)
@@ -106,7 +121,8 @@ class ClockSampler:
         if self.thread:
             self.thread.join(timeout=1)
         if not self.samples:
-            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "samples": 0, "reasons": ["unsampled"]}
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "samples": 0, "reasons": ["unsampled"],
+                    "sampling_error": self.error}
         active = sorted({n for _, bits in self.samples for n, m in self.REASONS.items() if bits & m})
         return {"sm_mhz": statistics.median(m for m, _ in self.samples), "sm_max_mhz": self.max_mhz,
                 "samples": len(self.samples), "reasons": active, "source": "NVML, 10 ms"}

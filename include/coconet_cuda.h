@@ -202,9 +202,16 @@ int coconet_fused_rs_adam_ag(coconet_ctx_t ctx, coconet_tlist_t tl, const void* 
  * the same kernel (K12). */
 typedef struct {
   float lr, beta1, beta2, t, eps, wd;
-  int math;  /* FAST only for now (EXACT is rejected: sums cannot match bit-wise) */
+  int math;  /* FAST: fp32 element math, m'/v' stored in pass 1 (38 B/element at fp16 g).
+                EXACT: the reference's double element math (expr.hpp:186-222) with a
+                read-only pass 1 and m', v', u recomputed in pass 2 from the same old
+                values, as eval_pointwise does (state.hpp:139-190); only the norm
+                summation order differs from the Engine. `sched` is ignored. */
   int sched; /* coconet_lamb_sched; both give bit-identical results */
   int64_t lag_elems; /* STREAMED: pass-1 -> pass-2 distance in elements (0 = default) */
+  int trust_guard;   /* 0: the golden's raw lr*sqrt(P)/sqrt(U) (reference parity);
+                        1: ratio = lr when either norm is 0 (apex/NVLAMB; FusedLAMB) */
+  int pad_;
 } coconet_lamb_params;
 
 /* LAMB schedules (bit-identical results). GRID: pass 1 over the whole shard,

@@ -52,7 +52,7 @@ class AdamParams(C.Structure):
 class LambParams(C.Structure):
     _fields_ = [("lr", C.c_float), ("beta1", C.c_float), ("beta2", C.c_float), ("t", C.c_float),
                 ("eps", C.c_float), ("wd", C.c_float), ("math", C.c_int), ("sched", C.c_int),
-                ("lag_elems", C.c_int64)]
+                ("lag_elems", C.c_int64), ("trust_guard", C.c_int), ("pad_", C.c_int)]
 
 
 class BdrParams(C.Structure):

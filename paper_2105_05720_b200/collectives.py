@@ -140,6 +140,7 @@ class LambHParams:
     math: int = _lib.MATH_FAST
     sched: int = _lib.LAMB_AUTO   # GRID or STREAMED (L2-resident pass 2); results are bit-identical
     lag_elems: int = 0            # STREAMED: pass-1 -> pass-2 distance in elements (0 = library default)
+    trust_guard: bool = False     # ratio = lr for a zero-norm tensor (apex/NVLAMB); False = the golden's formula
 
 
 def fused_rs_adam_ag(ctx: Context, tl: TensorList, grads, params, m: SymmBuffer, v: SymmBuffer,
@@ -155,7 +156,8 @@ def fused_rs_adam_ag(ctx: Context, tl: TensorList, grads, params, m: SymmBuffer,
 def fused_rs_lamb_ag(ctx: Context, tl: TensorList, grads, params, m: SymmBuffer, v: SymmBuffer,
                      hp: LambHParams, stream=None) -> None:
     g_elem = elem_of(grads[0].dtype)
-    p = _lib.LambParams(hp.lr, hp.beta1, hp.beta2, hp.t, hp.eps, hp.wd, hp.math, hp.sched, hp.lag_elems)
+    p = _lib.LambParams(hp.lr, hp.beta1, hp.beta2, hp.t, hp.eps, hp.wd, hp.math, hp.sched, hp.lag_elems,
+                         int(hp.trust_guard))
     check(ctx.lib.coconet_fused_rs_lamb_ag(
         ctx.handle, tl.handle, _ptrs(ctx, grads), g_elem, _ptrs(ctx, params), ctx.ptr(m), ctx.ptr(v),
         C.byref(p), ctx.stream_ptr(stream)))

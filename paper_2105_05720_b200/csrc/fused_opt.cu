@@ -65,6 +65,9 @@ struct AdamK {
 struct LambK {
   double lr;
   float fb1, fb2, fcm, fcv, frbc1, frbc2, feps, fwd;
+  // EXACT: the double constants eval_expr forms from the f32 decls
+  double b1, b2, c1, c2, bc1, bc2, eps, wd;
+  int guard;  // trust_ratio(): lr when a norm is 0 (apex/NVLAMB) instead of the raw formula
   const int64_t* csr_ptr;  // per rank: n_tensors+1 entries at csr_begin[r]
   const int64_t* csr_idx;
   double* seg_part;
@@ -402,6 +405,16 @@ __device__ __forceinline__ float lamb_u(float m, float v, float p, const LambK& 
   return __fdividef(m * k.frbc1, sqrtf(v * k.frbc2) + k.feps) + k.fwd * p;
 }
 
+// Per-tensor trust ratio of the golden: lr*sqrt(sum p^2)/sqrt(sum u^2)
+// (expr text of tests/golden/lamb_fused_program.json, left-associative). The
+// raw formula freezes a zero-norm tensor (ratio 0) and turns 0/0 into NaN;
+// with k.guard (the torch-facing FusedLAMB) a zero norm gives ratio = lr, the
+// apex / NVLAMB convention.
+__device__ __forceinline__ double trust_ratio(double P, double U, const LambK& k) {
+  if (k.guard && (P == 0.0 || U == 0.0)) return k.lr;
+  return __ddiv_rn(__dmul_rn(k.lr, __dsqrt_rn(P)), __dsqrt_rn(U));
+}
+
 // LAMB, two passes inside one cooperative kernel:
 //  pass 1: RS pull -> m, v update -> per-segment partial sums of p^2 and u^2
 //  grid sync -> per-tensor partials of this rank (fixed segment order, so
@@ -517,7 +530,7 @@ __global__ void __launch_bounds__(kThreads, 2) lamb_kernel(OptArgs a, LambK k) {
         P += __ldcg(xch_me + (int64_t(q) * a.n_tensors + d.tensor) * 2);
         Uu += __ldcg(xch_me + (int64_t(q) * a.n_tensors + d.tensor) * 2 + 1);
       }
-    const float ratio = float((k.lr * sqrt(P)) / sqrt(Uu));
+    const float ratio = float(trust_ratio(P, Uu, k));
     const int64_t poff = d.boff;
     const int64_t q0 = d.toff >> 2, q1 = (d.toff + d.len + 3) >> 2;
     for (int64_t qb = q0 + lane; qb < q1; qb += 32 * U) {
@@ -546,6 +559,144 @@ __global__ void __launch_bounds__(kThreads, 2) lamb_kernel(OptArgs a, LambK k) {
 #pragma unroll
           for (int j = 0; j < Ranks<WT>::kMax; ++j)
             if (Ranks<WT>::has(j, W)) st4m(reinterpret_cast<float*>(s_base[j] + poff) + e0, pn, lo, hi);
+        }
+      }
+    }
+  }
+  edge_barrier(rs, 1);
+}
+
+// LAMB element in EXACT math: eval_expr's double arithmetic on the golden's
+// expression (tests/golden/lamb_fused_program.json; parser association,
+// json_io.hpp:166-183, explicit _rn so nothing contracts):
+//   m' = m*b1 + c1*g ; v' = v*b2 + (c2*g)*g
+//   u  = (m'/bc1) / (sqrt(v'/bc2) + eps) + wd*p
+__device__ __forceinline__ double lamb_u_exact(float g, float m, float v, float p, const LambK& k, double& mn,
+                                               double& vn) {
+  const double gd = g;
+  mn = __dadd_rn(__dmul_rn(double(m), k.b1), __dmul_rn(k.c1, gd));
+  vn = __dadd_rn(__dmul_rn(double(v), k.b2), __dmul_rn(__dmul_rn(k.c2, gd), gd));
+  const double den = __dadd_rn(__dsqrt_rn(__ddiv_rn(vn, k.bc2)), k.eps);
+  return __dadd_rn(__ddiv_rn(__ddiv_rn(mn, k.bc1), den), __dmul_rn(k.wd, double(p)));
+}
+
+// Between the two LAMB passes: this rank's per-tensor (P, U) partials, summed
+// over its segments in CSR (fixed) order, into every rank's exchange slot
+// [me][t] (state.hpp:163-167 combines them in rank order afterwards).
+__device__ __forceinline__ void lamb_push_partials(const OptArgs& a, const LambK& k, char* const* s_base, int me,
+                                                   int W, bool ok, int64_t wid, int64_t wstride, int lane) {
+  const int64_t xch_off = int64_t(group_area(a.rs.group));
+  for (int64_t t = ok ? wid : a.n_tensors; t < a.n_tensors; t += wstride) {
+    const int64_t* ptr = k.csr_ptr + k.csr_begin[me];
+    const int64_t b = ptr[t], e = ptr[t + 1];
+    double sp = 0.0, su = 0.0;
+    for (int64_t i = b + lane; i < e; i += 32) {
+      const int64_t s = k.csr_idx[i];
+      sp += k.seg_part[2 * s];
+      su += k.seg_part[2 * s + 1];
+    }
+    sp = warp_sum(sp);
+    su = warp_sum(su);
+    if (lane < W) {
+      double* xq = reinterpret_cast<double*>(s_base[lane] + xch_off);
+      xq[(int64_t(me) * a.n_tensors + t) * 2] = sp;
+      xq[(int64_t(me) * a.n_tensors + t) * 2 + 1] = su;
+    }
+  }
+}
+
+// LAMB in EXACT math (COCONET_MATH_EXACT): the reference evaluates the
+// ReduceTensor pre-pass and the element pass from the SAME old m, v
+// (state.hpp:139-190: the pre-pass does no Update stores, the element pass
+// recomputes update(m, ...) from the old values). So pass 1 here is read-only
+// (ring-order g, m, v, p -> u in double -> per-segment double sums of p*p and
+// u*u) and pass 2 recomputes m', v', u from the same inputs, stores float(m'),
+// float(v') and pushes float(p - ratio*u) (40 B/element at fp16 g against
+// FAST's 38). Only the order of the two norm sums differs from the Engine's
+// sequential accumulation.
+template <typename G, int WT>
+__global__ void __launch_bounds__(kThreads, 2) lamb_exact_kernel(OptArgs a, LambK k) {
+  __shared__ char* s_base[kMaxRanks];
+  const RankSet& rs = a.rs;
+  if (threadIdx.x < kMaxRanks) s_base[threadIdx.x] = threadIdx.x < rs.world ? rs.base[threadIdx.x] : nullptr;
+  const int W = WT > 0 ? WT : rs.world;
+  const int me = rs.rank();
+  const bool ok = edge_barrier(rs, 0);  // no early return before the grid syncs
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t sb = a.seg_begin[me], se = ok ? a.seg_begin[me + 1] : sb;
+  float* m = reinterpret_cast<float*>(s_base[me] + a.m_off);
+  float* v = reinterpret_cast<float*>(s_base[me] + a.v_off);
+  const char* pme = s_base[me];
+  const int64_t wstride = int64_t(gridDim.x) * kWarps;
+  const int64_t wid = int64_t(blockIdx.x) * kWarps + warp;
+  for (int pass = 0; pass < 2; ++pass) {
+    if (pass == 1) {
+      __threadfence();
+      cg::this_grid().sync();
+      lamb_push_partials(a, k, s_base, me, W, ok, wid, wstride, lane);
+      __threadfence_system();
+      cg::this_grid().sync();
+      if (!rank_barrier(rs, 2)) return;
+    }
+    const double* xch_me = reinterpret_cast<const double*>(s_base[me] + group_area(rs.group));
+    for (SegIter it(a.segs, a.offs, a.n_tensors, sb + wid, se, wstride); it.valid(); it.next()) {
+      const SegD d = it.get();
+      const int64_t s = it.index();
+      double ratio = 0.0;
+      if (pass == 1) {
+        double P = 0.0, U = 0.0;
+#pragma unroll
+        for (int q = 0; q < Ranks<WT>::kMax; ++q)  // rank order 0..W-1
+          if (Ranks<WT>::has(q, W)) {
+            P += __ldcg(xch_me + (int64_t(q) * a.n_tensors + d.tensor) * 2);
+            U += __ldcg(xch_me + (int64_t(q) * a.n_tensors + d.tensor) * 2 + 1);
+          }
+        ratio = trust_ratio(P, U, k);
+      }
+      const int64_t q0 = d.toff >> 2, q1 = (d.toff + d.len + 3) >> 2;
+      double sp = 0.0, su = 0.0;
+      for (int64_t q = q0 + lane; q < q1; q += 32) {
+        float g[Ranks<WT>::kMax][4], mm[4], vv[4], pp[4];
+        const int64_t e0 = q << 2;
+        const int64_t si = d.sidx + (e0 - d.toff);
+        ring_load4<G, COCONET_SUM, WT>(s_base, d.aoff + e0 * int64_t(sizeof(G)), me, W, g);
+        ld4(m + si, mm);
+        ld4(v + si, vv);
+        ld4(reinterpret_cast<const float*>(pme + d.boff) + e0, pp);
+        int lo, hi;
+        quad_range(d, e0, lo, hi);
+        float gs[4];
+        ring_fold4<COCONET_SUM, WT>(g, W, gs);
+        float pn[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          double mn, vn;
+          const double u = lamb_u_exact(gs[i], mm[i], vv[i], pp[i], k, mn, vn);
+          if (pass == 0) {
+            if (i >= lo && i < hi) {
+              sp = __dadd_rn(sp, __dmul_rn(double(pp[i]), double(pp[i])));
+              su = __dadd_rn(su, __dmul_rn(u, u));
+            }
+          } else {
+            mm[i] = float(mn);
+            vv[i] = float(vn);
+            pn[i] = float(__dsub_rn(double(pp[i]), __dmul_rn(ratio, u)));
+          }
+        }
+        if (pass == 1) {
+          st4m(m + si, mm, lo, hi);
+          st4m(v + si, vv, lo, hi);
+#pragma unroll
+          for (int j = 0; j < Ranks<WT>::kMax; ++j)  // AllGather push
+            if (Ranks<WT>::has(j, W)) st4m(reinterpret_cast<float*>(s_base[j] + d.boff) + e0, pn, lo, hi);
+        }
+      }
+      if (pass == 0) {
+        sp = warp_sum(sp);
+        su = warp_sum(su);
+        if (lane == 0) {
+          k.seg_part[2 * s] = sp;
+          k.seg_part[2 * s + 1] = su;
         }
       }
     }
@@ -692,6 +843,9 @@ __global__ void __launch_bounds__((NW + 1) * 32, 2) lamb_tma_kernel(OptArgs a, L
   for (int pass = 0; pass < 2; ++pass) {
     if (pass == 1) {
       // ---- between the passes: per-tensor partials -> exchange -> totals (GRID)
+      // Pass 1 wrote m, v with generic stores; pass 2's producer reads them
+      // with cp.async.bulk (the async proxy): order the two proxies first.
+      asm volatile("fence.proxy.async.global;" ::: "memory");
       __threadfence();
       cg::this_grid().sync();
       const int64_t xch_off = int64_t(group_area(rs.group));
@@ -745,7 +899,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, 2) lamb_tma_kernel(OptArgs a, L
               P += __ldcg(xch_me + (int64_t(q) * a.n_tensors + tens) * 2);
               U += __ldcg(xch_me + (int64_t(q) * a.n_tensors + tens) * 2 + 1);
             }
-          ratio = float((k.lr * sqrt(P)) / sqrt(U));
+          ratio = float(trust_ratio(P, U, k));
         }
         float sp = 0.f, su = 0.f;
         for (int64_t qa = q0; qa < q1; qa += kTmaChunkQ) {
@@ -1218,7 +1372,7 @@ __global__ void __launch_bounds__(NT, 512 / NT) lamb_stream_kernel(OptArgs a, La
             P += xs[q].x;
             Uu += xs[q].y;
           }
-        const float ratio = float((k.lr * sqrt(P)) / sqrt(Uu));
+        const float ratio = float(trust_ratio(P, Uu, k));
 #pragma unroll
         for (int u = 0; u < U; ++u) {
           const int64_t q = qc + tid + NT * u;
@@ -1354,6 +1508,17 @@ const void* lamb_pick(int W) {
 }
 
 template <typename G>
+const void* lamb_exact_pick(int W) {
+  switch (W) {
+    case 1: return reinterpret_cast<const void*>(&lamb_exact_kernel<G, 1>);
+    case 2: return reinterpret_cast<const void*>(&lamb_exact_kernel<G, 2>);
+    case 4: return reinterpret_cast<const void*>(&lamb_exact_kernel<G, 4>);
+    case 8: return reinterpret_cast<const void*>(&lamb_exact_kernel<G, 8>);
+    default: return reinterpret_cast<const void*>(&lamb_exact_kernel<G, 0>);
+  }
+}
+
+template <typename G>
 const void* lamb_stream_pick(int W) {
   switch (W) {
     case 1: return reinterpret_cast<const void*>(&lamb_stream_kernel<G, 1, 64, 4>);
@@ -1485,10 +1650,8 @@ int coconet_fused_rs_lamb_ag(coconet_ctx_t c, coconet_tlist_t tl, const void* co
                              const coconet_lamb_params* hp, void* stream_) {
   if (!c || !tl || !g || !p || !hp) return set_error(COCONET_ERR_INVALID_INPUT, "null argument");
   if (tl->ctx != c) return set_error(COCONET_ERR_INVALID_INPUT, "tensor list belongs to another context");
-  if (hp->math != COCONET_MATH_FAST)
-    return set_error(COCONET_ERR_UNSUPPORTED,
-                     "LAMB runs in FAST math only: its whole-tensor sums cannot reproduce the "
-                     "reference's sequential double accumulation bit-for-bit");
+  if (hp->math != COCONET_MATH_FAST && hp->math != COCONET_MATH_EXACT)
+    return set_error(COCONET_ERR_INVALID_INPUT, "bad math");
   if (hp->sched < COCONET_LAMB_AUTO || hp->sched > COCONET_LAMB_TMA)
     return set_error(COCONET_ERR_INVALID_INPUT, "bad LAMB schedule");
   // exchange [rank][tensor] (P, U) doubles + ready flags [rank][tensor]
@@ -1511,6 +1674,15 @@ int coconet_fused_rs_lamb_ag(coconet_ctx_t c, coconet_tlist_t tl, const void* co
   k.frbc2 = float(1.0 / (1.0 - std::pow(double(hp->beta2), double(hp->t))));
   k.feps = hp->eps;
   k.fwd = hp->wd;
+  k.b1 = double(hp->beta1);
+  k.b2 = double(hp->beta2);
+  k.c1 = 1.0 - k.b1;
+  k.c2 = 1.0 - k.b2;
+  k.bc1 = 1.0 - std::pow(k.b1, double(hp->t));
+  k.bc2 = 1.0 - std::pow(k.b2, double(hp->t));
+  k.eps = double(hp->eps);
+  k.wd = double(hp->wd);
+  k.guard = hp->trust_guard ? 1 : 0;
   k.csr_ptr = tl->d_csr_ptr;
   k.csr_idx = tl->d_csr_idx;
   k.seg_part = tl->d_seg_part;
@@ -1523,6 +1695,13 @@ int coconet_fused_rs_lamb_ag(coconet_ctx_t c, coconet_tlist_t tl, const void* co
   // AUTO: the TMA ring with buckets of >= kTmaMinBucket elements at W = 1,
   // >= 4x that across ranks (BERT-336M, W = 2/8 virtual: TMA wins at 16384,
   // GRID at 4096; profiles/r01_lamb_w_probe.json), GRID otherwise
+  if (hp->math == COCONET_MATH_EXACT) {  // one schedule: the read-only pass 1 of lamb_exact_kernel
+    const void* fn = g_elem == COCONET_F32   ? lamb_exact_pick<float>(W)
+                     : g_elem == COCONET_F16 ? lamb_exact_pick<__half>(W)
+                                             : lamb_exact_pick<__nv_bfloat16>(W);
+    void* args[] = {&a, &k};
+    return launch_opt(c, tl, fn, args, false, stream);
+  }
   const bool tma_auto = tl->bucket_cap >= (W == 1 ? kTmaMinBucket : 4 * kTmaMinBucket);
   const int sched = hp->sched == COCONET_LAMB_AUTO ? (tma_auto ? COCONET_LAMB_TMA : COCONET_LAMB_GRID) : hp->sched;
   if (sched == COCONET_LAMB_TMA) {

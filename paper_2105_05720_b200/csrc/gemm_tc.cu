@@ -375,7 +375,7 @@ __device__ void mp_comm_warp(const OvArgs& a, char* const* base, int lane) {
     int u = 0;
     if (lane == 0) u = int(atomicAdd(ticket, 1u) - a.ticket_base);
     u = __shfl_sync(full, u, 0);
-    if (u >= a.n_units) break;
+    if (u < 0 || u >= a.n_units) break;  // u < 0: the ticket counter is behind ticket_base
     const int mt = u / (a.nl * 4);
     const int rem = u - mt * a.nl * 4;
     const int lr = rem >> 2, rg = rem & 3;
@@ -898,15 +898,13 @@ int coconet_mm_overlap_fused_ar(coconet_ctx_t c, int group, const void* a, const
   const int W = c->groups[size_t(group)].size;
   if (cols % W) return set_error(COCONET_ERR_DIVISIBILITY, "column extent does not divide over the group");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  // Schedule: with every rank on this GPU (VIRTUAL) there is no link to hide
-  // the GEMM behind - both halves contend for the same HBM and SM memory pipe
-  // and the one-kernel overlap measures slower than GEMM then the fused
-  // all-reduce - so VIRTUAL runs the two kernels back to back
-  // (bitwise the same result); DISTRIBUTED (NVLink-bound comm) runs the fused
-  // kernel. COCONET_MP_OVERLAP=fused|sequential forces either.
+  // Schedule: on one GPU the one-kernel overlap measures slower than GEMM
+  // then the fused all-reduce (both halves contend for the same HBM and SM
+  // memory pipe), and it has not been measured over NVLink
+  // yet, so AUTO runs the two kernels back to back (bitwise the same result)
+  // in both modes. COCONET_MP_OVERLAP=fused|sequential forces either.
   const char* ov_env = getenv("COCONET_MP_OVERLAP");
-  const bool sequential = ov_env ? std::strcmp(ov_env, "sequential") == 0
-                                 : (c->mode == COCONET_MODE_VIRTUAL && W > 1);
+  const bool sequential = ov_env ? std::strcmp(ov_env, "sequential") == 0 : W > 1;
   if (sequential) {
     int rc = coconet_matmul(c, group, a, w, partial, in_elem, in_elem, rows, cols, k_local, COCONET_MATH_FAST, stream);
     if (rc) return rc;
@@ -948,17 +946,25 @@ int coconet_mm_overlap_fused_ar(coconet_ctx_t c, int group, const void* a, const
   o.thresh = th <= 0 ? 0 : uint64_t(th);
   o.math = hp->math;
   // every owner's units each add one arrival to every rank's counter
-  c->mp_arrivals[group] += uint32_t(p.g.tiles_m) * 4u * uint32_t(W);
-  o.arrive_target = c->mp_arrivals[group];
+  const uint32_t arrivals = c->mp_arrivals[group] + uint32_t(p.g.tiles_m) * 4u * uint32_t(W);
+  o.arrive_target = arrivals;
   // tickets drawn this call: one per unit, plus the one failing draw with
-  // which each of the grid's warps (sm_count CTAs x kFusedWarps) leaves the loop
+  // which each of the grid's warps (sm_count CTAs - launch_tc's cooperative
+  // grid - x kFusedWarps) leaves the loop
   o.ticket_base = c->mp_tickets[group];
-  c->mp_tickets[group] += uint32_t(o.n_units) + uint32_t(c->sm_count) * uint32_t(kFusedWarps);
+  const uint32_t tickets = o.ticket_base + uint32_t(o.n_units) + uint32_t(c->sm_count) * uint32_t(kFusedWarps);
   for (int i = 0; i < p.g.ranks; ++i)
     p.g.flags[i] = reinterpret_cast<uint32_t*>(p.g.c[i] - o.part_off + o.flag_off);
   p.g.epoch = o.rs.epoch;
   p.g.local_peers = c->mode == COCONET_MODE_VIRTUAL ? 1 : 0;
-  return launch_tc<true>(c, &p, in_elem, in_elem, &o, s);
+  rc = launch_tc<true>(c, &p, in_elem, in_elem, &o, s);
+  // the host mirrors of the device counters advance only with a launch that
+  // happened, so a failed launch cannot leave them ahead of the device
+  if (rc == COCONET_OK) {
+    c->mp_arrivals[group] = arrivals;
+    c->mp_tickets[group] = tickets;
+  }
+  return rc;
 }
 
 }  // extern "C"

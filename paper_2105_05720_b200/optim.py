@@ -22,7 +22,11 @@ from .runtime import Context
 
 
 def _rehome(ctx: Context, params, grad_dtype):
-    """Moves each parameter's storage and a zeroed .grad into the heap."""
+    """Moves each parameter's storage into the heap. With fp32 grads the .grad
+    is a heap view too (backward writes what the kernel pulls); autograd only
+    produces grads of the parameter's dtype, so for a 16-bit grad_dtype .grad
+    stays an ordinary fp32 tensor and `_stage_grads` casts it into the 16-bit
+    heap buffer before each fused launch."""
     pbufs, gbufs = [], []
     rank = None if ctx.mode == "distributed" else 0
     for p in params:
@@ -33,7 +37,7 @@ def _rehome(ctx: Context, params, grad_dtype):
         p.data = view
         g = ctx.view(gb, rank)
         g.zero_()
-        p.grad = g
+        p.grad = g if grad_dtype == torch.float32 else torch.zeros_like(view)
         pbufs.append(pb)
         gbufs.append(gb)
     return pbufs, gbufs
@@ -49,6 +53,9 @@ class _FusedBase(torch.optim.Optimizer):
         for p in self.plist:
             if p.dtype != torch.float32:
                 raise ValueError("master weights must be fp32")
+        if grad_dtype not in (torch.float32, torch.float16, torch.bfloat16):
+            raise ValueError("grad_dtype must be float32, float16 or bfloat16")
+        self.grad_dtype = grad_dtype
         self.pbufs, self.gbufs = _rehome(ctx, self.plist, grad_dtype)
         self.tl = TensorList(ctx, [p.numel() for p in self.plist], bucket_cap=bucket_cap)
         self.m = ctx.alloc([self.tl.shard_elems], torch.float32)
@@ -59,9 +66,18 @@ class _FusedBase(torch.optim.Optimizer):
         self.t = 0
 
     def zero_grad(self, set_to_none: bool = False):
-        # the grads are heap views the kernels read: keep them, zero in place
+        # the grads are heap views the kernels read (or their fp32 staging
+        # tensors): keep them, zero in place
         for p in self.plist:
             p.grad.zero_()
+
+    def _stage_grads(self):
+        """16-bit grad_dtype: cast each fp32 .grad into its heap buffer."""
+        if self.grad_dtype == torch.float32:
+            return
+        rank = None if self.ctx.mode == "distributed" else 0
+        for p, gb in zip(self.plist, self.gbufs):
+            self.ctx.view(gb, rank).copy_(p.grad)
 
 
 class FusedAdam(_FusedBase):
@@ -80,6 +96,7 @@ class FusedAdam(_FusedBase):
         self.t += 1
         hp = AdamHParams(lr=g["lr"], beta1=g["betas"][0], beta2=g["betas"][1], t=float(self.t), eps=g["eps"],
                          cv_beta1=False, math=self.math, algo=_lib.ALGO_TWO_SHOT)
+        self._stage_grads()
         fused_rs_adam_ag(self.ctx, self.tl, self.gbufs, self.pbufs, self.m, self.v, hp)
         return loss
 
@@ -97,7 +114,10 @@ class FusedLAMB(_FusedBase):
         loss = closure() if closure is not None else None
         g = self.param_groups[0]
         self.t += 1
+        # trust_guard: a zero-norm tensor (e.g. a zero-initialised bias) steps
+        # with ratio = lr instead of freezing or turning NaN (apex / NVLAMB)
         hp = LambHParams(lr=g["lr"], beta1=g["betas"][0], beta2=g["betas"][1], t=float(self.t), eps=g["eps"],
-                         wd=g["weight_decay"])
+                         wd=g["weight_decay"], trust_guard=True)
+        self._stage_grads()
         fused_rs_lamb_ag(self.ctx, self.tl, self.gbufs, self.pbufs, self.m, self.v, hp)
         return loss

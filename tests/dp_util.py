@@ -19,6 +19,14 @@ from paper_2105_05720_b200.runtime import Context
 GOLD = Path(__file__).resolve().parent / "golden"
 
 
+GOLD_DIR = GOLD
+
+
+def golden_lamb_list(W: int) -> dict:
+    """tests/golden/lamb_list_cases.json (oracle/make_lamb_golden.py)."""
+    return next(r for r in json.loads((GOLD / "lamb_list_cases.json").read_text()) if r["W"] == W)
+
+
 def golden(name: str) -> dict:
     for f in GOLD.glob("*_cases.json"):
         for rec in json.loads(f.read_text()):

@@ -287,8 +287,12 @@ def _run_mp(ctx, ranks, world, rows, H, fused):
     if ctx.mode == "distributed":
         dist.barrier()
     hp = BdrHParams(0.1, 1, 11617925594314093840, _lib.MATH_FAST)
-    if fused:
-        mm_overlap_fused_ar(ctx, xb, wb, bb, rb, part, out, hp)
+    if fused:  # force the one-kernel overlap (AUTO runs the pair back to back)
+        os.environ["COCONET_MP_OVERLAP"] = "fused"
+        try:
+            mm_overlap_fused_ar(ctx, xb, wb, bb, rb, part, out, hp)
+        finally:
+            os.environ.pop("COCONET_MP_OVERLAP", None)
     else:
         matmul(ctx, xb, wb, part, math=_lib.MATH_FAST)
         fused_rs_bdr_ag(ctx, part, bb, rb, out, hp)

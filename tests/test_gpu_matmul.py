@@ -80,7 +80,8 @@ def test_mm_overlap_matches_sequential(W, rows, H, mode, monkeypatch):
     bit-identical output to running the same two kernels back to back
     (Overlap.OutputBitIdenticalToSequential, test_overlap.cpp:35-43), and is
     within 1e-2 of the fp32 reference for bf16 activations. mode=fused forces
-    the one-kernel overlap (VIRTUAL mode's AUTO runs the pair back to back)."""
+    the one-kernel overlap (AUTO runs the pair back to back until the overlap is
+    measured over NVLink)."""
     if mode == "fused":
         monkeypatch.setenv("COCONET_MP_OVERLAP", "fused")
     else:

@@ -194,3 +194,36 @@ def test_digest_is_fnv_over_sorted_keys():
         h = co.fnv1a(k, h)
         h = co.fnv1a(res[k][0].tobytes(), h)
     assert co.digest_results(res) == h
+
+
+# ---- per-tensor LAMB over a tensor list (oracle/make_lamb_golden.py) -------
+
+def _lamb_list_cases():
+    return json.loads((GOLD / "lamb_list_cases.json").read_text())
+
+
+@pytest.mark.parametrize("rec", _lamb_list_cases(), ids=lambda r: r["name"])
+def test_lamb_list_restated_equals_reference_engine(rec):
+    """The restated LAMB (co.lamb_oracle per tensor, on each tensor's own
+    ring-order RS) reproduces the reference Engine's per-tensor fused LAMB
+    programs bit for bit on every tensor of the list (p, m, v), W = 1..8; the
+    Engine itself is within 1e-6 of the reference oracle on the base program."""
+    from oracle.make_lamb_golden import restated
+    arrs = np.load(GOLD / "lamb_list_results.npz")
+    W = rec["W"]
+    assert rec["deviation_sched_vs_oracle"] <= 1e-6
+    rest = restated(rec["counts"], W, rec["seed"])
+    for i in range(len(rec["counts"])):
+        for name, j in (("p", 0), ("m", 1), ("v", 2)):
+            assert np.array_equal(rest[i][j], arrs[f"W{W}_{name}{i}"]), (name, i)
+
+
+@needs_ref
+def test_lamb_list_golden_regenerates():
+    """The committed per-tensor LAMB fixture is what the reference computes."""
+    from oracle.make_lamb_golden import COUNTS, base_program, fused_program
+    rec = next(r for r in _lamb_list_cases() if r["W"] == 4)
+    s = ref.RefSession(base_program(COUNTS), None, {"W": 4}, sched_program=fused_program(COUNTS))
+    s.gen(1)
+    s.run(1, ref.ENGINE_SCHED)
+    assert "%016x" % s.digest(ref.ENGINE_SCHED) == rec["engine_sched_digest"]
