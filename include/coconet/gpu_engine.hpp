@@ -9,19 +9,29 @@
 // plan step becomes one (fused) kernel launch instead of per-element CPU loops.
 //
 // Lowering of plan steps (EXACT math reproduces the reference Engine's digest
-// bit for bit; FAST trades that for fp32 element math):
+// bit for bit; FAST trades that for fp32 element math and bf16 tensor cores):
 //   FusedAllReduce  Adam expression   -> coconet_fused_rs_adam_ag   (one kernel)
-//                   LAMB expression   -> coconet_fused_rs_lamb_ag   (FAST only)
+//                   LAMB expression   -> coconet_fused_rs_lamb_ag   (one kernel,
+//                                        in-kernel per-tensor norm exchange)
 //                   dropout(x+b)+r    -> coconet_fused_rs_bdr_ag    (one kernel)
 //                   anything else     -> reduce_scatter + pointwise + all_gather
 //   AllReduce                         -> coconet_allreduce (flat ring chunks)
 //   ReduceScatter / AllGather(+gather)-> coconet_reduce_scatter / coconet_all_gather
-//   MatMul                            -> coconet_matmul
+//   MatMul          EXACT             -> coconet_matmul (fp64 k-order, bit-exact)
+//                   FAST              -> bf16 staging + coconet_matmul on tcgen05
 //   Pointwise                         -> coconet_pointwise (+ ReduceTensor pre-pass)
-//   Send / FusedSend / Recv           -> pointwise on the source stage + peer copy
+//   Send / FusedSend / Recv           -> pointwise on the source stage + coconet_send
 //   OverlapGroup {RS, FusedSend, AG}  -> coconet_rs_fused_send_ag   (one kernel)
+//   OverlapGroup {MatMul, FusedAR}    -> FAST: coconet_mm_overlap_fused_ar
+//                                        (tcgen05 GEMM + RS-bias-dropout-residual-AG)
 //   OverlapGroup (other)              -> members in order
 //   Reduce / Broadcast                -> coconet_reduce / coconet_broadcast
+// Two execution modes (GpuOptions::comm): VIRTUAL runs every rank of the
+// program in this process on one device (the reference's in-process rank
+// model); DISTRIBUTED runs ONE rank per process (one process per GPU, peers
+// mapped over NVLink), the caller supplying a world all-gather for the
+// bootstrap, the cross-rank ReduceTensor partials and the result assembly:
+// every process returns the same RunReport (runtime.hpp:101-138).
 // Counters (comm_bytes, intergroup_bytes, traffic_saved_bytes, kernel_steps,
 // memory_elems) follow the reference's accounting exactly; simulated_time is
 // the reference's own cost model (Engine::step_time); device_ms is measured.
@@ -48,9 +58,19 @@
 
 namespace coconet {
 
+// DISTRIBUTED mode: this process is world rank `rank` of `world`; allgather is
+// a collective over the program's world in rank order (every process passes
+// `bytes` bytes in, receives world * bytes).
+struct GpuComm {
+  int rank = -1;  // -1: VIRTUAL (every rank in this process)
+  int world = 0;
+  std::function<void(const void* in, size_t bytes, void* out)> allgather;
+};
+
 struct GpuOptions {
   int device = 0;
   int math = COCONET_MATH_EXACT;
+  GpuComm comm;
   bool fused_kernels = true;  // false: generic lowering only (for A/B checks)
   // run the plan once untimed first (then restore the inputs), so device_ms
   // covers the kernels only: no bucket-table builds, allocations, occupancy
@@ -104,6 +124,10 @@ class GpuEngine {
     cudaEvent_t e0, e1;
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
+    if (dist()) {  // host barrier: every rank starts its timed plan together
+      cudaStreamSynchronize(stream_);
+      gather_double(0.0);
+    }
     auto t0 = std::chrono::steady_clock::now();
     cudaEventRecord(e0, stream_);
     for (size_t i = 0; i < pl.steps.size(); ++i) {
@@ -126,6 +150,10 @@ class GpuEngine {
     float ms = 0;
     cudaEventElapsedTime(&ms, e0, e1);
     device_ms_ = ms;
+    if (dist()) {  // the job's time: max over ranks
+      const std::vector<double> all = gather_double(ms);
+      device_ms_ = *std::max_element(all.begin(), all.end());
+    }
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
     rep.simulated_time = clock;
@@ -138,6 +166,7 @@ class GpuEngine {
   }
 
   double device_ms() const { return device_ms_; }
+  bool distributed() const { return dist(); }
   const std::vector<std::string>& lowering() const { return lowering_; }
   uint64_t launches() const { return ctx_ ? coconet_launch_count(ctx_) : 0; }
 
@@ -169,6 +198,27 @@ class GpuEngine {
   // ---- memory
   const ccopt::ProcessGroup& group_of(int gid) const { return *p_.find_group(gid); }
 
+  // ---- ranks this process executes
+  bool dist() const { return opt_.comm.rank >= 0; }
+  // group rank r of gid lives in this process
+  bool mine(int gid, int r) const { return !dist() || group_of(gid).first_rank + r == opt_.comm.rank; }
+  bool member(int gid) const {
+    if (!dist()) return true;
+    const ccopt::ProcessGroup& g = group_of(gid);
+    return opt_.comm.rank >= g.first_rank && opt_.comm.rank < g.first_rank + g.world_size;
+  }
+  std::vector<int> my_ranks(int gid) const {
+    std::vector<int> rs;
+    for (int r = 0; r < group_of(gid).world_size; ++r)
+      if (mine(gid, r)) rs.push_back(r);
+    return rs;
+  }
+  std::vector<double> gather_double(double x) const {
+    std::vector<double> all(size_t(opt_.comm.world));
+    opt_.comm.allgather(&x, sizeof(double), all.data());
+    return all;
+  }
+
   int cgroup(int gid) {
     auto it = cgroups_.find(gid);
     if (it != cgroups_.end()) return it->second;
@@ -199,7 +249,21 @@ class GpuEngine {
       if (n.kind != OpKind::OverlapGroup)
         need += bytes_for(n.out_shape, n.out_layout, group_of(n.group).world_size) * 4 +
                 bytes_for(n.out_shape, Layout::replicated(), group_of(n.group).world_size) * 2;
-    ck(coconet_init(&ctx_, COCONET_MODE_VIRTUAL, 0, p_.world_size(), opt_.device, need));
+    if (dist()) {
+      if (opt_.comm.world != p_.world_size() || !opt_.comm.allgather)
+        throw Error(ErrCode::NoSuchRank, "DISTRIBUTED GpuEngine needs world == the program's world and an allgather");
+      cudaSetDevice(opt_.device);
+      ck(coconet_init(&ctx_, COCONET_MODE_DISTRIBUTED, opt_.comm.rank, p_.world_size(), opt_.device, need));
+      // bootstrap: every rank's heap handle to every rank (coconet_cuda.h)
+      std::vector<char> h(256);
+      size_t len = h.size();
+      ck(coconet_heap_handle(ctx_, h.data(), &len));
+      std::vector<char> all(len * size_t(opt_.comm.world));
+      opt_.comm.allgather(h.data(), len, all.data());
+      ck(coconet_open_peers(ctx_, all.data(), len));
+    } else {
+      ck(coconet_init(&ctx_, COCONET_MODE_VIRTUAL, 0, p_.world_size(), opt_.device, need));
+    }
     cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking);
     for (auto& g : p_.groups) cgroup(g.group_id);
     for (auto& d : p_.decls) vals_[d.name] = alloc_val(d.shape, d.layout, d.group);
@@ -221,16 +285,18 @@ class GpuEngine {
     const int wr = group_of(v.group).first_rank + group_rank;
     return static_cast<float*>(coconet_symm_ptr(ctx_, wr, v.off));
   }
-  // pointer passed to collective entry points: the same offset, rank 0's heap
-  void* sym(const DVal& v) const { return coconet_symm_ptr(ctx_, 0, v.off); }
+  // pointer passed to collective entry points: the same offset in the
+  // caller's heap (VIRTUAL: rank 0's; DISTRIBUTED: this process's rank)
+  void* sym(const DVal& v) const { return coconet_symm_ptr(ctx_, dist() ? opt_.comm.rank : 0, v.off); }
 
   void upload(const ccopt::ValueMap& in) {
     for (auto& d : p_.decls) {
       const ccopt::TensorVal& t = in.at(d.name);
       const DVal& v = vals_.at(d.name);
       for (size_t r = 0; r < t.per_rank.size(); ++r)
-        cudaMemcpyAsync(dptr(v, int(r)), t.per_rank[r].data(), t.per_rank[r].size() * sizeof(float),
-                        cudaMemcpyHostToDevice, stream_);
+        if (mine(v.group, int(r)))
+          cudaMemcpyAsync(dptr(v, int(r)), t.per_rank[r].data(), t.per_rank[r].size() * sizeof(float),
+                          cudaMemcpyHostToDevice, stream_);
     }
     cudaStreamSynchronize(stream_);
     host_in_ = &in;
@@ -246,11 +312,38 @@ class GpuEngine {
       const DVal& v = value(ValueRef{p_.find_node(id) != nullptr, id});
       TensorVal t = TensorVal::make(v.view.global, v.view.layout, v.group, v.view.world);
       for (int r = 0; r < v.view.world; ++r)
-        cudaMemcpyAsync(t.per_rank[size_t(r)].data(), dptr(v, r), t.per_rank[size_t(r)].size() * sizeof(float),
-                        cudaMemcpyDeviceToHost, stream_);
+        if (mine(v.group, r))
+          cudaMemcpyAsync(t.per_rank[size_t(r)].data(), dptr(v, r), t.per_rank[size_t(r)].size() * sizeof(float),
+                          cudaMemcpyDeviceToHost, stream_);
       out[id] = std::move(t);
     }
     cudaStreamSynchronize(stream_);
+    if (dist()) {
+      // every process contributes one buffer laid out as [value][group rank]
+      // (its own slots filled, the rest zero); slot (value, r) is taken from
+      // the process that owns group rank r
+      size_t total = 0;
+      for (auto& [id, t] : out)
+        for (auto& pr : t.per_rank) total += pr.size();
+      std::vector<float> mine_buf(std::max<size_t>(1, total), 0.f);
+      size_t pos = 0;
+      for (auto& [id, t] : out)
+        for (int r = 0; r < int(t.per_rank.size()); ++r) {
+          if (mine(t.group, r)) std::copy(t.per_rank[size_t(r)].begin(), t.per_rank[size_t(r)].end(), mine_buf.begin() + long(pos));
+          pos += t.per_rank[size_t(r)].size();
+        }
+      std::vector<float> all(mine_buf.size() * size_t(opt_.comm.world));
+      opt_.comm.allgather(mine_buf.data(), mine_buf.size() * sizeof(float), all.data());
+      pos = 0;
+      for (auto& [id, t] : out)
+        for (int r = 0; r < int(t.per_rank.size()); ++r) {
+          const size_t src = size_t(group_of(t.group).first_rank + r);
+          auto& pr = t.per_rank[size_t(r)];
+          std::copy(all.begin() + long(src * mine_buf.size() + pos),
+                    all.begin() + long(src * mine_buf.size() + pos + pr.size()), pr.begin());
+          pos += pr.size();
+        }
+    }
     return out;
   }
 
@@ -298,7 +391,7 @@ class GpuEngine {
       case OpKind::MatMul: exec_matmul(n); break;
       case OpKind::Pointwise: {
         DVal& out = node_out(n, n.out_layout);
-        pointwise(n, n.expr, n.inputs, out, n.group, n.out_layout, {});
+        pointwise(n, n.expr, n.inputs, out, n.group, n.out_layout, {});  // member-guarded inside
         lowering_.push_back(n.id + ":pointwise");
         break;
       }
@@ -306,10 +399,12 @@ class GpuEngine {
         const DVal& x = value(n.inputs[0]);
         DVal& out = node_out(n, n.out_layout);
         const int64_t total = num_elems(x.view.global);
-        coconet_tlist_t tl = tlist(n.group, {total});
-        const void* xs[1] = {sym(x)};
-        void* os[1] = {sym(out)};
-        ck(coconet_allreduce(ctx_, tl, xs, os, COCONET_F32, int(n.reducer), COCONET_ALGO_TWO_SHOT, stream_));
+        if (member(n.group)) {
+          coconet_tlist_t tl = tlist(n.group, {total});
+          const void* xs[1] = {sym(x)};
+          void* os[1] = {sym(out)};
+          ck(coconet_allreduce(ctx_, tl, xs, os, COCONET_F32, int(n.reducer), COCONET_ALGO_TWO_SHOT, stream_));
+        }
         count_ring(n.group, flat_elems(total, G), input_bw(n), true, true);
         lowering_.push_back(n.id + ":allreduce");
         break;
@@ -318,8 +413,9 @@ class GpuEngine {
         const DVal& x = value(n.inputs[0]);
         DVal& out = node_out(n, n.out_layout);
         const int axis = n.out_layout.dim;
-        ck(coconet_reduce_scatter(ctx_, cgroup(n.group), sym(x), sym(out), COCONET_F32, int(n.reducer),
-                                  int(n.out_shape.size()), n.out_shape.data(), axis, stream_));
+        if (member(n.group))
+          ck(coconet_reduce_scatter(ctx_, cgroup(n.group), sym(x), sym(out), COCONET_F32, int(n.reducer),
+                                    int(n.out_shape.size()), n.out_shape.data(), axis, stream_));
         count_ring(n.group, axis_elems(n.out_shape, axis, G), input_bw(n), true, false);
         lowering_.push_back(n.id + ":reduce_scatter");
         break;
@@ -334,8 +430,9 @@ class GpuEngine {
         const DVal& x = value(n.inputs[0]);
         DVal& out = node_out(n, n.out_layout);
         const int64_t total = num_elems(x.view.global);
-        ck(coconet_reduce(ctx_, cgroup(n.group), sym(x), sym(out), COCONET_F32, int(n.reducer), total, n.root,
-                          stream_));
+        if (member(n.group))
+          ck(coconet_reduce(ctx_, cgroup(n.group), sym(x), sym(out), COCONET_F32, int(n.reducer), total, n.root,
+                            stream_));
         // the reference's fold loop starts at rank 1 and counts inside it, so
         // rank 0 is never counted (runtime.hpp:420-424); mirrored as is
         for (int r = 1; r < G; ++r)
@@ -347,7 +444,8 @@ class GpuEngine {
         const DVal& x = value(n.inputs[0]);
         DVal& out = node_out(n, n.out_layout);
         const int64_t total = num_elems(x.view.global);
-        ck(coconet_broadcast(ctx_, cgroup(n.group), sym(x), sym(out), COCONET_F32, total, n.root, stream_));
+        if (member(n.group))
+          ck(coconet_broadcast(ctx_, cgroup(n.group), sym(x), sym(out), COCONET_F32, total, n.root, stream_));
         count(n.group, n.root, int64_t(G - 1) * total * input_bw(n));
         lowering_.push_back(n.id + ":broadcast");
         break;
@@ -367,18 +465,54 @@ class GpuEngine {
     return tl;
   }
 
+  struct MmShape {
+    int64_t rows, M, kl;
+  };
+  MmShape mm_shape(const ccopt::OpNode& n) const {
+    const DVal& x = value(n.inputs[0]);
+    const DVal& w = value(n.inputs[1]);
+    const ccopt::Shape& xs = x.view.global;
+    const int64_t K = xs.back();
+    const int G = group_of(n.group).world_size;
+    const bool contracted_sliced = x.view.layout.is_sliced() && x.view.layout.dim == int(xs.size()) - 1;
+    return MmShape{ccopt::num_elems(xs) / K, w.view.global[1], contracted_sliced ? K / G : K};
+  }
+  // tcgen05 tile constraints (coconet_matmul FAST): M % 128, K % 64, N % 128 or 192
+  static bool tc_shape(const MmShape& s) {
+    return s.rows % 128 == 0 && s.kl % 64 == 0 && (s.M % 128 == 0 || s.M % 192 == 0);
+  }
+  // bf16 copy of an fp32-stored value in a scratch symmetric buffer (the
+  // reference stores every decl as fp32; tcgen05 takes 16-bit)
+  DVal stage16(const DVal& v, const std::string& key) {
+    auto it = vals_.find(key);
+    if (it == vals_.end()) {
+      DVal s = v;
+      size_t off = 0;
+      ck(coconet_symm_alloc(ctx_, size_t(std::max<int64_t>(1, v.local)) * 2 + 256, &off));
+      s.off = off;
+      it = vals_.emplace(key, s).first;
+    }
+    for (int r : my_ranks(v.group))
+      ck(coconet_convert(ctx_, dptr(v, r), COCONET_F32, dptr(it->second, r), COCONET_BF16, v.local, stream_));
+    return it->second;
+  }
+
   void exec_matmul(const ccopt::OpNode& n) {
     using namespace ccopt;
     const DVal& x = value(n.inputs[0]);
     const DVal& w = value(n.inputs[1]);
     DVal& out = node_out(n, n.out_layout);
-    const Shape& xs = x.view.global;
-    const int64_t K = xs.back(), M = w.view.global[1], rows = num_elems(xs) / K;
-    const int G = group_of(n.group).world_size;
-    const bool contracted_sliced = x.view.layout.is_sliced() && x.view.layout.dim == int(xs.size()) - 1;
-    const int64_t kl = contracted_sliced ? K / G : K;
-    ck(coconet_matmul(ctx_, cgroup(n.group), sym(x), sym(w), sym(out), COCONET_F32, COCONET_F32, rows, M, kl,
-                      COCONET_MATH_EXACT, stream_));
+    const MmShape sh = mm_shape(n);
+    if (!member(n.group)) return;
+    if (opt_.math == COCONET_MATH_FAST && tc_shape(sh)) {
+      const DVal xb = stage16(x, "#bf16:" + n.id + ":a"), wb = stage16(w, "#bf16:" + n.id + ":b");
+      ck(coconet_matmul(ctx_, cgroup(n.group), sym(xb), sym(wb), sym(out), COCONET_BF16, COCONET_F32, sh.rows, sh.M,
+                        sh.kl, COCONET_MATH_FAST, stream_));
+      lowering_.push_back(n.id + ":matmul(tcgen05)");
+      return;
+    }
+    ck(coconet_matmul(ctx_, cgroup(n.group), sym(x), sym(w), sym(out), COCONET_F32, COCONET_F32, sh.rows, sh.M,
+                      sh.kl, COCONET_MATH_EXACT, stream_));
     lowering_.push_back(n.id + ":matmul");
   }
 
@@ -389,8 +523,9 @@ class GpuEngine {
       const DVal& x = value(n.inputs[0]);
       DVal& out = node_out(n, n.out_layout);
       const int axis = x.view.layout.dim;
-      ck(coconet_all_gather(ctx_, cgroup(n.group), sym(x), sym(out), COCONET_F32, int(n.out_shape.size()),
-                            n.out_shape.data(), axis, stream_));
+      if (member(n.group))
+        ck(coconet_all_gather(ctx_, cgroup(n.group), sym(x), sym(out), COCONET_F32, int(n.out_shape.size()),
+                              n.out_shape.data(), axis, stream_));
       count_ring(n.group, axis_elems(n.out_shape, axis, G), input_bw(n), false, true);
       lowering_.push_back(n.id + ":all_gather");
       return;
@@ -408,16 +543,17 @@ class GpuEngine {
     DVal& d = vals_.at(n.gather_decl);
     DVal& out = node_out(n, Layout::replicated());
     const Shape& gs = d.view.global;
-    if (d.view.layout.is_sliced()) {
+    if (!member(n.group)) {
+    } else if (d.view.layout.is_sliced()) {
       ck(coconet_all_gather(ctx_, cgroup(n.group), sym(d), sym(out), COCONET_F32, int(gs.size()), gs.data(),
                             d.view.layout.dim, stream_));
     } else {
-      for (int r = 0; r < G; ++r)
+      for (int r : my_ranks(n.group))
         cudaMemcpyAsync(dptr(out, r), dptr(d, r), size_t(out.local) * sizeof(float), cudaMemcpyDeviceToDevice,
                         stream_);
       ck(coconet_all_gather(ctx_, cgroup(n.group), nullptr, sym(out), COCONET_F32, int(gs.size()), gs.data(),
                             axis, stream_));
-      for (int r = 0; r < G; ++r)
+      for (int r : my_ranks(n.group))
         cudaMemcpyAsync(dptr(d, r), dptr(out, r), size_t(out.local) * sizeof(float), cudaMemcpyDeviceToDevice,
                         stream_);
     }
@@ -442,45 +578,55 @@ class GpuEngine {
     }
     DVal& out = vals_[n.id];
     out = alloc_val(n.out_shape, in_layout, n.group);
-    for (int r = 0; r < src->world_size; ++r) {
-      cudaMemcpyAsync(dptr(out, r), dptr(payload, r), size_t(payload.local) * sizeof(float),
-                      cudaMemcpyDeviceToDevice, stream_);
+    // every rank of both stages takes part (the interval covering them)
+    if (member(src_gid) || member(src_gid + n.group_offset))
+      ck(coconet_send(ctx_, cgroup(src_gid), cgroup(src_gid + n.group_offset), sym(payload), sym(out), COCONET_F32,
+                      payload.local, stream_));
+    for (int r = 0; r < src->world_size; ++r)
       rep_->intergroup_bytes[size_t(src->first_rank + r)] += payload.local * input_bw(n);
-    }
     lowering_.push_back(n.id + (n.kind == OpKind::FusedSend ? ":fused_send" : ":send"));
   }
 
   // ---- FusedAllReduce (runtime.hpp:471-516)
   void exec_fused_allreduce(const ccopt::OpNode& n) {
     using namespace ccopt;
-    const int G = group_of(n.group).world_size;
     const int axis = n.axis >= 0 ? n.axis : int(n.out_shape.size()) - 1;
-    const int bw = input_bw(n);
     const DVal& x = value(n.inputs[0]);
     bool done = false;
-    if (opt_.fused_kernels) done = try_fused_adam(n, axis) || try_fused_bdr(n, axis);
+    if (opt_.fused_kernels) done = try_fused_adam(n, axis) || try_fused_lamb(n, axis) || try_fused_bdr(n, axis);
     if (!done) {
       // generic: RS (axis chunks) -> pointwise on the slice -> AG
       DVal rs = alloc_val(x.view.global, Layout::sliced(axis), n.group);
-      ck(coconet_reduce_scatter(ctx_, cgroup(n.group), sym(x), sym(rs), COCONET_F32, int(n.reducer),
-                                int(x.view.global.size()), x.view.global.data(), axis, stream_));
+      if (member(n.group))
+        ck(coconet_reduce_scatter(ctx_, cgroup(n.group), sym(x), sym(rs), COCONET_F32, int(n.reducer),
+                                  int(x.view.global.size()), x.view.global.data(), axis, stream_));
       std::vector<ValueRef> ins = n.inputs;
       vals_["#rs:" + n.id] = rs;
       ins[0] = ValueRef{true, "#rs:" + n.id};
       DVal sl = alloc_val(n.out_shape, Layout::sliced(axis), n.group);
       pointwise(n, n.expr, ins, sl, n.group, Layout::sliced(axis), {});
       DVal& out = node_out(n, Layout::replicated());
-      ck(coconet_all_gather(ctx_, cgroup(n.group), sym(sl), sym(out), COCONET_F32, int(n.out_shape.size()),
-                            n.out_shape.data(), axis, stream_));
+      if (member(n.group))
+        ck(coconet_all_gather(ctx_, cgroup(n.group), sym(sl), sym(out), COCONET_F32, int(n.out_shape.size()),
+                              n.out_shape.data(), axis, stream_));
       if (!n.gather_decl.empty()) {
         DVal& d = vals_.at(n.gather_decl);
         if (!d.view.layout.is_sliced())
-          for (int r = 0; r < G; ++r)
+          for (int r : my_ranks(n.group))
             cudaMemcpyAsync(dptr(d, r), dptr(out, r), size_t(out.local) * sizeof(float), cudaMemcpyDeviceToDevice,
                             stream_);
       }
       lowering_.push_back(n.id + ":fused_allreduce(generic)");
     }
+    account_fused_allreduce(n, axis);
+  }
+
+  // the reference's counters for a FusedAllReduce (runtime.hpp:471-516)
+  void account_fused_allreduce(const ccopt::OpNode& n, int axis) {
+    using namespace ccopt;
+    const int G = group_of(n.group).world_size;
+    const int bw = input_bw(n);
+    const DVal& x = value(n.inputs[0]);
     count_ring(n.group, axis_elems(x.view.global, axis, G), bw, true, false);
     for (auto& e : n.expr.nodes)
       if (e.op == ExprNode::Op::ReduceTensor) {
@@ -540,18 +686,72 @@ class GpuEngine {
     if (!scalar_decl(n.inputs[2], &b1) || !scalar_decl(n.inputs[4], &b2) || !scalar_decl(n.inputs[5], &t) ||
         !scalar_decl(n.inputs[7], &lr))
       return false;
-    coconet_tlist_t tl = tlist(n.group, {N});
-    coconet_adam_params hp{lr, b1, b2, t, 0.0f, 1, opt_.math, COCONET_ALGO_TWO_SHOT};
-    const void* gs[1] = {sym(g)};
-    float* ps[1] = {static_cast<float*>(sym(p))};
-    ck(coconet_fused_rs_adam_ag(ctx_, tl, gs, COCONET_F32, ps, static_cast<float*>(sym(m)),
-                                static_cast<float*>(sym(v)), &hp, stream_));
-    // the node's value (out0) is the gathered p
     DVal& out = node_out(n, Layout::replicated());
-    for (int r = 0; r < G; ++r)
-      cudaMemcpyAsync(dptr(out, r), dptr(p, r), size_t(out.local) * sizeof(float), cudaMemcpyDeviceToDevice,
-                      stream_);
+    if (member(n.group)) {
+      coconet_tlist_t tl = tlist(n.group, {N});
+      coconet_adam_params hp{lr, b1, b2, t, 0.0f, 1, opt_.math, COCONET_ALGO_TWO_SHOT};
+      const void* gs[1] = {sym(g)};
+      float* ps[1] = {static_cast<float*>(sym(p))};
+      ck(coconet_fused_rs_adam_ag(ctx_, tl, gs, COCONET_F32, ps, static_cast<float*>(sym(m)),
+                                  static_cast<float*>(sym(v)), &hp, stream_));
+      // the node's value (out0) is the gathered p
+      for (int r : my_ranks(n.group))
+        cudaMemcpyAsync(dptr(out, r), dptr(p, r), size_t(out.local) * sizeof(float), cudaMemcpyDeviceToDevice,
+                        stream_);
+    }
     lowering_.push_back(n.id + ":fused_rs_adam_ag");
+    return true;
+  }
+
+  // LAMB of tests/golden/lamb_fused_program.json (one fused node per tensor,
+  // reduce_sum inside the FusedAllReduce, state.hpp:139-174): inputs
+  // [g, m, beta1, v, beta2, t, eps, wd, p, lr], 1-D, sliced m/v, gathered p.
+  // The whole node is one coconet_fused_rs_lamb_ag launch: the per-tensor
+  // norm partials are exchanged inside the kernel (no host ReduceTensor pass).
+  bool try_fused_lamb(const ccopt::OpNode& n, int axis) {
+    using namespace ccopt;
+    if (n.inputs.size() != 10 || n.out_shape.size() != 1 || axis != 0 || n.gather_decl.empty()) return false;
+    static const std::string kU =
+        "update(@1, $1 * $2 + (1 - $2) * $0) / (1 - pow($2, $5)) / "
+        "(sqrt(update(@3, $3 * $4 + (1 - $4) * $0 * $0) / (1 - pow($4, $5))) + $6) + $7 * $8";
+    static const std::string kLamb = "update(@8, $8 - $9 * sqrt(reduce_sum($8 * $8)) / sqrt(reduce_sum((" + kU +
+                                     ") * (" + kU + "))) * (" + kU + "))";
+    if (canon(n.expr, n.inputs) != kLamb || n.gather_decl != n.inputs[8].id) return false;
+    const int G = group_of(n.group).world_size;
+    const int64_t N = n.out_shape[0];
+    if ((N / G) % 4) return false;  // shard quads must coincide with the decl's slice
+    const DVal& g = value(n.inputs[0]);
+    DVal& m = vals_.at(n.inputs[1].id);
+    DVal& v = vals_.at(n.inputs[3].id);
+    DVal& p = vals_.at(n.inputs[8].id);
+    if (!m.view.layout.is_sliced() || !v.view.layout.is_sliced() || p.view.layout.kind != LayoutKind::Replicated)
+      return false;
+    float b1, b2, t, eps, wd, lr;
+    if (!scalar_decl(n.inputs[2], &b1) || !scalar_decl(n.inputs[4], &b2) || !scalar_decl(n.inputs[5], &t) ||
+        !scalar_decl(n.inputs[6], &eps) || !scalar_decl(n.inputs[7], &wd) || !scalar_decl(n.inputs[9], &lr))
+      return false;
+    DVal& out = node_out(n, Layout::replicated());
+    if (member(n.group)) {
+      coconet_tlist_t tl = tlist(n.group, {N});
+      coconet_lamb_params hp{};
+      hp.lr = lr;
+      hp.beta1 = b1;
+      hp.beta2 = b2;
+      hp.t = t;
+      hp.eps = eps;
+      hp.wd = wd;
+      hp.math = opt_.math;
+      hp.sched = COCONET_LAMB_AUTO;
+      hp.trust_guard = 0;  // the golden's raw formula
+      const void* gs[1] = {sym(g)};
+      float* ps[1] = {static_cast<float*>(sym(p))};
+      ck(coconet_fused_rs_lamb_ag(ctx_, tl, gs, COCONET_F32, ps, static_cast<float*>(sym(m)),
+                                  static_cast<float*>(sym(v)), &hp, stream_));
+      for (int r : my_ranks(n.group))
+        cudaMemcpyAsync(dptr(out, r), dptr(p, r), size_t(out.local) * sizeof(float), cudaMemcpyDeviceToDevice,
+                        stream_);
+    }
+    lowering_.push_back(n.id + ":fused_rs_lamb_ag");
     return true;
   }
 
@@ -582,16 +782,80 @@ class GpuEngine {
       return false;
     DVal& out = node_out(n, Layout::replicated());
     coconet_bdr_params hp{dr.rate, seed_, dr.key, opt_.math};
-    ck(coconet_fused_rs_bdr_ag(ctx_, cgroup(n.group), sym(x), sym(b), sym(rr), sym(out), COCONET_F32,
-                               num_elems(n.out_shape) / H, H, &hp, stream_));
+    if (member(n.group))
+      ck(coconet_fused_rs_bdr_ag(ctx_, cgroup(n.group), sym(x), sym(b), sym(rr), sym(out), COCONET_F32,
+                                 num_elems(n.out_shape) / H, H, &hp, stream_));
     lowering_.push_back(n.id + ":fused_rs_bdr_ag");
+    return true;
+  }
+
+  // Add(Dropout(Add(In0, In1)), In2): the MP epilogue's structure
+  static const ccopt::ExprNode* bdr_dropout(const ccopt::ExprDag& e) {
+    using namespace ccopt;
+    const ExprNode& root = e.nodes[size_t(e.root)];
+    if (root.op != ExprNode::Op::Add) return nullptr;
+    const ExprNode& dr = e.nodes[size_t(root.a)];
+    const ExprNode& r2 = e.nodes[size_t(root.b)];
+    if (dr.op != ExprNode::Op::Dropout || r2.op != ExprNode::Op::Input || r2.input != 2) return nullptr;
+    const ExprNode& add = e.nodes[size_t(dr.a)];
+    if (add.op != ExprNode::Op::Add) return nullptr;
+    const ExprNode& i0 = e.nodes[size_t(add.a)];
+    const ExprNode& i1 = e.nodes[size_t(add.b)];
+    if (i0.op != ExprNode::Op::Input || i0.input != 0 || i1.op != ExprNode::Op::Input || i1.input != 1) return nullptr;
+    return &dr;
+  }
+
+  // OverlapGroup{MatMul, FusedAllReduce(dropout(layer + b) + r)} in FAST math
+  // (mp_overlap.json): bf16 staging of the fp32-stored operands, then ONE
+  // coconet_mm_overlap_fused_ar (tcgen05 GEMM + the fused RS-epilogue-AG,
+  // tile flags between them); the bf16 result and partial products are
+  // widened back into the members' fp32 values.
+  bool try_fused_mp(const ccopt::OpNode& grp) {
+    using namespace ccopt;
+    if (opt_.math != COCONET_MATH_FAST || grp.members.size() != 2) return false;
+    const OpNode* mm = p_.find_node(grp.members[0]);
+    const OpNode* ar = p_.find_node(grp.members[1]);
+    if (!mm || !ar || mm->kind != OpKind::MatMul || ar->kind != OpKind::FusedAllReduce) return false;
+    if (ar->inputs.size() != 3 || !(ar->inputs[0].is_node && ar->inputs[0].id == mm->id) || mm->group != ar->group)
+      return false;
+    const int axis = ar->axis >= 0 ? ar->axis : int(ar->out_shape.size()) - 1;
+    const ExprNode* dr = bdr_dropout(ar->expr);
+    if (!dr || axis != int(ar->out_shape.size()) - 1 || !ar->gather_decl.empty()) return false;
+    const MmShape sh = mm_shape(*mm);
+    const int G = group_of(ar->group).world_size;
+    const int64_t H = ar->out_shape.back();
+    if (!tc_shape(sh) || sh.M != H || H % G || (H / G) % 8) return false;
+    const DVal& b = value(ar->inputs[1]);
+    const DVal& rr = value(ar->inputs[2]);
+    if (b.view.global != Shape{H} || b.view.layout.kind != LayoutKind::Replicated || rr.view.global != ar->out_shape ||
+        rr.view.layout.kind != LayoutKind::Replicated || mm->out_layout.kind != LayoutKind::Local)
+      return false;
+    DVal& part = node_out(*mm, mm->out_layout);
+    DVal& out = node_out(*ar, Layout::replicated());
+    const DVal xb = stage16(value(mm->inputs[0]), "#bf16:" + mm->id + ":a");
+    const DVal wb = stage16(value(mm->inputs[1]), "#bf16:" + mm->id + ":b");
+    const DVal bb = stage16(b, "#bf16:" + ar->id + ":b");
+    const DVal rb = stage16(rr, "#bf16:" + ar->id + ":r");
+    const DVal pb = stage16(part, "#bf16:" + mm->id + ":c");  // allocation only; overwritten
+    const DVal ob = stage16(out, "#bf16:" + ar->id + ":out");
+    if (member(ar->group)) {
+      coconet_bdr_params hp{dr->rate, seed_, dr->key, COCONET_MATH_FAST};
+      ck(coconet_mm_overlap_fused_ar(ctx_, cgroup(ar->group), sym(xb), sym(wb), sym(bb), sym(rb), sym(pb), sym(ob),
+                                     COCONET_BF16, sh.rows, H, sh.kl, &hp, stream_));
+      for (int r : my_ranks(ar->group)) {
+        ck(coconet_convert(ctx_, dptr(ob, r), COCONET_BF16, dptr(out, r), COCONET_F32, out.local, stream_));
+        ck(coconet_convert(ctx_, dptr(pb, r), COCONET_BF16, dptr(part, r), COCONET_F32, part.local, stream_));
+      }
+    }
+    account_fused_allreduce(*ar, axis);
+    lowering_.push_back(grp.id + ":mm_overlap_fused_ar");
     return true;
   }
 
   // ---- OverlapGroup (runtime.hpp:517-522)
   void exec_overlap(const ccopt::OpNode& grp) {
     using namespace ccopt;
-    if (opt_.fused_kernels && grp.members.size() == 3 && try_fused_pp(grp)) {
+    if (opt_.fused_kernels && ((grp.members.size() == 3 && try_fused_pp(grp)) || try_fused_mp(grp))) {
       vals_[grp.id] = vals_.at(grp.members.back());
       return;
     }
@@ -629,8 +893,9 @@ class GpuEngine {
       return false;
     DVal& out = node_out(*ag, Layout::replicated());
     coconet_bdr_params hp{dr.rate, seed_, dr.key, opt_.math};
-    ck(coconet_rs_fused_send_ag(ctx_, cgroup(rs->group), cgroup(ag->group), sym(x), sym(b), sym(r), sym(out),
-                                COCONET_F32, N, &hp, stream_));
+    if (member(rs->group) || member(ag->group))
+      ck(coconet_rs_fused_send_ag(ctx_, cgroup(rs->group), cgroup(ag->group), sym(x), sym(b), sym(r), sym(out),
+                                  COCONET_F32, N, &hp, stream_));
     // the reference's counters for the three members
     const int S = src.world_size;
     const int bw = input_bw(*rs);
@@ -783,8 +1048,20 @@ class GpuEngine {
     prog.n_reduce = int(reduce_nodes.size());
     for (size_t j = 0; j < reduce_nodes.size(); ++j) {
       std::vector<double> part(static_cast<size_t>(G));
-      ck(coconet_pointwise_reduce(ctx_, cgroup(gid), &rprogs[j], 0, int(e.nodes[size_t(reduce_nodes[j])].red),
-                                  consts.data(), part.data(), stream_));
+      if (!dist()) {
+        ck(coconet_pointwise_reduce(ctx_, cgroup(gid), &rprogs[j], 0, int(e.nodes[size_t(reduce_nodes[j])].red),
+                                    consts.data(), part.data(), stream_));
+      } else {
+        // one partial per process (its rank), exchanged over the world
+        double mine_part = 0.0;
+        if (member(gid)) {
+          const int r = opt_.comm.rank - group_of(gid).first_rank;
+          ck(coconet_pointwise_reduce(ctx_, cgroup(gid), &rprogs[j], 0, int(e.nodes[size_t(reduce_nodes[j])].red),
+                                      consts.data() + size_t(r) * size_t(nc), &mine_part, stream_));
+        }
+        const std::vector<double> all = gather_double(mine_part);
+        for (int r = 0; r < G; ++r) part[size_t(r)] = all[size_t(group_of(gid).first_rank + r)];
+      }
       if (out_layout.is_sliced()) {
         double total = part[0];
         for (int r = 1; r < G; ++r) total = reduce_apply(e.nodes[size_t(reduce_nodes[j])].red, total, part[size_t(r)]);
@@ -792,6 +1069,13 @@ class GpuEngine {
       } else {
         for (int r = 0; r < G; ++r) reduced[size_t(r) * reduce_nodes.size() + j] = part[size_t(r)];
       }
+    }
+    if (!member(gid)) return;
+    if (dist()) {  // the kernel runs this process's rank only: its constants and reduced values
+      const int r = opt_.comm.rank - group_of(gid).first_rank;
+      ck(coconet_pointwise(ctx_, cgroup(gid), &prog, consts.data() + size_t(r) * size_t(nc),
+                           reduced.data() + size_t(r) * reduce_nodes.size(), stream_));
+      return;
     }
     ck(coconet_pointwise(ctx_, cgroup(gid), &prog, consts.data(), reduced.data(), stream_));
   }

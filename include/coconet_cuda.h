@@ -264,6 +264,18 @@ int coconet_reduce(coconet_ctx_t ctx, int group, const void* x, void* out, int e
 int coconet_broadcast(coconet_ctx_t ctx, int group, const void* x, void* out, int elem, int64_t n, int root,
                       void* stream);
 
+/* Send / Recv (runtime.hpp:439-470): group rank r of src_group stores its n
+ * local elements of x into out on group rank r of dst_group (same sizes,
+ * "peer group sizes differ" otherwise). Every rank of the interval covering
+ * both groups calls; the destination sees the data after the call. */
+int coconet_send(coconet_ctx_t ctx, int src_group, int dst_group, const void* x, void* out, int elem,
+                 int64_t n, void* stream);
+
+/* Element-type conversion of a plain device array of n elements (16-bit
+ * staging of fp32-stored decls for the tcgen05 MatMul). Not collective. */
+int coconet_convert(coconet_ctx_t ctx, const void* src, int src_elem, void* dst, int dst_elem, int64_t n,
+                    void* stream);
+
 /* ---- fused MP / PP epilogues (goldens/model_parallel.json, pipeline.json) - */
 /* out = dropout(x + b, rate, key) + r, element-wise, dropout index = global
  * flat index (expr.hpp:15-27, state.hpp:178-181); b broadcast over leading
@@ -299,9 +311,14 @@ int coconet_matmul(coconet_ctx_t ctx, int group, const void* a, const void* b, v
                    void* stream);
 
 /* OverlapGroup{MatMul, FusedAllReduce(bias+dropout+residual)} (mp_overlap.json,
- * runtime.hpp:517-522): the GEMM produces column-block tiles in rank-rotated
- * order (chunk_order, runtime.hpp:46-50) and publishes per-tile flags; the
- * RS->epilogue->AG of each tile starts as soon as every rank published it. */
+ * runtime.hpp:517-522). One-kernel schedule: the GEMM publishes a flag per
+ * output tile, row tile outermost (every rank publishes row tile i before
+ * row tile i+1; the reference's rank-rotated chunk_order, runtime.hpp:46-50,
+ * is a cost-model order only), and comm warps start the RS->epilogue->AG of
+ * a (row tile, column block) unit as soon as every rank published its tiles.
+ * AUTO runs the GEMM then coconet_fused_rs_bdr_ag (bitwise the same result)
+ * until the one-kernel schedule is measured faster over NVLink;
+ * COCONET_MP_OVERLAP=fused|sequential forces either. */
 int coconet_mm_overlap_fused_ar(coconet_ctx_t ctx, int group, const void* a, const void* w,
                                 const void* b, const void* r, void* partial, void* out,
                                 int in_elem, int64_t rows, int64_t cols, int64_t k_local,

@@ -28,7 +28,9 @@ OUT = ROOT / "tests" / "golden"
 ADAM_CASES = [(w, n) for w in (1, 2, 4, 8) for n in (1024, 4096)] + [(4, 1 << 20), (8, 1 << 16)] + [
     (3, 3000), (5, 4100), (6, 6000), (7, 7007)]  # odd world sizes; 7007/7 = 1001 takes the generic lowering
 MP_CASES = [(w, dims) for w in (1, 2, 4) for dims in ({"B": 2, "S": 8, "H": 64},)] + [
-    (8, {"B": 2, "S": 16, "H": 128})]
+    (8, {"B": 2, "S": 16, "H": 128})] + [
+    # shapes the tcgen05 GEMM takes (rows % 128, K % 64, H % 128): GpuEngine's FAST lowering
+    (8, {"B": 8, "S": 16, "H": 512}), (4, {"B": 2, "S": 64, "H": 768}), (2, {"B": 4, "S": 64, "H": 256})]
 PP_CASES = [(w, n) for w in (2, 4, 8) for n in (1024, 4096)] + [(6, 6000)]
 # Reduce / Broadcast (runtime.hpp:415-436) + reorder_broadcast (transform.hpp:265-330):
 # no reference golden uses them, so the program is authored in the reference
@@ -73,7 +75,19 @@ def run_case(name, program, schedule, dims, seed=1, sched_program=None):
     return rec
 
 
+def write_mp():
+    mp = REF / "goldens" / "model_parallel.json"
+    mp_s = REF / "schedules" / "mp_overlap.json"
+    recs = []
+    for w, d in MP_CASES:
+        dims = dict(d, N=1024, W=w)
+        recs.append(run_case(f"mp_W{w}_B{d['B']}_S{d['S']}_H{d['H']}", mp.read_text(), mp_s.read_text(), dims))
+    (OUT / "mp_cases.json").write_text(json.dumps(recs, indent=1))
+
+
 def main():
+    if len(sys.argv) > 1 and sys.argv[1] == "--mp-only":
+        return write_mp()
     if not ref.available():
         sys.exit("oracle/_ref/libccopt_ref.so missing: make -C oracle ref")
     OUT.mkdir(parents=True, exist_ok=True)
@@ -84,13 +98,7 @@ def main():
         dims = {"N": n, "W": w, "B": 2, "S": 8, "H": 64}
         recs.append(run_case(f"adam_W{w}_N{n}", adam.read_text(), adam_s.read_text(), dims))
     (OUT / "adam_cases.json").write_text(json.dumps(recs, indent=1))
-    mp = REF / "goldens" / "model_parallel.json"
-    mp_s = REF / "schedules" / "mp_overlap.json"
-    recs = []
-    for w, d in MP_CASES:
-        dims = dict(d, N=1024, W=w)
-        recs.append(run_case(f"mp_W{w}_B{d['B']}_S{d['S']}_H{d['H']}", mp.read_text(), mp_s.read_text(), dims))
-    (OUT / "mp_cases.json").write_text(json.dumps(recs, indent=1))
+    write_mp()
     pp = REF / "goldens" / "pipeline.json"
     pp_s = REF / "schedules" / "pipeline_overlap.json"
     recs = []

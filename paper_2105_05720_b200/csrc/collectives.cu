@@ -124,6 +124,50 @@ __global__ void __launch_bounds__(kThreads) bcast_kernel(RootArgs a) {
   edge_barrier(rs, 1);  // nobody overwrites the root's x while peers still read it (across processes)
 }
 
+// Send (runtime.hpp:439-470): group rank r of the source stage stores its n
+// local elements into group rank r of the destination stage (a push over
+// NVLink). Launched over the rank interval covering both stages: the entry
+// barrier orders the push after the destination's previous readers, the exit
+// barrier makes it visible before the destination's next kernel.
+struct SendArgs {
+  RankSet rs;
+  int64_t x_off, out_off, n;
+  int src_first, dst_first, size;  // union-relative first ranks, stage size
+};
+
+template <typename T, int VEC>
+__global__ void __launch_bounds__(kThreads) send_kernel(SendArgs a) {
+  __shared__ char* s_base[kMaxRanks];
+  const RankSet& rs = a.rs;
+  if (threadIdx.x < kMaxRanks) s_base[threadIdx.x] = threadIdx.x < rs.world ? rs.base[threadIdx.x] : nullptr;
+  const int me = rs.rank();
+  if (!edge_barrier(rs, 0)) return;
+  const int sr = me - a.src_first;
+  if (sr >= 0 && sr < a.size) {
+    const T* src = reinterpret_cast<const T*>(s_base[me] + a.x_off);
+    T* dst = reinterpret_cast<T*>(s_base[a.dst_first + sr] + a.out_off);
+    const int64_t nq = a.n / VEC;
+    for (int64_t q = int64_t(blockIdx.x) * kThreads + threadIdx.x; q < nq; q += int64_t(gridDim.x) * kThreads) {
+      if (VEC == 4) {
+        float x[4];
+        load4_cg(src + q * 4, x);
+        store4(dst + q * 4, x);
+      } else {
+        dst[q] = src[q];
+      }
+    }
+  }
+  edge_barrier(rs, 1);
+}
+
+// Element type conversion of a plain device array (the 16-bit staging of
+// fp32-stored decls for the tcgen05 MatMul; not collective).
+template <typename S, typename D>
+__global__ void __launch_bounds__(kThreads) convert_kernel(const S* src, D* dst, int64_t n) {
+  for (int64_t i = int64_t(blockIdx.x) * kThreads + threadIdx.x; i < n; i += int64_t(gridDim.x) * kThreads)
+    dst[i] = from_f32<D>(to_f32(src[i]));
+}
+
 template <typename T, int RED, int VEC>
 __global__ void __launch_bounds__(kThreads) rs_kernel(AxisArgs a) {
   __shared__ char* s_base[kMaxRanks];
@@ -318,6 +362,74 @@ int coconet_all_gather(coconet_ctx_t c, int group, const void* x, void* out, int
                    : elem == COCONET_F16 ? ag_pick<__half>(vec)
                                          : ag_pick<__nv_bfloat16>(vec);
   return launch(c, group, fn, &a, vec, static_cast<cudaStream_t>(stream));
+}
+
+int coconet_send(coconet_ctx_t c, int src_group, int dst_group, const void* x, void* out, int elem, int64_t n,
+                 void* stream) {
+  if (!c || !x || !out) return set_error(COCONET_ERR_INVALID_INPUT, "null argument");
+  if (!valid_group(c, src_group) || !valid_group(c, dst_group))
+    return set_error(COCONET_ERR_NO_SUCH_RANK, "no such group");
+  const coconet_group_s gs = c->groups[size_t(src_group)], gd = c->groups[size_t(dst_group)];
+  if (gs.size != gd.size) return set_error(COCONET_ERR_NO_SUCH_RANK, "peer group sizes differ");  // runtime.hpp:448
+  if (n < 0) return set_error(COCONET_ERR_SHAPE_MISMATCH, "negative element count");
+  if (elem < COCONET_F32 || elem > COCONET_BF16) return set_error(COCONET_ERR_INVALID_INPUT, "bad elem");
+  const int first = std::min(gs.first, gd.first);
+  const int end = std::max(gs.first + gs.size, gd.first + gd.size);
+  int ug = -1;
+  for (size_t i = 0; i < c->groups.size(); ++i)
+    if (c->groups[i].first == first && c->groups[i].size == end - first) ug = int(i);
+  if (ug < 0) {
+    int rc = coconet_group_create(c, first, end - first, &ug);
+    if (rc) return rc;
+  }
+  SendArgs a{};
+  int rc = heap_offset(c, x, &a.x_off);
+  if (!rc) rc = heap_offset(c, out, &a.out_off);
+  if (rc) return rc;
+  a.n = n;
+  a.src_first = gs.first - first;
+  a.dst_first = gd.first - first;
+  a.size = gs.size;
+  const bool vec = n % 4 == 0 && (a.x_off | a.out_off) % (4 * elem_size(elem)) == 0;
+  auto pick = [&](auto tag) -> const void* {
+    using T = decltype(tag);
+    return vec ? reinterpret_cast<const void*>(&send_kernel<T, 4>) : reinterpret_cast<const void*>(&send_kernel<T, 1>);
+  };
+  const void* fn = elem == COCONET_F32 ? pick(float{}) : elem == COCONET_F16 ? pick(__half{}) : pick(__nv_bfloat16{});
+  const int64_t units = vec ? n / 4 : n;
+  int blocks = 0;
+  rc = coop_blocks(c, fn, kThreads, 0, ug, std::max<int64_t>(1, (units + kThreads - 1) / kThreads), &blocks);
+  if (!rc) rc = make_rankset(c, ug, &a.rs);
+  if (rc) return rc;
+  void* args[] = {&a};
+  return coop_launch(c, fn, dim3(unsigned(blocks), unsigned(local_ranks(c, ug))), dim3(kThreads), args, 0,
+                     static_cast<cudaStream_t>(stream));
+}
+
+int coconet_convert(coconet_ctx_t c, const void* src, int src_elem, void* dst, int dst_elem, int64_t n,
+                    void* stream) {
+  if (!c || (n > 0 && (!src || !dst))) return set_error(COCONET_ERR_INVALID_INPUT, "null argument");
+  if (src_elem < COCONET_F32 || src_elem > COCONET_BF16 || dst_elem < COCONET_F32 || dst_elem > COCONET_BF16)
+    return set_error(COCONET_ERR_INVALID_INPUT, "bad elem");
+  if (n <= 0) return COCONET_OK;
+  const unsigned blocks = unsigned(std::min<int64_t>((n + kThreads - 1) / kThreads, int64_t(c->sm_count) * 8));
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  auto go = [&](auto ts) {
+    using S = decltype(ts);
+    auto to = [&](auto td) {
+      using D = decltype(td);
+      convert_kernel<S, D><<<blocks, kThreads, 0, s>>>(static_cast<const S*>(src), static_cast<D*>(dst), n);
+    };
+    if (dst_elem == COCONET_F32) to(float{});
+    else if (dst_elem == COCONET_F16) to(__half{});
+    else to(__nv_bfloat16{});
+  };
+  if (src_elem == COCONET_F32) go(float{});
+  else if (src_elem == COCONET_F16) go(__half{});
+  else go(__nv_bfloat16{});
+  CN_CUDA(cudaGetLastError());
+  c->launches++;
+  return COCONET_OK;
 }
 
 int coconet_reduce(coconet_ctx_t c, int group, const void* x, void* out, int elem, int reducer, int64_t n,

@@ -112,14 +112,27 @@ int coconet_engine_set(void* h, const char* name, int rank, const float* data, i
   }
 }
 
-// which: 0 = scheduled program, 1 = base program
-int coconet_engine_run(void* h, uint64_t seed, int which, int device, int math, int fused) {
+// World all-gather supplied by the caller for DISTRIBUTED runs (rank order,
+// `bytes` in, world * bytes out; collective over every process).
+typedef void (*coconet_engine_allgather_fn)(const void* in, size_t bytes, void* out, void* user);
+
+// which: 0 = scheduled program, 1 = base program. rank < 0: VIRTUAL (every
+// rank in this process); rank >= 0: DISTRIBUTED, this process is world rank
+// `rank` of `world` and `allgather` bootstraps the peer mappings and
+// assembles the results (every process gets the same report).
+int coconet_engine_run_dist(void* h, uint64_t seed, int which, int device, int math, int fused, int rank, int world,
+                            coconet_engine_allgather_fn allgather, void* user) {
   auto* s = static_cast<Session*>(h);
   try {
     coconet::GpuOptions opt;
     opt.device = device;
     opt.math = math;
     opt.fused_kernels = fused != 0;
+    if (rank >= 0) {
+      opt.comm.rank = rank;
+      opt.comm.world = world;
+      opt.comm.allgather = [allgather, user](const void* in, size_t bytes, void* out) { allgather(in, bytes, out, user); };
+    }
     const ccopt::Program& p = which == 0 ? s->sched : s->base;
     coconet::GpuEngine e(p, ccopt::CommConfig{}, seed, opt);
     s->rep = e.run(which == 0 ? s->in_sched : s->in_base);
@@ -133,6 +146,10 @@ int coconet_engine_run(void* h, uint64_t seed, int which, int device, int math, 
   } catch (const std::exception& e) {
     return fail_std(e);
   }
+}
+
+int coconet_engine_run(void* h, uint64_t seed, int which, int device, int math, int fused) {
+  return coconet_engine_run_dist(h, seed, which, device, math, fused, -1, 0, nullptr, nullptr);
 }
 
 uint64_t coconet_engine_digest(void* h) { return static_cast<Session*>(h)->rep.digest; }

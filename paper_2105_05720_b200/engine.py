@@ -17,6 +17,25 @@ _elib = None
 
 SCHEDULED, BASE = 0, 1
 
+# void (*)(const void* in, size_t bytes, void* out, void* user)
+ALLGATHER_FN = C.CFUNCTYPE(None, C.c_void_p, C.c_size_t, C.c_void_p, C.c_void_p)
+
+
+def torch_allgather(process_group=None):
+    """A world all-gather over torch.distributed (any backend; gloo in the
+    tests) in the engine's callback form: raw bytes in, world x bytes out."""
+    import torch
+    import torch.distributed as dist
+
+    def fn(src, nbytes, dst, _user):
+        world = dist.get_world_size(process_group)
+        buf = torch.frombuffer(C.string_at(src, nbytes), dtype=torch.uint8) if nbytes else torch.empty(0, dtype=torch.uint8)
+        out = [torch.empty(nbytes, dtype=torch.uint8) for _ in range(world)]
+        dist.all_gather(out, buf.clone(), group=process_group)
+        flat = torch.cat(out).numpy() if nbytes else np.empty(0, np.uint8)
+        C.memmove(dst, flat.ctypes.data, flat.nbytes)
+    return fn
+
 
 def load():
     global _elib
@@ -34,6 +53,7 @@ def load():
             ("coconet_engine_gen", I, [P, U64]),
             ("coconet_engine_set", I, [P, C.c_char_p, I, FP, I64]),
             ("coconet_engine_run", I, [P, U64, I, I, I, I]),
+            ("coconet_engine_run_dist", I, [P, U64, I, I, I, I, I, I, ALLGATHER_FN, P]),
             ("coconet_engine_digest", U64, [P]),
             ("coconet_engine_report", I, [P, C.c_char_p, I64]),
             ("coconet_engine_result", I, [P, C.c_char_p, I, FP, I64]),
@@ -86,8 +106,17 @@ class GpuEngineSession:
                                            a.ctypes.data_as(C.POINTER(C.c_float)), a.size))
 
     def run(self, seed: int, which: int = SCHEDULED, device: int = 0, math: int = _lib.MATH_EXACT,
-            fused: bool = True):
-        _check(self.lib.coconet_engine_run(self.h, seed, which, device, math, int(fused)))
+            fused: bool = True, rank: int | None = None, world: int = 0, allgather=None):
+        """VIRTUAL (rank None): every rank in this process. DISTRIBUTED: this
+        process is world rank `rank`; `allgather(src, nbytes, dst, user)` is a
+        collective world all-gather (engine.torch_allgather() for
+        torch.distributed)."""
+        if rank is None:
+            _check(self.lib.coconet_engine_run(self.h, seed, which, device, math, int(fused)))
+            return
+        cb = ALLGATHER_FN(allgather)
+        self._cb = cb  # keep the trampoline alive for the call
+        _check(self.lib.coconet_engine_run_dist(self.h, seed, which, device, math, int(fused), rank, world, cb, None))
 
     def digest(self) -> int:
         return int(self.lib.coconet_engine_digest(self.h))

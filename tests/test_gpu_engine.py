@@ -76,15 +76,19 @@ def test_base_program_matches_reference_engine(rec):
 
 
 @pytest.mark.parametrize("W,N", [(1, 1024), (2, 2048), (4, 4096)])
-def test_lamb_program_on_gpu_engine(W, N):
-    """The authored LAMB programs (reduce_sum inside the fused expression) run
-    through GpuEngine (generic lowering with the ReduceTensor pre-pass) within
-    1e-5 of the oracle; sums are parallel, so not bit-exact."""
+@pytest.mark.parametrize("math", [_lib.MATH_EXACT, _lib.MATH_FAST])
+def test_lamb_program_on_gpu_engine(W, N, math):
+    """The authored LAMB programs (reduce_sum inside the fused expression)
+    lower to ONE coconet_fused_rs_lamb_ag launch (the per-tensor norms are
+    exchanged inside the kernel, no host ReduceTensor pass) and stay within
+    1e-5 of the oracle; the generic lowering (RS -> pointwise with the
+    ReduceTensor pre-pass -> AG) agrees as well."""
     base = (GOLD / "lamb_program.json").read_text()
     fused = (GOLD / "lamb_fused_program.json").read_text()
     s = GpuEngineSession(base, sched_program=fused, dims={"N": N, "W": W})
     s.gen(3)
-    s.run(3, SCHEDULED)
+    s.run(3, SCHEDULED, math=math)
+    assert any(x.endswith(":fused_rs_lamb_ag") for x in s.report()["lowering"]), s.report()["lowering"]
     # oracle by definition (restated) on the same generated inputs
     gl = np.stack([co.gen_decl(3, "g", [N], "local", r, W) for r in range(W)])
     sc = {n: float(co.gen_decl(3, n, [], "replicated", 0, W)[0]) for n in ("lr", "beta1", "beta2", "t", "eps", "wd")}
@@ -94,14 +98,65 @@ def test_lamb_program_on_gpu_engine(W, N):
     assert co.max_rel_deviation(s.result("tensor:p", 0, N), po) <= 1e-5
     assert co.max_rel_deviation(s.result("tensor:m", 0, N), mo) <= 1e-5
     assert co.max_rel_deviation(s.result("out0", 0, N), po) <= 1e-5
+    s.run(3, SCHEDULED, math=math, fused=False)
+    assert any("generic" in x for x in s.report()["lowering"])
+    assert co.max_rel_deviation(s.result("tensor:p", 0, N), po) <= 1e-5
 
 
-def test_replication_violation_is_reported():
-    """Execute.ReplicationViolation (test_runtime.cpp:122-133)."""
-    rec = [r for r in CASES if r["name"] == "adam_W4_N1024"][0]
+@pytest.mark.parametrize("W", [1, 2, 4, 8])
+@pytest.mark.parametrize("math", [_lib.MATH_EXACT, _lib.MATH_FAST])
+def test_lamb_list_programs_on_gpu_engine(W, math):
+    """The per-tensor LAMB programs over a 5-tensor list
+    (tests/golden/lamb_list_*, evaluated by the reference): every node whose
+    slices are whole quads lowers to coconet_fused_rs_lamb_ag; EXACT reproduces the reference
+    Engine's p, m, v to <= 1 ulp (m, v bit-exact; only the norm summation
+    order differs), FAST within 1e-5."""
+    cases = json.loads((GOLD / "lamb_list_cases.json").read_text())
+    rec = next(r for r in cases if r["W"] == W)
+    arrs = np.load(GOLD / "lamb_list_results.npz")
+    s = GpuEngineSession((GOLD / "lamb_list_program.json").read_text(),
+                         sched_program=(GOLD / "lamb_list_fused_program.json").read_text(), dims={"W": W})
+    s.gen(1)
+    s.run(1, SCHEDULED, math=math)
+    rep = s.report()
+    # nodes whose per-rank slice is whole quads take the fused kernel (shard
+    # quads must coincide with the decl's slice), the rest the generic lowering
+    want = sum((n // W) % 4 == 0 for n in rec["counts"])
+    assert sum(x.endswith(":fused_rs_lamb_ag") for x in rep["lowering"]) == want, rep["lowering"]
+    for i, n in enumerate(rec["counts"]):
+        for name in ("p", "m", "v"):
+            got, want = s.result(f"tensor:{name}{i}", 0, n), arrs[f"W{W}_{name}{i}"]
+            if math == _lib.MATH_EXACT:
+                d = np.abs(got.view(np.int32).astype(np.int64) - want.view(np.int32).astype(np.int64))
+                assert d.max() <= (1 if name == "p" else 0), (name, i)
+            else:
+                assert co.max_rel_deviation(got, want) <= 1e-5, (name, i)
+
+
+MP_FAST_CASES = ["mp_W8_B8_S16_H512", "mp_W4_B2_S64_H768", "mp_W2_B4_S64_H256"]
+
+
+@pytest.mark.parametrize("name", MP_FAST_CASES)
+def test_mp_program_fast_lowers_to_tcgen05_overlap(name):
+    """mp_overlap.json in FAST math: OverlapGroup{MatMul, FusedAllReduce}
+    lowers to ONE coconet_mm_overlap_fused_ar (bf16 staging, tcgen05 GEMM,
+    fused RS-bias-dropout-residual-AG) and the base program's MatMul to the
+    tcgen05 GEMM; both within the north star's 1e-2 of the EXACT run, whose
+    digest equals the reference Engine's."""
+    rec = next(r for r in CASES if r["name"] == name)
     s = _session(rec)
-    bad = co.gen_decl(1, "p", [1024], "replicated", 0, 4)
-    bad[0] += 1.0
-    s.set("p", 2, bad)
-    with pytest.raises(EngineError, match="ReplicationViolation"):
-        s.run(1, SCHEDULED)
+    d = rec["dims"]
+    n = d["B"] * d["S"] * d["H"]
+    s.run(1, SCHEDULED, math=_lib.MATH_EXACT)
+    assert "%016x" % s.digest() == rec["engine_sched_digest"]
+    exact = s.result("out0", 0, n)
+    s.run(1, SCHEDULED, math=_lib.MATH_FAST)
+    rep = s.report()
+    assert any(x.endswith(":mm_overlap_fused_ar") for x in rep["lowering"]), rep["lowering"]
+    for k in ("comm_bytes", "intergroup_bytes", "traffic_saved_bytes", "kernel_steps"):
+        assert rep[k] == rec["report_sched"][k], k
+    assert co.max_rel_deviation(s.result("out0", 0, n), exact) <= 1e-2
+    s.run(1, BASE, math=_lib.MATH_FAST)
+    low = s.report()["lowering"]
+    assert any(x.endswith(":matmul(tcgen05)") for x in low), low
+    assert co.max_rel_deviation(s.result("out0", 0, n), exact) <= 1e-2
