@@ -35,7 +35,8 @@ sys.path.insert(0, str(ROOT))
 
 METRIC = "fused AR+Adam/LAMB step time & NVLink-roofline fraction, 1/2/4/8 B200"
 UNIT = "Gelem/s"
-NVLINK_GBS = 770.0  # measured peer copy per direction (B200_PROFILING.md)
+NVLINK_GBS = 770.0  # B200_PROFILING.md's measured peer copy per direction (900 nominal); at N>1
+# bench.py measures its own peer copy and uses that when it can
 BUCKET_CAP = 16384  # N=1: segments of the TMA LAMB schedule
 BUCKET_CAP_MULTI = 16384  # N>1: the TMA schedule across ranks is fastest at 16384
 # (W=2/8 virtual, profiles/r01_lamb_w_probe.json); GRID would prefer 4096
@@ -201,12 +202,85 @@ def run_reference(args):
 # ---------------------------------------------------------------------------
 # the CUDA path
 
+def lamb_parity(ctx, tl, counts, grads, params, m, v, hp, world, rank, distributed):
+    """One fused step after the timed region, checked against an fp64 torch
+    evaluation of the LAMB definition (tests/golden/lamb_list_*: per tensor
+    m' = b1 m + (1-b1) g, v' = b2 v + (1-b2) g^2, u = m'/bc1 / (sqrt(v'/bc2) +
+    eps) + wd p, p' = p - lr ||p||/||u|| u) on the pre-step state, over EVERY
+    tensor: p (this rank's gathered copy), m and v (every rank's shard). g is
+    the sum of all ranks' fp16 gradients. Tolerance: the north star's 1e-5
+    for fp32 optimizer state."""
+    import math
+
+    import torch
+    import torch.distributed as dist
+
+    me = ctx.local_ranks()[0]
+    dev = torch.device("cuda")
+
+    def shards(buf):
+        loc = ctx.view(buf, me).clone()
+        if not distributed:
+            return [loc]
+        allb = [torch.empty_like(loc) for _ in range(world)]
+        dist.all_gather(allb, loc)
+        return allb
+
+    m0, v0 = shards(m), shards(v)
+    p0 = [ctx.view(b, me).clone() for b in params]
+    g_sum = []
+    for b in grads:
+        x = ctx.view(b, me).double()
+        if distributed:
+            dist.all_reduce(x)
+        g_sum.append(x)
+    fused_rs_lamb_ag = __import__("paper_2105_05720_b200.collectives", fromlist=["x"]).fused_rs_lamb_ag
+    fused_rs_lamb_ag(ctx, tl, grads, params, m, v, hp)
+    ctx.check()
+    m1, v1 = shards(m), shards(v)
+    # element -> shard position per tensor, from every rank's segment table
+    idx = [[] for _ in counts]
+    for r in range(world):
+        segs = torch.from_numpy(tl.segments(r))
+        for t, toff, ln, sidx in segs.tolist():
+            idx[t].append((toff, ln, r, sidx))
+    b1, b2 = float(hp.beta1), float(hp.beta2)
+    bc1, bc2 = 1 - b1 ** hp.t, 1 - b2 ** hp.t
+    worst, checked = 0.0, 0
+    for t, n in enumerate(counts):
+        pos = torch.empty(n, dtype=torch.int64)
+        src = torch.empty(n, dtype=torch.int64)
+        for toff, ln, r, sidx in idx[t]:
+            pos[toff:toff + ln] = torch.arange(sidx, sidx + ln)
+            src[toff:toff + ln] = r
+        pos, src = pos.to(dev), src.to(dev)
+        stack = lambda parts: torch.stack(parts)[src, pos]  # noqa: E731
+        mo, vo = stack(m0).double(), stack(v0).double()
+        g, p = g_sum[t], p0[t].double()
+        mn = b1 * mo + (1 - b1) * g
+        vn = b2 * vo + (1 - b2) * g * g
+        u = (mn / bc1) / ((vn / bc2).sqrt() + float(hp.eps)) + float(hp.wd) * p
+        pn = p - float(hp.lr) * math.sqrt(float((p * p).sum())) / math.sqrt(float((u * u).sum())) * u
+
+        def dev_of(a, b):
+            return float((a.double() - b).abs().max() / torch.maximum(a.double().abs().max(), b.abs().max()).clamp_min(1e-12))
+
+        worst = max(worst, dev_of(ctx.view(params[t], me), pn), dev_of(stack(m1), mn), dev_of(stack(v1), vn))
+        checked += 1
+    if distributed:
+        from paper_2105_05720_b200.runtime import max_over_ranks
+        worst = max_over_ranks(worst)
+    return {"max_rel_dev": worst, "tensors_checked": checked, "tolerance": 1e-5, "ok": worst <= 1e-5,
+            "checker": "torch fp64 LAMB definition on the pre-step state (p, m, v of every tensor)"}
+
+
 def run_coconet(args):
     import torch
     import torch.distributed as dist
 
-    from paper_2105_05720_b200 import _lib
-    from paper_2105_05720_b200.collectives import LambHParams, TensorList, fused_rs_lamb_ag, gen_values
+    from paper_2105_05720_b200 import _lib  # noqa: F401
+    from paper_2105_05720_b200.collectives import (AdamHParams, LambHParams, TensorList, fused_rs_adam_ag,
+                                                   fused_rs_lamb_ag, gen_values, unfused_lamb)
     from paper_2105_05720_b200.runtime import Context, max_over_ranks
     from paper_2105_05720_b200.workloads import BERT_LARGE_PARAMS, bert_large_counts
 
@@ -230,9 +304,10 @@ def run_coconet(args):
     padded = [(n + 63) // 64 * 64 for n in counts]
     W = world
     shard_state = 2 * (sum(counts) // W + 64 * len(counts) + 4096) * 4  # m + v of one rank's shard
+    full_state = (sum(counts) + 64 * len(counts) + 4096) * 4  # one fp32 buffer over the size-1 group's list
     need = (sum(padded) * (2 + 4) + shard_state  # flat g, p + the fused step's m, v
             + shard_state + 2 * 8192 * E2E_GROUPS * 4  # the e2e pipeline's per-group m, v
-            + (2 * sum(padded) * 4 if distributed else 0)  # the NCCL baseline's replicated m, v
+            + 3 * full_state  # the unfused baseline's replicated m, v and its u scratch
             + (256 << 20))
     ctx = Context(W, mode="distributed" if distributed else "virtual", rank=rank, device=local_rank,
                   heap_bytes=need)
@@ -273,10 +348,23 @@ def run_coconet(args):
             dist.barrier()
         torch.cuda.synchronize()
 
+    def event_time(fn, steps):
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        barrier()
+        e0.record(stream)
+        for _ in range(steps):
+            fn()
+        e1.record(stream)
+        barrier()
+        t = e0.elapsed_time(e1) / steps
+        return max_over_ranks(t) if distributed else t
+
     for _ in range(args.warmup):
         step()
     ctx.check()
     barrier()
+
     def timed():
         sampler = ClockSampler(local_rank)
         sampler.start()
@@ -308,40 +396,57 @@ def run_coconet(args):
     N = BERT_LARGE_PARAMS
     value = W * N / (ms * 1e-3) / 1e9
 
-    # -- the unfused GPU baseline (north star): NCCL all_reduce of the flat
-    # fp16 gradients, then a separate LAMB over ALL elements on every rank
-    # (replicated state, DDP + fused-optimizer style), on the same box
-    nccl_baseline = None
-    if distributed and not share:
-        try:  # the baseline is reported, never allowed to sink the bench line
-            g1 = ctx.group(rank, 1)
-            tl1 = TensorList(ctx, counts, group=g1, bucket_cap=BUCKET_CAP)  # size-1 group: the TMA path
-            m1 = ctx.alloc([tl1.shard_elems], torch.float32)
-            v1 = ctx.alloc([tl1.shard_elems], torch.float32)
-            ctx.view(m1).zero_()
-            ctx.view(v1).fill_(1e-4)
-            flat = ctx.view(flat_g)
+    # -- parity of the timed call: one more step, every tensor checked
+    parity = None
+    if not args.no_parity:
+        try:
+            parity = lamb_parity(ctx, tl, counts, grads, params, m, v, hp, world, rank, distributed)
+        except Exception as e:
+            parity = {"failed": repr(e)[:300]}
+        torch.cuda.empty_cache()
+
+    # -- the unfused GPU baseline (north star: "NCCL plus separate kernels"):
+    # NCCL all_reduce of the flat fp16 gradients (N > 1), then the same LAMB
+    # as apex FusedLAMB's FOUR separate multi-tensor kernels over all elements
+    # on every rank (replicated state; coconet_unfused_lamb, csrc/unfused.cu)
+    baseline = None
+    if not args.no_baseline:
+        try:
+            g1 = ctx.group(ctx.local_ranks()[0], 1)
+            tl1 = TensorList(ctx, counts, group=g1, bucket_cap=BUCKET_CAP)
+            m1, v1, u1 = (ctx.alloc([tl1.shard_elems], torch.float32) for _ in range(3))
+            ctx.view(m1).zero_() if distributed else ctx.view(m1, 0).zero_()
+            (ctx.view(v1) if distributed else ctx.view(v1, 0)).fill_(1e-4)
+            norms = torch.zeros(2 * len(counts), dtype=torch.float64, device="cuda")
+            flat = ctx.view(flat_g) if distributed else ctx.view(flat_g, 0)
 
             def base_step():
-                dist.all_reduce(flat)
-                fused_rs_lamb_ag(ctx, tl1, grads, params, m1, v1, hp)
+                if distributed:
+                    dist.all_reduce(flat)
+                unfused_lamb(ctx, tl1, grads, params, m1, v1, u1, norms, hp)
 
-            for _ in range(args.warmup):
+            for _ in range(3):
                 base_step()
-            barrier()
-            b0 = torch.cuda.Event(enable_timing=True)
-            b1 = torch.cuda.Event(enable_timing=True)
-            b0.record(stream)
-            for _ in range(args.steps):
-                base_step()
-            b1.record(stream)
-            barrier()
-            bms = max_over_ranks(b0.elapsed_time(b1) / args.steps)
-            nccl_baseline = {"ms_per_step": bms, "value": W * N / (bms * 1e-3) / 1e9, "unit": UNIT,
-                             "what": "NCCL all_reduce (fp16, flat) + separate LAMB over all elements per rank",
-                             "speedup_of_fused": bms / ms}
+            ctx.check()
+            bms = event_time(base_step, max(3, min(args.steps, 10)))
+            baseline = {"ms_per_step": bms, "value": W * N / (bms * 1e-3) / 1e9, "unit": UNIT,
+                        "what": ("NCCL all_reduce (fp16, flat) + " if distributed else "") +
+                                "apex-FusedLAMB-structured separate kernels (stage 1, l2norm partials, "
+                                "per-tensor combine, stage 2: 46 B/element) over all elements per rank",
+                        "fused_speedup": bms / ms}
+            if distributed:
+                baseline["nccl_allreduce_ms"] = event_time(lambda: dist.all_reduce(flat), 3)
+            tl1.close()
+            for b in (m1, v1, u1):
+                ctx.free(b)
         except Exception as e:
-            nccl_baseline = {"failed": repr(e)}
+            baseline = {"failed": repr(e)[:300]}
+        if world == 1:  # Adam on the same list: the fused FAST kernel vs torch._fused_adam_ (fp32 grads)
+            try:
+                baseline["adam"] = adam_vs_torch(ctx, counts, event_time)
+            except Exception as e:
+                baseline["adam"] = {"failed": repr(e)[:300]}
+        torch.cuda.empty_cache()
 
     # -- e2e: through the public API with HOST buffers (pinned): every step
     # copies this rank's fp16 gradients H2D and its updated fp32 parameters
@@ -376,6 +481,14 @@ def run_coconet(args):
 
     # -- roofline of the dominant (only) kernel
     hbm_peak, tc_peak, peak_kind = peaks()
+    nvl_peak, nvl_kind = NVLINK_GBS, "B200_PROFILING.md measured peer copy per direction (900 nominal)"
+    if distributed and not share:
+        try:
+            from tools.dist_extras import peer_copy_gbs
+            measured = max_over_ranks(-peer_copy_gbs(ctx))  # min over ranks
+            nvl_peak, nvl_kind = -measured, "peer copy measured in this run (min over ranks, per direction)"
+        except Exception:
+            pass
     shard = N / W
     # per-rank HBM bytes: W=1 two-pass LAMB = 38 B/elem; W>1 the
     # shard's 38 B minus its g read / p write (served by the peers' HBM) plus this
@@ -386,12 +499,15 @@ def run_coconet(args):
         achieved = hbm_bytes / (ms * 1e-3) / 1e9
         roof = {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                 "frac": achieved / hbm_peak, "peak_kind": peak_kind,
-                "algorithmic_bytes_per_launch": hbm_bytes}
+                "algorithmic_bytes_per_launch": hbm_bytes,
+                "compulsory_bytes_per_launch": 26.0 * N,
+                "compulsory_frac": 26.0 * N / (ms * 1e-3) / 1e9 / hbm_peak}
     else:
         achieved = nvl_bytes / (ms * 1e-3) / 1e9
-        roof = {"bound": "nvlink", "achieved": achieved, "peak": NVLINK_GBS, "unit": "GB/s",
-                "frac": achieved / NVLINK_GBS, "peak_kind": "measured peer copy (B200_PROFILING.md)",
-                "algorithmic_bytes_per_launch": nvl_bytes}
+        roof = {"bound": "nvlink", "achieved": achieved, "peak": nvl_peak, "unit": "GB/s",
+                "frac": achieved / nvl_peak, "peak_kind": nvl_kind,
+                "algorithmic_bytes_per_launch": nvl_bytes,
+                "hbm_bytes_per_launch": hbm_bytes, "hbm_frac": hbm_bytes / (ms * 1e-3) / 1e9 / hbm_peak}
     prof = ROOT / "profiles" / "ncu_traffic.json"
     roof["traffic"] = None
     if prof.exists() and W == 1:  # the committed capture is of the W=1 launch
@@ -401,19 +517,29 @@ def run_coconet(args):
             pass
 
     extras = None
-    if rank == 0 and world == 1 and not args.no_extras:
-        # the other BASELINE configs on this GPU with virtual ranks (kernel and
-        # protocol cost; "NVLink" traffic is local HBM here) - see DESIGN.md
-        try:
-            ctx.close()
-            from tools.pattern_probe import c1, c2_w8, c3, c4, c5, unfused_baselines
-            extras = {"note": "one GPU, virtual ranks: all ranks' traffic is local HBM"}
-            for f in (c1, c2_w8, c3, c4, c5, unfused_baselines):
-                f(extras)
-            if "unfused_torch_foreach_lamb_bert336m_ms" in extras:
-                extras["fused_lamb_speedup_vs_unfused"] = extras["unfused_torch_foreach_lamb_bert336m_ms"] / ms
-        except Exception as e:
-            extras = {"failed": repr(e)}
+    if not args.no_extras:
+        if world == 1:
+            # the other BASELINE configs on this GPU with virtual ranks (kernel and
+            # protocol cost; "NVLink" traffic is local HBM here) - see DESIGN.md
+            try:
+                ctx.close()
+                from tools.pattern_probe import c1, c2_w8, c3, c4, c5
+                extras = {"note": "one GPU, virtual ranks: all ranks' traffic is local HBM"}
+                for fn in (c1, c2_w8, c3, c4, c5):
+                    fn(extras)
+            except Exception as e:
+                extras = {"failed": repr(e)}
+        else:
+            # the other BASELINE configs across the N GPUs, each beside its NCCL baseline
+            try:
+                ctx.close()  # a fresh symmetric heap sized for C5's 3.9e9 fp32 g and p
+                from tools.dist_extras import C5_PARAMS, run_all
+                n5 = C5_PARAMS // (64 if share else 1)
+                ctx = Context(W, mode="distributed", rank=rank, device=local_rank,
+                              heap_bytes=2 * n5 * 4 + 2 * (n5 // W + (1 << 20)) * 4 + (2 << 30))
+                extras = run_all(ctx, nvl_peak, tc_peak)
+            except Exception as e:
+                extras = {"failed": repr(e)[:300]}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -446,14 +572,57 @@ def run_coconet(args):
                             f"pipelined by {len(pipe.groups)} tensor groups (collectives.LambHostPipeline)"},
             "gpu_launches": launches, "clocks": clocks,
             "kernel_ms": ms,
+            "parity": parity,
+            "unfused_baseline": baseline,
             "extras": extras,
-            "nccl_baseline": nccl_baseline,
         }
         print(json.dumps(line))
     if ctx.handle:
         ctx.close()
     if distributed:
         dist.destroy_process_group()
+
+
+def adam_vs_torch(ctx, counts, event_time):
+    """Adam over the BERT-336M list with fp32 grads: the fused FAST kernel
+    (W=1: the TMA ring) vs torch._fused_adam_ (torch's own multi-tensor fused
+    Adam) on the same tensors."""
+    import torch
+
+    from paper_2105_05720_b200.collectives import AdamHParams, TensorList, fused_rs_adam_ag
+
+    g1 = ctx.group(ctx.local_ranks()[0], 1)
+    tl = TensorList(ctx, counts, group=g1, bucket_cap=BUCKET_CAP)
+    bufs_g = [ctx.alloc([n]) for n in counts]
+    bufs_p = [ctx.alloc([n]) for n in counts]
+    m, v = ctx.alloc([tl.shard_elems]), ctx.alloc([tl.shard_elems])
+    r = ctx.local_ranks()[0]
+    for b in bufs_g:
+        ctx.view(b, r).normal_()
+    for b in bufs_p:
+        ctx.view(b, r).uniform_(0.1, 0.9)
+    ctx.view(m, r).zero_()
+    ctx.view(v, r).fill_(1e-3)
+    hp = AdamHParams(1e-3, 0.9, 0.999, 1.0, 1e-8, False, 1, 1)  # FAST, TWO_SHOT
+    fused = lambda: fused_rs_adam_ag(ctx, tl, bufs_g, bufs_p, m, v, hp)  # noqa: E731
+    for _ in range(3):
+        fused()
+    ours = event_time(fused, 10)
+    tp = [ctx.view(b, r) for b in bufs_p]
+    tg = [ctx.view(b, r) for b in bufs_g]
+    tm = [torch.zeros(n, device="cuda") for n in counts]
+    tv = [torch.full((n,), 1e-3, device="cuda") for n in counts]
+    steps = [torch.tensor(1.0, device="cuda") for _ in counts]
+    ref = lambda: torch._fused_adam_(tp, tg, tm, tv, [], steps, amsgrad=False, lr=1e-3, beta1=0.9,  # noqa: E731
+                                     beta2=0.999, weight_decay=0.0, eps=1e-8, maximize=False)
+    for _ in range(3):
+        ref()
+    theirs = event_time(ref, 10)
+    tl.close()
+    for b in bufs_g + bufs_p + [m, v]:
+        ctx.free(b)
+    return {"fused_fast_ms": ours, "torch_fused_adam_ms": theirs, "fused_speedup": theirs / ours,
+            "what": "Adam, BERT-336M list, fp32 grads/params/state, W=1"}
 
 
 def main():
@@ -464,6 +633,8 @@ def main():
     ap.add_argument("--impl", default="coconet", choices=["coconet", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-extras", action="store_true")
+    ap.add_argument("--no-parity", action="store_true")
+    ap.add_argument("--no-baseline", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

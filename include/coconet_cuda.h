@@ -237,6 +237,19 @@ int coconet_fused_rs_lamb_ag(coconet_ctx_t ctx, coconet_tlist_t tl, const void* 
                              int g_elem, float* const* p, float* m_shard, float* v_shard,
                              const coconet_lamb_params* hp, void* stream);
 
+/* The unfused GPU baseline the north star measures against ("NCCL plus
+ * separate kernels"; the paper's LAMB comparison is DDP AllReduce + apex
+ * FusedLAMB): the same LAMB step as FOUR separate multi-tensor
+ * kernels - stage 1 (m', v', u into u_scratch), per-segment L2-norm partials
+ * of p and u, per-tensor combine, stage 2 (p -= ratio*u) - over a list whose
+ * group has ONE rank (after an all-reduce every rank updates every element,
+ * replicated state). m, v, u_scratch: coconet_tlist_shard_elems fp32 each;
+ * norms_scratch: 2 * n_tensors doubles. 46 B/element at fp16 g against the
+ * fused kernel's 38. Same element math as FAST. */
+int coconet_unfused_lamb(coconet_ctx_t ctx, coconet_tlist_t tl, const void* const* g, int g_elem,
+                         float* const* p, float* m, float* v, float* u_scratch, double* norms_scratch,
+                         const coconet_lamb_params* hp, void* stream);
+
 /* ---- collectives (runtime.hpp:306-414, exec_gather_decl :529-557) --------- */
 /* Flat-chunk AllReduce over a tensor list (AR: x -> out, in place allowed),
  * fp32 ring-order reduction; elem = storage type of x and out. This is also

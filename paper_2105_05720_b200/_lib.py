@@ -101,6 +101,7 @@ _SIGNATURES = {
     "coconet_fused_rs_adam_ag": (_I, [_P, _P, _PP, _I, _PP, _P, _P, C.POINTER(AdamParams), _P]),
     "coconet_send": (_I, [_P, _I, _I, _P, _P, _I, _I64, _P]),
     "coconet_convert": (_I, [_P, _P, _I, _P, _I, _I64, _P]),
+    "coconet_unfused_lamb": (_I, [_P, _P, _PP, _I, _PP, _P, _P, _P, _P, C.POINTER(LambParams), _P]),
     "coconet_fused_rs_lamb_ag": (_I, [_P, _P, _PP, _I, _PP, _P, _P, C.POINTER(LambParams), _P]),
     "coconet_allreduce": (_I, [_P, _P, _PP, _PP, _I, _I, _I, _P]),
     "coconet_reduce_scatter": (_I, [_P, _I, _P, _P, _I, _I, _I, _PI64, _I, _P]),

@@ -163,6 +163,26 @@ def fused_rs_lamb_ag(ctx: Context, tl: TensorList, grads, params, m: SymmBuffer,
         C.byref(p), ctx.stream_ptr(stream)))
 
 
+def unfused_lamb(ctx: Context, tl: TensorList, grads, params, m: SymmBuffer, v: SymmBuffer, u: SymmBuffer,
+                 norms: torch.Tensor, hp: LambHParams, stream=None) -> None:
+    """The "separate kernels" baseline (coconet_unfused_lamb): apex FusedLAMB's
+    four multi-tensor passes over a size-1 group's list. `norms` is a device
+    float64 tensor of 2 * n_tensors."""
+    g_elem = elem_of(grads[0].dtype)
+    p = _lib.LambParams(hp.lr, hp.beta1, hp.beta2, hp.t, hp.eps, hp.wd, hp.math, hp.sched, hp.lag_elems,
+                        int(hp.trust_guard))
+    check(ctx.lib.coconet_unfused_lamb(
+        ctx.handle, tl.handle, _ptrs(ctx, grads), g_elem, _ptrs(ctx, params), ctx.ptr(m), ctx.ptr(v), ctx.ptr(u),
+        C.c_void_p(norms.data_ptr()), C.byref(p), ctx.stream_ptr(stream)))
+
+
+def send(ctx: Context, src_group: int, dst_group: int, x: SymmBuffer, out: SymmBuffer, stream=None) -> None:
+    """Send/Recv (runtime.hpp:439-470): group rank r of src_group stores its x
+    into out on group rank r of dst_group."""
+    check(ctx.lib.coconet_send(ctx.handle, src_group, dst_group, ctx.ptr(x), ctx.ptr(out), elem_of(x.dtype),
+                               x.numel, ctx.stream_ptr(stream)))
+
+
 def allreduce(ctx: Context, tl: TensorList, xs, outs, reducer: int = _lib.SUM,
               algo: int = _lib.ALGO_AUTO, stream=None) -> None:
     """Tensor-list AllReduce (runtime.hpp:384-395; scattered_collective :624-675)."""
