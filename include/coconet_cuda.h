@@ -229,8 +229,12 @@ enum coconet_lamb_sched {
   COCONET_LAMB_AUTO = 0,
   COCONET_LAMB_GRID = 1,
   COCONET_LAMB_STREAMED = 2,
-  COCONET_LAMB_TMA = 3 /* GRID's two passes fed by TMA bulk copies into a shared-memory ring
+  COCONET_LAMB_TMA = 3, /* GRID's two passes fed by TMA bulk copies into a shared-memory ring
                           (norms summed in a different fixed order) */
+  COCONET_LAMB_WINDOWED = 4 /* group size 1: the TMA ring over windows of consecutive tensors
+                               (lag_elems = window size), pass 2 of a window one window after
+                               its pass 1 so its m, v, p re-reads hit L2; per-window arrival
+                               counters instead of grid-wide syncs. m, v bit-identical to TMA */
 };
 
 int coconet_fused_rs_lamb_ag(coconet_ctx_t ctx, coconet_tlist_t tl, const void* const* g,

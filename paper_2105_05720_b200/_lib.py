@@ -16,7 +16,7 @@ F32, F16, BF16 = 0, 1, 2
 SUM, MAX, MIN = 0, 1, 2
 MATH_EXACT, MATH_FAST = 0, 1
 ALGO_AUTO, ALGO_TWO_SHOT, ALGO_ONE_SHOT = 0, 1, 2
-LAMB_AUTO, LAMB_GRID, LAMB_STREAMED, LAMB_TMA = 0, 1, 2, 3
+LAMB_AUTO, LAMB_GRID, LAMB_STREAMED, LAMB_TMA, LAMB_WINDOWED = 0, 1, 2, 3, 4
 MODE_VIRTUAL, MODE_DISTRIBUTED = 0, 1
 MAX_RANKS = 8
 

@@ -1004,6 +1004,372 @@ __global__ void __launch_bounds__((NW + 1) * 32, 2) lamb_tma_kernel(OptArgs a, L
   edge_barrier(rs, 1);
 }
 
+// ---- LAMB, WINDOWED TMA schedule (group size 1). GRID/TMA read m, v and p
+// twice from HBM (38 B/element at fp16 g) because pass 2 of ANY tensor waits
+// for pass 1 of EVERY tensor (one grid-wide sync). Here the tensors are cut
+// into windows of consecutive tensors (tlist_window_plan) and the persistent
+// grid runs the phases
+//     P1(w0); then per window w: P1head(w+1), P2(w), P1tail(w+1)
+// so a window's pass 2 re-reads its m, v, p right after its pass 1 (plus a
+// short head of the next window that covers the synchronisation), while
+// they can still be in the 126 MB L2 (compulsory traffic: 26 B/element).
+// Work is handed out DYNAMICALLY in batches of 4 chunk items (an atomic
+// ticket per window and pass), so every CTA finishes a window within about
+// one batch of the others. The producer warp draws the tickets and passes
+// each chunk's descriptor to the consumers through shared memory next to its
+// TMA stage. The CTA that completes a window's pass 1 last sums the per-item
+// norm partials (fixed item order: deterministic) into per-tensor trust
+// ratios and releases ready[w]; P2(w) waits for it. Deadlock-free: ready[w]
+// needs only P1(w) items, all handed out before any CTA first waits; all CTAs
+// are co-resident (cooperative launch). Element math is the TMA kernel's, so
+// m, v are bit-identical to it and p equal within rounding of the norm sums.
+struct LambWin {
+  const int64_t* items;  // segment | chunk << 40, window by window, tensor-major
+  const int64_t* wi;     // [K+1] window k = items [wi[k], wi[k+1])
+  const int64_t* titem;  // [n_tensors+1] items of tensor t
+  const int* tfirst;     // [K+1] window k = tensors [tfirst[k], tfirst[k+1])
+  unsigned long long* tick;  // [K][2] cumulative tickets (batches) of P1 / P2
+  uint32_t* cnt;         // [K] cumulative pass-1 arrivals
+  uint32_t* ready;       // [K] = call once the window's ratios are published
+  float2* ipart;         // [n_items] per-item CTA norm partials (sum p^2, sum u^2)
+  float* ratio;          // [n_tensors]
+  int K;
+  uint32_t call;         // calls since the plan (and grid size) was set, this one included
+  int64_t head;          // items of window w+1 run before P2(w)
+};
+
+constexpr int kWinBatch = 4;  // chunk items per ticket
+
+// Phase j of: P1(0); then per window w: P1head(w+1), P2(w), P1tail(w+1)
+// (the last window: P2 only). part: 0 whole, 1 head, 2 tail. 3K - 1 phases.
+__device__ __forceinline__ void win_phase(int j, int K, int& pass, int& w, int& part) {
+  if (j == 0) {
+    pass = 0;
+    w = 0;
+    part = 0;
+    return;
+  }
+  const int i = j - 1;
+  const int ww = i / 3, r = i - 3 * ww;
+  if (ww == K - 1 || r == 1) {
+    pass = 1;
+    w = ww;
+    part = 0;
+  } else {
+    pass = 0;
+    w = ww + 1;
+    part = r == 0 ? 1 : 2;
+  }
+}
+
+// Spin (relaxed polls: no L1 invalidation per poll) until *p == want, then
+// ONE acquire fence.
+__device__ __forceinline__ void wait_equal(const uint32_t* p, uint32_t want, const RankSet& rs) {
+  uint32_t v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  if (v != want) {
+    const unsigned long long t0 = globaltimer();
+    do {
+      __nanosleep(64);
+      asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+      if (globaltimer() - t0 > rs.timeout_ns) {
+        atomicCAS(rs.status, 0, COCONET_ERR_TIMEOUT);
+        break;
+      }
+    } while (v != want);
+  }
+  asm volatile("fence.acq_rel.gpu;" ::: "memory");
+}
+
+// Chunk descriptor handed from the producer to the consumers with its stage.
+struct ChunkD {
+  int64_t toff, sidx, aoff, boff, item;  // item < 0: end of this CTA's phase
+  int len, tensor, chunk, pad_;
+};
+
+__device__ __forceinline__ ChunkD load_chunk(const OptArgs& a, const int64_t* items, int64_t item) {
+  ChunkD d;
+  const int64_t it = items[item];
+  const Seg sg = a.segs[it & ((int64_t(1) << 40) - 1)];
+  d.item = item;
+  d.chunk = int(it >> 40);
+  d.toff = sg.toff;
+  d.sidx = sg.sidx;
+  d.len = meta_len(sg.meta);
+  d.tensor = meta_tensor(sg.meta);
+  d.aoff = a.offs[d.tensor];
+  d.boff = a.offs[a.n_tensors + d.tensor];
+  d.pad_ = 0;
+  return d;
+}
+
+template <typename G, int NW, int QPT>
+__global__ void __launch_bounds__((NW + 1) * 32, 2) lamb_win_kernel(OptArgs a, LambK k, TmaArgs ta, LambWin lw) {
+  using ST = TmaStage<G, NW, QPT>;
+  constexpr int kChunkQ = ST::CHUNK_Q;
+  constexpr int kMaxStages = 16;
+  extern __shared__ __align__(128) uint8_t smem_raw[];
+  __shared__ char* s_base[kMaxRanks];
+  __shared__ float s_red[2][NW][2];
+  __shared__ ChunkD s_desc[kMaxStages];
+  __shared__ int s_last;
+  __shared__ double s_blk[2][NW];
+  const RankSet& rs = a.rs;
+  if (threadIdx.x < kMaxRanks) s_base[threadIdx.x] = threadIdx.x < rs.world ? rs.base[threadIdx.x] : nullptr;
+  const int S = ta.stages;
+  uint8_t* stage0 = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
+  uint64_t* full = reinterpret_cast<uint64_t*>(stage0 + size_t(S) * ST::BYTES);
+  uint64_t* empty = full + S;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < S; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], NW);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  const int me = rs.rank();
+  edge_barrier(rs, 0);  // publishes the barrier inits to the CTA (group size 1: no peer)
+  float* m = reinterpret_cast<float*>(s_base[me] + a.m_off);
+  float* v = reinterpret_cast<float*>(s_base[me] + a.v_off);
+  char* pme = s_base[me];
+  const bool producer = warp == NW;
+  const int ctid = threadIdx.x;
+  const unsigned long long NG = gridDim.x;
+  uint32_t st = 0, ph = 0;
+  int red = 0;
+  long long pend = -1;  // producer: the head's overshooting ticket, kept for the tail
+  for (int j = 0; j < 3 * lw.K - 1; ++j) {
+    int pass, w, part;
+    win_phase(j, lw.K, pass, w, part);
+    const int64_t wb = lw.wi[w], n = lw.wi[w + 1] - wb;
+    const long long nbat = (n + kWinBatch - 1) / kWinBatch;
+    if (pass == 1 && lane == 0) wait_equal(&lw.ready[w], lw.call, rs);  // the window's ratios are out
+    __syncwarp();
+    if (producer) {
+      if (lane == 0) {
+        if (pass == 1) asm volatile("fence.proxy.async.global;" ::: "memory");  // other CTAs' m, v stores
+        unsigned long long* tk = &lw.tick[2 * w + pass];
+        const unsigned long long base = (unsigned long long)(lw.call - 1) * ((unsigned long long)nbat + NG);
+        const long long lim = part == 1 ? min(nbat, (long long)(lw.head / kWinBatch)) : nbat;
+        long long t;
+        if (part == 2) {  // the head's overshoot, or its failing draw (-2) already happened
+          t = pend >= 0 ? pend : nbat;
+          pend = -1;
+        } else {
+          t = (long long)(atomicAdd(tk, 1ull) - base);
+        }
+        while (t < lim) {
+          const long long nxt = (long long)(atomicAdd(tk, 1ull) - base);  // in flight while t's chunks go out
+          for (int q = 0; q < kWinBatch; ++q) {
+            const int64_t item = t * kWinBatch + q;
+            if (item >= n) break;
+            const ChunkD d = load_chunk(a, lw.items, wb + item);
+            const int64_t qa = (d.toff >> 2) + int64_t(d.chunk) * kChunkQ;
+            const int64_t qb = min(qa + int64_t(kChunkQ), (d.toff + d.len + 3) >> 2);
+            mbar_wait(&empty[st], ph ^ 1u);
+            s_desc[st] = d;
+            uint8_t* dst = stage0 + size_t(st) * ST::BYTES;
+            const uint32_t abytes = uint32_t(qb - qa) * 16u;
+            const char* ga = pme + d.aoff + qa * 4 * int64_t(sizeof(G));
+            const char* g0 = reinterpret_cast<const char*>(reinterpret_cast<uintptr_t>(ga) & ~uintptr_t(15));
+            const char* g1 = reinterpret_cast<const char*>(
+                (reinterpret_cast<uintptr_t>(pme + d.aoff + qb * 4 * int64_t(sizeof(G))) + 15) & ~uintptr_t(15));
+            const uint32_t gbytes = pass == 0 ? uint32_t(g1 - g0) : 0u;
+            const int64_t si = d.sidx + (qa * 4 - d.toff);
+            mbar_expect_tx(&full[st], gbytes + 3u * abytes);
+            if (pass == 0) bulk_load(dst, g0, gbytes, &full[st]);
+            bulk_load(dst + ST::G_BYTES, m + si, abytes, &full[st]);
+            bulk_load(dst + ST::G_BYTES + ST::A_BYTES, v + si, abytes, &full[st]);
+            bulk_load(dst + ST::G_BYTES + 2 * ST::A_BYTES, pme + d.boff + qa * 16, abytes, &full[st]);
+            if (++st == uint32_t(S)) {
+              st = 0;
+              ph ^= 1u;
+            }
+          }
+          t = nxt;
+        }
+        if (part == 1) pend = t < nbat ? t : -2;  // the head's overshoot belongs to the tail
+        // end of this CTA's phase: an empty stage with an end marker
+        mbar_wait(&empty[st], ph ^ 1u);
+        s_desc[st].item = -1;
+        mbar_arrive(&full[st]);
+        if (++st == uint32_t(S)) {
+          st = 0;
+          ph ^= 1u;
+        }
+      }
+      __syncwarp();
+      st = __shfl_sync(0xffffffffu, st, 0);
+      ph = __shfl_sync(0xffffffffu, ph, 0);
+      continue;
+    }
+    // ---- consumers
+    int ratio_t = -1;
+    float ratio = 0.f;
+    for (;;) {
+      mbar_wait(&full[st], ph);
+      const ChunkD d0 = s_desc[st];
+      if (d0.item < 0) {
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[st]);
+        if (++st == uint32_t(S)) {
+          st = 0;
+          ph ^= 1u;
+        }
+        break;
+      }
+      const SegD d{d0.toff, d0.sidx, d0.aoff, d0.boff, d0.len, me, d0.tensor};
+      if (pass == 1 && d0.tensor != ratio_t) {
+        ratio = __ldcg(&lw.ratio[d0.tensor]);
+        ratio_t = d0.tensor;
+      }
+      const int64_t qa = (d.toff >> 2) + int64_t(d0.chunk) * kChunkQ;
+      const int64_t qb = min(qa + int64_t(kChunkQ), (d.toff + d.len + 3) >> 2);
+      const uint8_t* src = stage0 + size_t(st) * ST::BYTES;
+      float sp = 0.f, su = 0.f;
+#pragma unroll
+      for (int qq = 0; qq < QPT; ++qq) {
+        const int64_t q = qa + ctid + qq * (NW * 32);
+        if (q < qb) {
+          const int64_t e0 = q << 2;
+          int lo, hi;
+          quad_range(d, e0, lo, hi);
+          const int64_t si = d.sidx + (e0 - d.toff);
+          const float4 mq = *reinterpret_cast<const float4*>(src + ST::G_BYTES + (q - qa) * 16);
+          const float4 vq = *reinterpret_cast<const float4*>(src + ST::G_BYTES + ST::A_BYTES + (q - qa) * 16);
+          const float4 pq = *reinterpret_cast<const float4*>(src + ST::G_BYTES + 2 * ST::A_BYTES + (q - qa) * 16);
+          float mm[4] = {mq.x, mq.y, mq.z, mq.w}, vv[4] = {vq.x, vq.y, vq.z, vq.w},
+                pp[4] = {pq.x, pq.y, pq.z, pq.w};
+          if (pass == 0) {
+            const uintptr_t ga = reinterpret_cast<uintptr_t>(pme + d.aoff + qa * 4 * int64_t(sizeof(G)));
+            const uintptr_t goff = (ga & 15u) + uintptr_t(q - qa) * 4u * sizeof(G);
+            float gs[4];
+            if constexpr (sizeof(G) == 4) {
+              const float4 gq = *reinterpret_cast<const float4*>(src + goff);
+              gs[0] = gq.x; gs[1] = gq.y; gs[2] = gq.z; gs[3] = gq.w;
+            } else {
+              const uint2 gq = *reinterpret_cast<const uint2*>(src + goff);
+              const G* h = reinterpret_cast<const G*>(&gq);
+#pragma unroll
+              for (int i = 0; i < 4; ++i) gs[i] = to_f32(h[i]);
+            }
+            float fp = 0.f, fu = 0.f;
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              const float mn = fmaf(k.fcm, gs[i], mm[i] * k.fb1);
+              const float vn = fmaf(k.fcv * gs[i], gs[i], vv[i] * k.fb2);
+              mm[i] = mn;
+              vv[i] = vn;
+              if (i >= lo && i < hi) {
+                const float uu = lamb_u(mn, vn, pp[i], k);
+                fp = fmaf(pp[i], pp[i], fp);
+                fu = fmaf(uu, uu, fu);
+              }
+            }
+            sp += fp;
+            su += fu;
+            st4m(m + si, mm, lo, hi);
+            st4m(v + si, vv, lo, hi);
+          } else {
+            float pn[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) pn[i] = pp[i] - ratio * lamb_u(mm[i], vv[i], pp[i], k);
+            st4m(reinterpret_cast<float*>(pme + d.boff) + e0, pn, lo, hi);
+          }
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[st]);
+      if (++st == uint32_t(S)) {
+        st = 0;
+        ph ^= 1u;
+      }
+      if (pass == 0) {  // the item's norm partial, CTA-reduced in fixed order
+        sp = warp_sumf(sp);
+        su = warp_sumf(su);
+        if (lane == 0) {
+          s_red[red][warp][0] = sp;
+          s_red[red][warp][1] = su;
+        }
+        asm volatile("bar.sync 1, %0;" ::"n"(NW * 32) : "memory");
+        if (ctid == 0) {
+          float tp = 0.f, tu = 0.f;
+#pragma unroll
+          for (int ww = 0; ww < NW; ++ww) {
+            tp += s_red[red][ww][0];
+            tu += s_red[red][ww][1];
+          }
+          lw.ipart[d0.item] = make_float2(tp, tu);
+        }
+        red ^= 1;
+      }
+    }
+    if (pass == 0 && part != 1) {  // this CTA is done with the window's pass 1
+      asm volatile("fence.proxy.async.global;" ::: "memory");  // m, v stores before their bulk readers
+      asm volatile("bar.sync 1, %0;" ::"n"(NW * 32) : "memory");
+      if (ctid == 0) {
+        __threadfence();
+        const uint32_t old = atomicAdd(&lw.cnt[w], 1u);
+        const int last = old + 1u == lw.call * uint32_t(gridDim.x);
+        if (last) __threadfence();
+        s_last = last;
+      }
+      asm volatile("bar.sync 1, %0;" ::"n"(NW * 32) : "memory");
+      if (s_last) {
+        // the window's per-tensor trust ratios from the per-item partials in
+        // item order: big tensors with every consumer thread, small ones a warp each
+        for (int t = lw.tfirst[w]; t < lw.tfirst[w + 1]; ++t) {
+          const int64_t i0 = lw.titem[t], i1 = lw.titem[t + 1];
+          if (i1 - i0 <= 64) continue;
+          double P = 0.0, U = 0.0;
+          for (int64_t i = i0 + ctid; i < i1; i += NW * 32) {
+            const float2 pu = __ldcg(&lw.ipart[i]);
+            P += double(pu.x);
+            U += double(pu.y);
+          }
+          P = warp_sum(P);
+          U = warp_sum(U);
+          if (lane == 0) {
+            s_blk[0][warp] = P;
+            s_blk[1][warp] = U;
+          }
+          asm volatile("bar.sync 1, %0;" ::"n"(NW * 32) : "memory");
+          if (ctid == 0) {
+            double tp = 0.0, tu = 0.0;
+            for (int ww = 0; ww < NW; ++ww) {
+              tp += s_blk[0][ww];
+              tu += s_blk[1][ww];
+            }
+            lw.ratio[t] = float(trust_ratio(tp, tu, k));
+          }
+          asm volatile("bar.sync 1, %0;" ::"n"(NW * 32) : "memory");
+        }
+        for (int t = lw.tfirst[w] + warp; t < lw.tfirst[w + 1]; t += NW) {
+          const int64_t i0 = lw.titem[t], i1 = lw.titem[t + 1];
+          if (i1 - i0 > 64) continue;
+          double P = 0.0, U = 0.0;
+          for (int64_t i = i0 + lane; i < i1; i += 32) {
+            const float2 pu = __ldcg(&lw.ipart[i]);
+            P += double(pu.x);
+            U += double(pu.y);
+          }
+          P = warp_sum(P);
+          U = warp_sum(U);
+          if (lane == 0) lw.ratio[t] = float(trust_ratio(P, U, k));
+        }
+        asm volatile("bar.sync 1, %0;" ::"n"(NW * 32) : "memory");
+        if (ctid == 0) {
+          __threadfence();
+          st_release_sys(&lw.ready[w], lw.call);
+        }
+      }
+    }
+  }
+  edge_barrier(rs, 1);
+}
+
 // ---- Adam, TMA schedule (W = 1): one pass, the producer of lamb_tma_kernel
 // streaming g, m, v, p into the shared-memory ring and NW consumer warps
 // applying adam_elem (EXACT or FAST) and writing m, v, p.
@@ -1539,6 +1905,9 @@ constexpr int64_t kDefaultLag = int64_t(1) << 21;
 // 2.4 ms), from 4096 up it wins (LAMB 2.06 vs 2.26 ms, Adam EXACT 2.0 vs
 // 2.5 ms at 16384). Group size 1 only (peer bulk copies untested).
 constexpr int64_t kTmaMinBucket = 4096;
+// WINDOWED LAMB: elements per window (COCONET_LAMB_WIN_ELEMS or
+// coconet_lamb_params.lag_elems override it)
+constexpr int64_t kDefaultWindow = int64_t(2) << 20;
 
 int check_state(coconet_ctx* c, const void* ptr, int64_t* off) {
   int rc = heap_offset(c, ptr, off);
@@ -1652,7 +2021,7 @@ int coconet_fused_rs_lamb_ag(coconet_ctx_t c, coconet_tlist_t tl, const void* co
   if (tl->ctx != c) return set_error(COCONET_ERR_INVALID_INPUT, "tensor list belongs to another context");
   if (hp->math != COCONET_MATH_FAST && hp->math != COCONET_MATH_EXACT)
     return set_error(COCONET_ERR_INVALID_INPUT, "bad math");
-  if (hp->sched < COCONET_LAMB_AUTO || hp->sched > COCONET_LAMB_TMA)
+  if (hp->sched < COCONET_LAMB_AUTO || hp->sched > COCONET_LAMB_WINDOWED)
     return set_error(COCONET_ERR_INVALID_INPUT, "bad LAMB schedule");
   // exchange [rank][tensor] (P, U) doubles + ready flags [rank][tensor]
   if (size_t(kMaxRanks) * tl->n_tensors * (2 * sizeof(double) + sizeof(uint32_t)) > kTileFlagsOff)
@@ -1704,6 +2073,60 @@ int coconet_fused_rs_lamb_ag(coconet_ctx_t c, coconet_tlist_t tl, const void* co
   }
   const bool tma_auto = tl->bucket_cap >= (W == 1 ? kTmaMinBucket : 4 * kTmaMinBucket);
   const int sched = hp->sched == COCONET_LAMB_AUTO ? (tma_auto ? COCONET_LAMB_TMA : COCONET_LAMB_GRID) : hp->sched;
+  if (sched == COCONET_LAMB_WINDOWED) {
+    if (W != 1) return set_error(COCONET_ERR_UNSUPPORTED, "the WINDOWED LAMB schedule runs at group size 1");
+    const char* we = getenv("COCONET_LAMB_WIN_ELEMS");
+    const int64_t win = hp->lag_elems > 0 ? hp->lag_elems : (we ? atoll(we) : kDefaultWindow);
+    rc = tlist_window_plan(tl, win, TmaStage<float, 8, 2>::CHUNK_Q);
+    if (rc) return rc;
+    const char* ce = getenv("COCONET_LAMB_TMA_CTAS");
+    const int per_sm = ce ? std::max(1, std::min(4, atoi(ce))) : 3;
+    const void* fn = nullptr;
+    int sbytes = 0, threads = 0;
+    auto pick = [&](auto tag_g) {
+      using Gt = decltype(tag_g);
+      using ST = TmaStage<Gt, 8, 2>;
+      fn = reinterpret_cast<const void*>(&lamb_win_kernel<Gt, 8, 2>);
+      sbytes = ST::BYTES;
+      threads = ST::THREADS;
+    };
+    if (g_elem == COCONET_F32) pick(float{});
+    else if (g_elem == COCONET_F16) pick(__half{});
+    else pick(__nv_bfloat16{});
+    TmaArgs ta;
+    ta.stages = std::min(16, (200 << 10) / per_sm / sbytes);
+    if (ta.stages < 2) return set_error(COCONET_ERR_UNSUPPORTED, "TMA ring does not fit");
+    const size_t smem = size_t(ta.stages) * size_t(sbytes) + size_t(ta.stages) * 16 + 128;
+    rc = ensure_smem(c, fn, smem);
+    if (rc) return rc;
+    int blocks = 0;
+    rc = coop_blocks(c, fn, threads, smem, tl->group, int64_t(c->sm_count) * per_sm, &blocks);
+    if (rc) return rc;
+    if (ta.stages > 16) ta.stages = 16;
+    LambWin lw;
+    lw.items = tl->d_win_items;
+    lw.wi = tl->d_win_item;
+    lw.titem = tl->d_titem;
+    lw.tfirst = tl->d_win_t;
+    lw.tick = tl->d_win_tick;
+    lw.cnt = tl->d_win_cnt;
+    lw.ready = tl->d_win_ready;
+    lw.ipart = tl->d_ipart;
+    lw.ratio = tl->d_ratio;
+    lw.K = tl->n_windows;
+    // tickets, arrivals and ready flags are cumulative over calls (no reset
+    // kernel): restart them when the grid size changes
+    if (tl->win_blocks != blocks) {
+      CN_CUDA(cudaMemsetAsync(tl->win_state, 0, tl->win_state_bytes, stream));
+      tl->win_blocks = blocks;
+      tl->win_calls = 0;
+    }
+    lw.call = ++tl->win_calls;
+    const char* he = getenv("COCONET_LAMB_WIN_HEAD");
+    lw.head = int64_t(he ? std::max(0, atoi(he)) : 2) * blocks * kWinBatch;
+    void* args[] = {&a, &k, &ta, &lw};
+    return coop_launch(c, fn, dim3(unsigned(blocks), 1u), dim3(unsigned(threads)), args, smem, stream);
+  }
   if (sched == COCONET_LAMB_TMA) {
     // 8 consumer warps x 2 quads per thread (2048-element chunks), 3 CTAs
     // per SM: the best of the sweep in profiles/r01_lamb_tma_sweep.json

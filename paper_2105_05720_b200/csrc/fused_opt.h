@@ -71,12 +71,36 @@ struct coconet_tlist {
   uint32_t* d_cnt = nullptr;             // [rank][tensor] pass-1 completion counters
   double* d_item_part = nullptr;         // per pass-1 item: sum p^2, sum u^2
   uint32_t stream_calls = 0;
+  // WINDOWED LAMB schedule (W = 1): consecutive-tensor windows of about
+  // win_elems elements, cut into chunk items (built on first use,
+  // tlist_window_plan)
+  int64_t win_elems = -1;
+  int win_chunk_q = 0;
+  int n_windows = 0;
+  int64_t n_items = 0;
+  void* win_mem = nullptr;
+  int64_t* d_win_items = nullptr;  // [n_items] segment | chunk << 40, window by window, tensor-major
+  int64_t* d_win_item = nullptr;   // [K+1] item range of each window
+  int64_t* d_titem = nullptr;      // [n_tensors+1] item range of each tensor
+  int* d_win_t = nullptr;          // [K+1] first tensor of each window
+  float2* d_ipart = nullptr;       // [n_items] per-item norm partials
+  float* d_ratio = nullptr;        // [n_tensors] trust ratios
+  void* win_state = nullptr;       // the cumulative counters below, zeroed together
+  size_t win_state_bytes = 0;
+  unsigned long long* d_win_tick = nullptr;  // [K][2] tickets
+  uint32_t* d_win_cnt = nullptr;   // [K] pass-1 arrivals
+  uint32_t* d_win_ready = nullptr; // [K] call number once a window's ratios are published
+  uint32_t win_calls = 0;
+  int win_blocks = 0;              // grid size the counters were advanced with
 };
 
 namespace coconet {
 // Builds (or keeps) the STREAMED-LAMB work lists for a pass-1 -> pass-2 lag
 // of `lag` elements; uploads them when the list has a device table.
 int tlist_stream_plan(coconet_tlist* tl, int64_t lag);
+// Builds (or keeps) the WINDOWED-LAMB windows for a target window size and
+// chunk items of chunk_q quads.
+int tlist_window_plan(coconet_tlist* tl, int64_t win_elems, int chunk_q);
 int tlist_bind(coconet_tlist* tl, const void* const* a, const void* const* b, int a_elem_bytes,
                int b_elem_bytes, cudaStream_t stream);
 }

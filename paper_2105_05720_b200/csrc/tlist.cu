@@ -212,9 +212,10 @@ int coconet_tlist_plan(int world, int n_tensors, const int64_t* counts, int64_t 
 
 int coconet_tlist_destroy(coconet_tlist_t tl) {
   if (!tl) return COCONET_OK;
-  if (tl->dev_mem || tl->stream_mem) cudaDeviceSynchronize();
+  if (tl->dev_mem || tl->stream_mem || tl->win_mem) cudaDeviceSynchronize();
   if (tl->dev_mem) cudaFree(tl->dev_mem);
   if (tl->stream_mem) cudaFree(tl->stream_mem);
+  if (tl->win_mem) cudaFree(tl->win_mem);
   delete tl;
   return COCONET_OK;
 }
@@ -379,6 +380,78 @@ int tlist_stream_plan(coconet_tlist* tl, int64_t lag) {
 // Uploads per-tensor heap offsets of the g/x and p/out tensors when they
 // changed since the last call (pageable source: the copy is staged before
 // cudaMemcpyAsync returns, and it is stream-ordered after earlier kernels).
+// Windows of consecutive tensors (rank 0's CSR order) holding about
+// win_elems elements each (a tensor larger than that is a window alone), and
+// their chunk items: every segment of the window's tensors, tensor by tensor,
+// cut into chunks of chunk_q quads (segment | chunk << 40), so the persistent
+// grid splits a window evenly by chunks.
+int tlist_window_plan(coconet_tlist* tl, int64_t win_elems, int chunk_q) {
+  if (tl->win_elems == win_elems && tl->win_chunk_q == chunk_q && tl->win_mem) return COCONET_OK;
+  const int64_t* ptr = tl->csr_ptr.data() + tl->csr_begin[0];
+  std::vector<int64_t> items, win_item{0}, titem{0};
+  std::vector<int> win_t{0};
+  int64_t acc = 0;
+  for (int t = 0; t < tl->n_tensors; ++t) {
+    for (int64_t i = ptr[t]; i < ptr[t + 1]; ++i) {
+      const int64_t s = tl->csr_idx[size_t(i)];
+      const Seg& sg = tl->table[size_t(s)];
+      const int64_t q0 = sg.toff >> 2, q1 = (sg.toff + meta_len(sg.meta) + 3) >> 2;
+      for (int64_t k = 0; q0 + k * chunk_q < q1; ++k) items.push_back(s | (k << 40));
+    }
+    titem.push_back(int64_t(items.size()));
+    acc += tl->counts[size_t(t)];
+    if (acc >= win_elems || t == tl->n_tensors - 1) {
+      win_item.push_back(int64_t(items.size()));
+      win_t.push_back(t + 1);
+      acc = 0;
+    }
+  }
+  const int K = int(win_item.size()) - 1;
+  if (tl->win_mem) {
+    cudaDeviceSynchronize();
+    cudaFree(tl->win_mem);
+    tl->win_mem = nullptr;
+  }
+  const size_t b_items = std::max<size_t>(1, items.size()) * sizeof(int64_t);
+  const size_t b_wi = size_t(K + 1) * sizeof(int64_t), b_ti = size_t(tl->n_tensors + 1) * sizeof(int64_t);
+  const size_t b_wt = size_t(K + 1) * sizeof(int), b_part = std::max<size_t>(1, items.size()) * sizeof(float2);
+  const size_t b_ratio = size_t(tl->n_tensors) * sizeof(float);
+  const size_t b_tick = size_t(K) * 2 * sizeof(unsigned long long), b_cnt = size_t(K) * sizeof(uint32_t);
+  const size_t b_state = (b_tick + 15) / 16 * 16 + 2 * ((b_cnt + 15) / 16 * 16);
+  const size_t total = b_items + b_wi + b_ti + b_wt + b_part + b_ratio + b_state + 8 * 16;
+  CN_CUDA(cudaMalloc(&tl->win_mem, total));
+  CN_CUDA(cudaMemset(tl->win_mem, 0, total));
+  char* p = static_cast<char*>(tl->win_mem);
+  auto carve = [&](size_t n) {
+    char* q = p;
+    p += (n + 15) / 16 * 16;
+    return q;
+  };
+  tl->d_win_items = reinterpret_cast<int64_t*>(carve(b_items));
+  tl->d_win_item = reinterpret_cast<int64_t*>(carve(b_wi));
+  tl->d_titem = reinterpret_cast<int64_t*>(carve(b_ti));
+  tl->d_win_t = reinterpret_cast<int*>(carve(b_wt));
+  tl->d_ipart = reinterpret_cast<float2*>(carve(b_part));
+  tl->d_ratio = reinterpret_cast<float*>(carve(b_ratio));
+  tl->win_state = p;
+  tl->win_state_bytes = b_state;
+  tl->d_win_tick = reinterpret_cast<unsigned long long*>(carve(b_tick));
+  tl->d_win_cnt = reinterpret_cast<uint32_t*>(carve(b_cnt));
+  tl->d_win_ready = reinterpret_cast<uint32_t*>(carve(b_cnt));
+  if (!items.empty())
+    CN_CUDA(cudaMemcpy(tl->d_win_items, items.data(), items.size() * sizeof(int64_t), cudaMemcpyHostToDevice));
+  CN_CUDA(cudaMemcpy(tl->d_win_item, win_item.data(), b_wi, cudaMemcpyHostToDevice));
+  CN_CUDA(cudaMemcpy(tl->d_titem, titem.data(), b_ti, cudaMemcpyHostToDevice));
+  CN_CUDA(cudaMemcpy(tl->d_win_t, win_t.data(), b_wt, cudaMemcpyHostToDevice));
+  tl->win_elems = win_elems;
+  tl->win_chunk_q = chunk_q;
+  tl->n_windows = K;
+  tl->n_items = int64_t(items.size());
+  tl->win_calls = 0;
+  tl->win_blocks = 0;
+  return COCONET_OK;
+}
+
 int tlist_bind(coconet_tlist* tl, const void* const* a, const void* const* b, int a_elem_bytes,
                int b_elem_bytes, cudaStream_t stream) {
   const coconet_ctx* c = tl->ctx;
