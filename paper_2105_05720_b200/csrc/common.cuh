@@ -174,6 +174,12 @@ __device__ __forceinline__ bool wait_flag(const uint32_t* p, uint32_t want, cons
 // Pairwise barrier between this CTA and the CTA with the same blockIdx.x on
 // every other rank of the group: thread q < W signals rank q and waits for
 // rank q. `fence` orders this CTA's prior (remote) writes before the signal.
+// The waiter resets the slot it consumed to 0, so a slot is always 0 before
+// its next use (the peer's next signal into it comes only after this rank
+// reached a later barrier of the same launch, or the entry barrier of the
+// next one; every barrier of a launch uses its own phase). The protocol
+// therefore does not depend on the host's epoch advancing: a launch
+// captured in a CUDA graph replays correctly with its baked-in epoch.
 __device__ __forceinline__ bool rank_barrier(const RankSet& rs, int phase) {
   if (rs.world == 1) {  // no peer to meet
     __syncthreads();
@@ -186,7 +192,9 @@ __device__ __forceinline__ bool rank_barrier(const RankSet& rs, int phase) {
   if (q < rs.world) {
     __threadfence_system();
     st_release_sys(flag_slot(rs.base[q], rs.group, phase, me, blockIdx.x), rs.epoch);
-    ok = wait_flag(flag_slot(rs.base[me], rs.group, phase, q, blockIdx.x), rs.epoch, rs);
+    uint32_t* mine = flag_slot(rs.base[me], rs.group, phase, q, blockIdx.x);
+    ok = wait_flag(mine, rs.epoch, rs);
+    if (ok) *reinterpret_cast<volatile uint32_t*>(mine) = 0u;  // consumed
   }
   return __syncthreads_and(ok);
 }

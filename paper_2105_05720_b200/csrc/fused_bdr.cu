@@ -358,12 +358,17 @@ int coconet_rs_fused_send_ag(coconet_ctx_t c, int src_group, int dst_group, cons
       hp->math == COCONET_MATH_EXACT ? pp_fn<COCONET_MATH_EXACT>(elem, v16, gs.size)
                                      : pp_fn<COCONET_MATH_FAST>(elem, v16, gs.size);
   const int vn = v16 ? 8 : 4;
+  // Only the source stage computes. VIRTUAL: the grid covers the S sender
+  // ranks only (blockIdx.y = union rank < S), so every resident CTA moves
+  // data (the destination ranks' CTAs would only meet no-op edge barriers);
+  // DISTRIBUTED: every process launches its own rank (receivers take part in
+  // the entry/exit barriers).
   int blocks = 0;
-  rc = coop_blocks(c, fn, kThreads, 0, ug, (n / gs.size / vn + kThreads - 1) / kThreads, &blocks);
+  rc = coop_blocks(c, fn, kThreads, 0, src_group, (n / gs.size / vn + kThreads - 1) / kThreads, &blocks);
   if (!rc) rc = make_rankset(c, ug, &a.rs);
   if (rc) return rc;
   void* args[] = {&a, &k};
-  return coop_launch(c, fn, dim3(unsigned(blocks), unsigned(local_ranks(c, ug))), dim3(kThreads), args, 0,
+  return coop_launch(c, fn, dim3(unsigned(blocks), unsigned(local_ranks(c, src_group))), dim3(kThreads), args, 0,
                      static_cast<cudaStream_t>(stream));
 }
 

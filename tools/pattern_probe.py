@@ -80,6 +80,17 @@ def c1(out):
             # ranks and pushes p to W ranks (8N), plus m, v, p read and m, v
             # written on its own chunk (20N/W): (8W + 20) N in total
             out[f"c1_adam_W4_N2^20_{name}_{an}_device_cold_GBs"] = (8 * W + 20) * N / (dev * 1e-3) / 1e9
+            # the same call captured in a CUDA graph, 20 calls per replay:
+            # no Python or C-ABI host time per call (the small-message floor)
+            gr = torch.cuda.CUDAGraph()
+            st = torch.cuda.Stream()
+            st.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(st):
+                with torch.cuda.graph(gr, stream=st):
+                    for _ in range(20):
+                        f()
+            torch.cuda.current_stream().wait_stream(st)
+            out[f"c1_adam_W4_N2^20_{name}_{an}_graph_us"] = timeit(gr.replay, 10) * 1e3 / 20
     ctx.close()
 
 
