@@ -490,16 +490,25 @@ def run_coconet(args):
         except Exception:
             pass
     shard = N / W
-    # per-rank HBM bytes: W=1 two-pass LAMB = 38 B/elem; W>1 the
-    # shard's 38 B minus its g read / p write (served by the peers' HBM) plus this
-    # rank's whole g read by its owners (2N) and whole p written by them (4N)
-    hbm_bytes = 38.0 * shard if W == 1 else 32.0 * shard + 6.0 * N
+    # per-rank HBM bytes: W=1 the ONCHIP schedule (AUTO) moves
+    # 30 B/elem (pass 1: g 2 + m, v, p 12 read, m', v' 8 written; pass 2: p 4 +
+    # 4) plus 8 B for every element whose u did not fit on chip (its pass 2
+    # re-reads m', v'); the two-pass TMA schedule 38 B/elem. W>1 (TMA): the
+    # shard's 38 B minus its g read / p write (served by the peers' HBM) plus
+    # this rank's whole g read by its owners (2N) and whole p written by them (4N)
+    spilled = tl.onchip_spilled() if W == 1 else -1
+    sched_name = "ONCHIP" if spilled >= 0 else "TMA"
+    if W == 1:
+        hbm_bytes = 30.0 * shard + 8.0 * spilled if spilled >= 0 else 38.0 * shard
+    else:
+        hbm_bytes = 32.0 * shard + 6.0 * N
     nvl_bytes = (W - 1) / W * N * (2 + 4)
     if W == 1:
         achieved = hbm_bytes / (ms * 1e-3) / 1e9
         roof = {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                 "frac": achieved / hbm_peak, "peak_kind": peak_kind,
-                "algorithmic_bytes_per_launch": hbm_bytes,
+                "algorithmic_bytes_per_launch": hbm_bytes, "schedule": sched_name,
+                "spilled_elems": spilled if spilled >= 0 else None,
                 "compulsory_bytes_per_launch": 26.0 * N,
                 "compulsory_frac": 26.0 * N / (ms * 1e-3) / 1e9 / hbm_peak}
     else:

@@ -157,6 +157,10 @@ int coconet_tlist_chunk(coconet_tlist_t tl, int r, int64_t* lo, int64_t* hi);
  * (or -count if cap is too small). */
 int64_t coconet_tlist_segments(coconet_tlist_t tl, int r, int64_t* tensor, int64_t* toff,
                                int64_t* len, int64_t* sidx, int64_t cap);
+/* ONCHIP-LAMB plan of the last ONCHIP launch on this list: elements whose u
+ * did not fit on chip (their pass 2 re-reads m', v'), or -1 if none was built.
+ * Pass-level bytes at fp16 g: 30 per element + 8 per spilled element. */
+int64_t coconet_tlist_onchip_spilled(coconet_tlist_t tl);
 /* Shard index of flat position `pos` inside its owner's shard storage. */
 int64_t coconet_tlist_shard_index(coconet_tlist_t tl, int64_t pos);
 /* STREAMED-LAMB work list of rank r for a pass-1 -> pass-2 lag of `lag`
@@ -231,10 +235,15 @@ enum coconet_lamb_sched {
   COCONET_LAMB_STREAMED = 2,
   COCONET_LAMB_TMA = 3, /* GRID's two passes fed by TMA bulk copies into a shared-memory ring
                           (norms summed in a different fixed order) */
-  COCONET_LAMB_WINDOWED = 4 /* group size 1: the TMA ring over windows of consecutive tensors
+  COCONET_LAMB_WINDOWED = 4, /* group size 1: the TMA ring over windows of consecutive tensors
                                (lag_elems = window size), pass 2 of a window one window after
                                its pass 1 so its m, v, p re-reads hit L2; per-window arrival
                                counters instead of grid-wide syncs. m, v bit-identical to TMA */
+  COCONET_LAMB_ONCHIP = 5 /* group size 1: pass 1 keeps u = m'/(sqrt(v')+eps) + wd*p on chip
+                             (TMEM + shared memory of one CTA per SM) for windows of whole
+                             tensors, so pass 2 reads only p (30 B/element at fp16 g against
+                             38); items beyond a CTA's on-chip capacity take TMA's pass 2.
+                             m, v bit-identical to TMA */
 };
 
 int coconet_fused_rs_lamb_ag(coconet_ctx_t ctx, coconet_tlist_t tl, const void* const* g,

@@ -16,7 +16,7 @@ F32, F16, BF16 = 0, 1, 2
 SUM, MAX, MIN = 0, 1, 2
 MATH_EXACT, MATH_FAST = 0, 1
 ALGO_AUTO, ALGO_TWO_SHOT, ALGO_ONE_SHOT = 0, 1, 2
-LAMB_AUTO, LAMB_GRID, LAMB_STREAMED, LAMB_TMA, LAMB_WINDOWED = 0, 1, 2, 3, 4
+LAMB_AUTO, LAMB_GRID, LAMB_STREAMED, LAMB_TMA, LAMB_WINDOWED, LAMB_ONCHIP = 0, 1, 2, 3, 4, 5
 MODE_VIRTUAL, MODE_DISTRIBUTED = 0, 1
 MAX_RANKS = 8
 
@@ -98,6 +98,7 @@ _SIGNATURES = {
     "coconet_tlist_shard_index": (_I64, [_P, _I64]),
     "coconet_tlist_segments": (_I64, [_P, _I, _PI64, _PI64, _PI64, _PI64, _I64]),
     "coconet_tlist_stream_items": (_I64, [_P, _I64, _I, _PI64, _PI64, _PI64, _PI64, _I64]),
+    "coconet_tlist_onchip_spilled": (_I64, [_P]),
     "coconet_fused_rs_adam_ag": (_I, [_P, _P, _PP, _I, _PP, _P, _P, C.POINTER(AdamParams), _P]),
     "coconet_send": (_I, [_P, _I, _I, _P, _P, _I, _I64, _P]),
     "coconet_convert": (_I, [_P, _P, _I, _P, _I, _I64, _P]),

@@ -78,6 +78,10 @@ class TensorList:
         check(0 if got >= 0 else 3)
         return np.stack([np.frombuffer(b, dtype=np.int64)[:got] for b in bufs], axis=1)
 
+    def onchip_spilled(self) -> int:
+        """Elements the last ONCHIP-LAMB launch could not hold on chip (-1: no plan)."""
+        return int(self.lib.coconet_tlist_onchip_spilled(self.handle))
+
     def state_index_map(self, r: int):
         """(tensor, element, state index) arrays of every element rank r owns."""
         segs = self.segments(r)

@@ -1370,6 +1370,499 @@ __global__ void __launch_bounds__((NW + 1) * 32, 2) lamb_win_kernel(OptArgs a, L
   edge_barrier(rs, 1);
 }
 
+// ---- LAMB, ONCHIP schedule (group size 1). TMA/GRID pay 38 B/element at
+// fp16 g because pass 2 re-reads m', v' and p from HBM to recompute u. Here
+// pass 1 keeps u ON CHIP: every CTA (one per SM) holds the u of its chunk
+// items of the current window in TMEM (tcgen05.st/ld, 32 chunks of 16
+// columns) and in shared-memory slots next to the TMA ring, so pass 2 of a
+// held item reads p only: 30 B/element (g 2 + m, v, p 12 read, m, v 8
+// written; p 4 read and 4 written). The plan (tlist_onchip_plan) cuts the
+// tensor-ordered chunk items into windows of whole tensors small enough that
+// CTA c (items i == c mod G) holds all of its share; a tensor too large for
+// one window spills its items beyond `hold` per CTA, which take TMA's pass 2
+// (m', v', p re-read).
+// Per CTA the order is P1(0), then for each window k: the first `head` items
+// of P1(k+1), then P2(k) and the rest of P1(k+1) alternating, so the wait for
+// window k's norms is covered by pass-1 work and the ring always mixes heavy
+// (22 B) and light (8 B) items. Held items take ring slots in order
+// (live <= hold + head = cap). Norms: each CTA sums its items of a tensor
+// (thread partials, then the 8 warps in fixed order) into part[t][cta]; a
+// window's pass 1 is complete when its arrival counter reaches the grid size
+// (cumulative over calls: no reset kernel), after which every CTA reduces the
+// partials of the window's tensors in CTA order (deterministic) into a
+// shared-memory ratio table. m', v' are TMA's bit for bit; u is the same
+// lamb_u of the same fp32 m', v', p; only the norm summation order differs.
+struct LambOC {
+  const OcItem* items;
+  const int64_t* wi;     // [K+1]
+  const int* tfirst;     // [K+1]
+  const int64_t* titem;  // [n_tensors+1]
+  double2* part;         // [n_tensors][G]
+  uint32_t* cnt;         // [K] pass-1 arrivals per window, [K] CTAs out; zero between launches
+  int K;
+  int hold, cap, head, tslots;
+  int slot_off;  // byte offset of the shared-memory u slots from the ring base
+  int nosync;    // profiling only (COCONET_LAMB_OC_NOSYNC=1): skip the window waits, results invalid
+};
+
+__device__ __forceinline__ int64_t oc_first(int64_t b, int c, int G) {
+  int64_t r = (int64_t(c) - b) % G;
+  if (r < 0) r += G;
+  return b + r;
+}
+__device__ __forceinline__ int oc_count(int64_t b, int64_t e, int c, int G) {
+  const int64_t f = oc_first(b, c, G);
+  return f < e ? int((e - 1 - f) / G + 1) : 0;
+}
+
+// The per-window item order shared by the producer and the consumers:
+// head P1 items, then P2 and P1 alternating. next() = 0 done, 1 P1 (j), 2 P2 (j).
+struct OcSeq {
+  int n1, n2, h, j1, j2;
+  bool p2_turn;
+  __device__ __forceinline__ void start(int n2_, int n1_, int head) {
+    n1 = n1_;
+    n2 = n2_;
+    h = min(head, n1);
+    j1 = j2 = 0;
+    p2_turn = true;
+  }
+  __device__ __forceinline__ int next(int& j) {
+    if (j1 < h) {
+      j = j1++;
+      return 1;
+    }
+    if (j2 >= n2 && j1 >= n1) return 0;
+    if (j2 < n2 && (p2_turn || j1 >= n1)) {
+      j = j2++;
+      p2_turn = false;
+      return 2;
+    }
+    j = j1++;
+    p2_turn = true;
+    return 1;
+  }
+};
+
+// 32 items of one stream (P1 or P2) of this CTA, loaded by the producer warp
+// at once (lane l: item first + l*G) and handed out with shuffles.
+struct OcBatch {
+  int64_t toff, sidx, qa, aoff, boff;
+  int len, tensor;
+  __device__ __forceinline__ void load(const OptArgs& a, const OcItem* items, int64_t first, int G, int cnt,
+                                       int lane) {
+    if (lane < cnt) {
+      const OcItem it = items[first + int64_t(lane) * G];
+      toff = it.toff;
+      sidx = it.sidx;
+      qa = it.qa;
+      len = it.len;
+      tensor = it.tensor;
+      aoff = a.offs[tensor];
+      boff = a.offs[a.n_tensors + tensor];
+    } else {
+      toff = sidx = qa = aoff = boff = 0;
+      len = tensor = 0;
+    }
+  }
+};
+
+struct OcDesc {
+  int64_t toff, sidx, qa, aoff, boff;
+  int len, tensor;
+};
+
+// What the consumers need of an item, resolved by the producer: 48 bytes
+// (three 16-byte shared loads).
+struct OcStage {
+  float* mp;    // m' of the chunk's first element (v' at mp + v_minus_m)
+  float* pp;    // p of the chunk's first element
+  int nq;       // quads in the chunk
+  int off0;     // element offset of the chunk's first quad from the segment start (>= -3)
+  int len;      // segment length
+  int tensor;
+  int goff;     // byte offset of the chunk's g inside the stage
+  int pad_;
+};
+__device__ __forceinline__ OcDesc oc_get(const OcBatch& b, int j) {
+  const unsigned f = 0xffffffffu;
+  return OcDesc{__shfl_sync(f, b.toff, j), __shfl_sync(f, b.sidx, j), __shfl_sync(f, b.qa, j),
+                __shfl_sync(f, b.aoff, j), __shfl_sync(f, b.boff, j), __shfl_sync(f, b.len, j),
+                __shfl_sync(f, b.tensor, j)};
+}
+
+template <int N>
+__device__ __forceinline__ void tm_st(uint32_t taddr, const float* u) {
+  if constexpr (N == 8) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr),
+                 "r"(__float_as_uint(u[0])), "r"(__float_as_uint(u[1])), "r"(__float_as_uint(u[2])),
+                 "r"(__float_as_uint(u[3])), "r"(__float_as_uint(u[4])), "r"(__float_as_uint(u[5])),
+                 "r"(__float_as_uint(u[6])), "r"(__float_as_uint(u[7]))
+                 : "memory");
+  } else {
+    static_assert(N == 4, "x4 or x8");
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1,%2,%3,%4};" ::"r"(taddr),
+                 "r"(__float_as_uint(u[0])), "r"(__float_as_uint(u[1])), "r"(__float_as_uint(u[2])),
+                 "r"(__float_as_uint(u[3]))
+                 : "memory");
+  }
+}
+template <int N>
+__device__ __forceinline__ void tm_ld(uint32_t taddr, float* u) {
+  uint32_t r[8];
+  if constexpr (N == 8) {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+                 : "r"(taddr)
+                 : "memory");
+  } else {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+                 : "r"(taddr)
+                 : "memory");
+  }
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < N; ++i) u[i] = __uint_as_float(r[i]);
+}
+
+constexpr int kOcTmemCols = 512;
+
+// mbarrier wait for the consumers of the ONCHIP ring: the watchdog clock is
+// read once per 64 polls (try_wait already suspends in hardware).
+__device__ __forceinline__ void mbar_wait_lazy(uint64_t* bar, uint32_t parity) {
+  if (mbar_try(bar, parity)) return;
+  const unsigned long long t0 = globaltimer();
+  for (int i = 1;; ++i) {
+    if (mbar_try(bar, parity)) return;
+    if ((i & 63) == 0 && globaltimer() - t0 > 10000000000ull) __trap();
+  }
+}
+
+template <typename G, int NW, int QPT>
+__global__ void __launch_bounds__((NW + 1) * 32, 1) lamb_onchip_kernel(OptArgs a, LambK k, TmaArgs ta, LambOC oc) {
+  using ST = TmaStage<G, NW, QPT>;
+  constexpr int kChunkQ = ST::CHUNK_Q;
+  constexpr int kFpt = QPT * 4;               // u floats per consumer thread per chunk
+  constexpr int kSlotCols = kFpt * (NW / 4);  // TMEM columns of one chunk slot (128 lanes)
+  static_assert(NW % 4 == 0 && (kFpt == 4 || kFpt == 8), "TMEM slot layout");
+  constexpr int kMaxStages = 8;
+  extern __shared__ __align__(128) uint8_t smem_raw[];
+  __shared__ char* s_base[kMaxRanks];
+  __shared__ float s_red[2][NW][2];
+  __shared__ __align__(16) OcStage s_desc[kMaxStages];
+  __shared__ float s_ratio[kOcMaxTensors];
+  __shared__ uint32_t s_tmem;
+  __shared__ __align__(8) uint64_t s_p1done[2];  // window parity: one phase per two windows
+  const RankSet& rs = a.rs;
+  if (threadIdx.x < kMaxRanks) s_base[threadIdx.x] = threadIdx.x < rs.world ? rs.base[threadIdx.x] : nullptr;
+  const int S = ta.stages;
+  uint8_t* stage0 = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
+  uint64_t* full = reinterpret_cast<uint64_t*>(stage0 + size_t(S) * ST::BYTES);
+  uint64_t* empty = full + S;
+  uint8_t* slots = stage0 + oc.slot_off;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < S; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], NW);
+    }
+    mbar_init(&s_p1done[0], NW);
+    mbar_init(&s_p1done[1], NW);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&s_tmem)),
+                 "r"(kOcTmemCols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  const int me = rs.rank();
+  edge_barrier(rs, 0);  // publishes the barrier inits and the TMEM address (group size 1: no peer)
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = s_tmem;
+  float* m = reinterpret_cast<float*>(s_base[me] + a.m_off);
+  float* v = reinterpret_cast<float*>(s_base[me] + a.v_off);
+  const int64_t v_minus_m = (a.v_off - a.m_off) / 4;
+  char* pme = s_base[me];
+  const int NG = int(gridDim.x), cta = int(blockIdx.x);
+  const int K = oc.K;
+  uint32_t st = 0, ph = 0;
+  if (warp == NW) {
+    // ---------------- producer
+    OcBatch b1, b2;
+    for (int kk = -1; kk < K; ++kk) {
+      const int64_t w2b = kk >= 0 ? oc.wi[kk] : 0, w2e = kk >= 0 ? oc.wi[kk + 1] : 0;
+      const int64_t w1b = kk + 1 < K ? oc.wi[kk + 1] : 0, w1e = kk + 1 < K ? oc.wi[kk + 2] : 0;
+      const int n2 = kk >= 0 ? oc_count(w2b, w2e, cta, NG) : 0;
+      const int n1 = kk + 1 < K ? oc_count(w1b, w1e, cta, NG) : 0;
+      const int64_t f2 = oc_first(w2b, cta, NG), f1 = oc_first(w1b, cta, NG);
+      OcSeq seq;
+      seq.start(n2, n1, oc.head);
+      bool spill_ok = false;
+      int j, kind;
+      while ((kind = seq.next(j)) != 0) {
+        const bool p1 = kind == 1;
+        if ((j & 31) == 0) {
+          if (p1) b1.load(a, oc.items, f1 + int64_t(j) * NG, NG, min(32, n1 - j), lane);
+          else b2.load(a, oc.items, f2 + int64_t(j) * NG, NG, min(32, n2 - j), lane);
+        }
+        const OcDesc d = oc_get(p1 ? b1 : b2, j & 31);
+        if (lane == 0) {
+          const bool held = j < oc.hold;
+          if (!p1 && !held && !spill_ok) {  // m', v' of this window stored (generic proxy) by our consumers
+            // window kk+2 is not issued yet, so its barrier is at most one phase ahead
+            mbar_wait(&s_p1done[kk & 1], uint32_t(kk >> 1) & 1u);
+            asm volatile("fence.proxy.async.global;" ::: "memory");
+            spill_ok = true;
+          }
+          const int64_t qa = d.qa;
+          const int64_t qb = min(qa + int64_t(kChunkQ), (d.toff + d.len + 3) >> 2);
+          mbar_wait(&empty[st], ph ^ 1u);
+          uint8_t* dst = stage0 + size_t(st) * ST::BYTES;
+          const uint32_t abytes = uint32_t(qb - qa) * 16u;
+          const int64_t si = d.sidx + (qa * 4 - d.toff);
+          const uintptr_t ga = reinterpret_cast<uintptr_t>(pme + d.aoff + qa * 4 * int64_t(sizeof(G)));
+          OcStage sd;
+          sd.mp = m + si;
+          sd.pp = reinterpret_cast<float*>(pme + d.boff) + qa * 4;
+          sd.nq = int(qb - qa);
+          sd.off0 = int(qa * 4 - d.toff);
+          sd.len = d.len;
+          sd.tensor = d.tensor;
+          sd.goff = int(ga & 15u);
+          sd.pad_ = 0;
+          s_desc[st] = sd;
+          if (p1) {
+            const char* g0 = reinterpret_cast<const char*>(ga & ~uintptr_t(15));
+            const char* g1 = reinterpret_cast<const char*>(
+                (reinterpret_cast<uintptr_t>(pme + d.aoff + qb * 4 * int64_t(sizeof(G))) + 15) & ~uintptr_t(15));
+            const uint32_t gbytes = uint32_t(g1 - g0);
+            mbar_expect_tx(&full[st], gbytes + 3u * abytes);
+            bulk_load(dst, g0, gbytes, &full[st]);
+            bulk_load(dst + ST::G_BYTES, m + si, abytes, &full[st]);
+            bulk_load(dst + ST::G_BYTES + ST::A_BYTES, v + si, abytes, &full[st]);
+          } else if (!held) {
+            mbar_expect_tx(&full[st], 3u * abytes);
+            bulk_load(dst + ST::G_BYTES, m + si, abytes, &full[st]);
+            bulk_load(dst + ST::G_BYTES + ST::A_BYTES, v + si, abytes, &full[st]);
+          } else {
+            mbar_expect_tx(&full[st], abytes);
+          }
+          bulk_load(dst + ST::G_BYTES + 2 * ST::A_BYTES, sd.pp, abytes, &full[st]);
+        }
+        if (++st == uint32_t(S)) {
+          st = 0;
+          ph ^= 1u;
+        }
+      }
+    }
+  } else {
+    // ---------------- consumers
+    const int ctid = threadIdx.x;
+    // TMEM: warp w owns lanes 32*(w%4).. and columns (w/4)*kFpt.. of every kSlotCols-column chunk slot
+    const uint32_t tbase = tmem + (uint32_t(32 * (warp & 3)) << 16) + uint32_t((warp >> 2) * kFpt);
+    int base2 = 0;  // ring slot of window kk's first held item
+    int red = 0;
+    for (int kk = -1; kk < K; ++kk) {
+      const int64_t w2b = kk >= 0 ? oc.wi[kk] : 0, w2e = kk >= 0 ? oc.wi[kk + 1] : 0;
+      const int64_t w1b = kk + 1 < K ? oc.wi[kk + 1] : 0, w1e = kk + 1 < K ? oc.wi[kk + 2] : 0;
+      const int n2 = kk >= 0 ? oc_count(w2b, w2e, cta, NG) : 0;
+      const int n1 = kk + 1 < K ? oc_count(w1b, w1e, cta, NG) : 0;
+      int base1 = base2 + min(n2, oc.hold);
+      if (base1 >= oc.cap) base1 -= oc.cap;
+      const int t2 = kk >= 0 ? oc.tfirst[kk] : 0;
+      OcSeq seq;
+      seq.start(n2, n1, oc.head);
+      int cur_t = -1;  // P1 tensor whose thread partials are open
+      float sp = 0.f, su = 0.f;
+      // flush the open tensor's CTA partial: fixed-order sum of the NW warps
+      auto flush = [&]() {
+        const float wp = warp_sumf(sp), wu = warp_sumf(su);
+        if (lane == 0) {
+          s_red[red][warp][0] = wp;
+          s_red[red][warp][1] = wu;
+        }
+        asm volatile("bar.sync 1, %0;" ::"n"(NW * 32) : "memory");
+        if (ctid == 0) {
+          float tp = 0.f, tu = 0.f;
+#pragma unroll
+          for (int w = 0; w < NW; ++w) {
+            tp += s_red[red][w][0];
+            tu += s_red[red][w][1];
+          }
+          oc.part[int64_t(cur_t) * NG + cta] = make_double2(double(tp), double(tu));
+        }
+        red ^= 1;
+        sp = su = 0.f;
+      };
+      // this CTA's pass 1 of window kk+1 is complete: partials out, m', v'
+      // ordered before the spilled bulk re-reads, arrival counted
+      auto finish_p1 = [&]() {
+        if (cur_t >= 0) flush();
+        cur_t = -1;
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+        asm volatile("fence.proxy.async.global;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&s_p1done[(kk + 1) & 1]);
+        asm volatile("bar.sync 1, %0;" ::"n"(NW * 32) : "memory");
+        if (ctid == 0) {
+          __threadfence();
+          atomicAdd(&oc.cnt[kk + 1], 1u);
+        }
+      };
+      if (kk + 1 < K && n1 == 0) finish_p1();
+      int j, kind;
+      while ((kind = seq.next(j)) != 0) {
+        const bool p1 = kind == 1;
+        if (!p1 && j == 0) {
+          // window kk's norms: every CTA's pass 1 is in, reduce in CTA order
+          if (ctid == 0 && !oc.nosync) wait_equal(&oc.cnt[kk], uint32_t(NG), rs);
+          asm volatile("bar.sync 1, %0;" ::"n"(NW * 32) : "memory");
+          const int t2e = oc.tfirst[kk + 1];
+          for (int t = t2 + warp; t < t2e; t += NW) {
+            const int64_t i0 = oc.titem[t];
+            const int n = int(min(oc.titem[t + 1] - i0, int64_t(NG)));
+            const int c0 = int(i0 % NG);
+            double P = 0.0, U = 0.0;
+            for (int r = lane; r < n; r += 32) {
+              const int c = c0 + r >= NG ? c0 + r - NG : c0 + r;
+              const double2 pu = __ldcg(&oc.part[int64_t(t) * NG + c]);
+              P += pu.x;
+              U += pu.y;
+            }
+            P = warp_sum(P);
+            U = warp_sum(U);
+            if (lane == 0) s_ratio[t - t2] = float(trust_ratio(P, U, k));
+          }
+          asm volatile("bar.sync 1, %0;" ::"n"(NW * 32) : "memory");
+        }
+        mbar_wait_lazy(&full[st], ph);
+        const OcStage d = s_desc[st];
+        if (p1 && d.tensor != cur_t) {
+          if (cur_t >= 0) flush();
+          cur_t = d.tensor;
+        }
+        const bool held = j < oc.hold;
+        int slot = (p1 ? base1 : base2) + j;
+        if (slot >= oc.cap) slot -= oc.cap;
+        const uint8_t* src = stage0 + size_t(st) * ST::BYTES;
+        float u[kFpt];
+        if (!p1 && held) {
+          if (slot < oc.tslots) {
+            tm_ld<kFpt>(tbase + uint32_t(slot * kSlotCols), u);
+          } else {
+            const uint8_t* sl = slots + size_t(slot - oc.tslots) * (kChunkQ * 16);
+#pragma unroll
+            for (int qq = 0; qq < QPT; ++qq) {
+              const float4 x = *reinterpret_cast<const float4*>(sl + qq * (NW * 32 * 16) + ctid * 16);
+              u[qq * 4 + 0] = x.x; u[qq * 4 + 1] = x.y; u[qq * 4 + 2] = x.z; u[qq * 4 + 3] = x.w;
+            }
+          }
+        }
+        const float ratio = p1 ? 0.f : s_ratio[d.tensor - t2];
+        float fp = 0.f, fu = 0.f;
+#pragma unroll
+        for (int qq = 0; qq < QPT; ++qq) {
+          const int qi = ctid + qq * (NW * 32);  // quad inside the chunk
+          const bool in = qi < d.nq;
+          const int er = 4 * qi + d.off0;  // its first element's offset in the segment
+          const int lo = in ? max(0, -er) : 4, hi = min(4, d.len - er);
+          const bool whole = lo == 0 && hi == 4;
+          const float4 pq = *reinterpret_cast<const float4*>(src + ST::G_BYTES + 2 * ST::A_BYTES + qi * 16);
+          const float pp[4] = {pq.x, pq.y, pq.z, pq.w};
+          if (p1) {
+            const float4 mq = *reinterpret_cast<const float4*>(src + ST::G_BYTES + qi * 16);
+            const float4 vq = *reinterpret_cast<const float4*>(src + ST::G_BYTES + ST::A_BYTES + qi * 16);
+            float mm[4] = {mq.x, mq.y, mq.z, mq.w}, vv[4] = {vq.x, vq.y, vq.z, vq.w};
+            float gs[4];
+            if constexpr (sizeof(G) == 4) {
+              const float4 gq = *reinterpret_cast<const float4*>(src + d.goff + qi * 16);
+              gs[0] = gq.x; gs[1] = gq.y; gs[2] = gq.z; gs[3] = gq.w;
+            } else {
+              const uint2 gq = *reinterpret_cast<const uint2*>(src + d.goff + qi * 8);
+              const G* h = reinterpret_cast<const G*>(&gq);
+#pragma unroll
+              for (int i = 0; i < 4; ++i) gs[i] = to_f32(h[i]);
+            }
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              const float mn = fmaf(k.fcm, gs[i], mm[i] * k.fb1);
+              const float vn = fmaf(k.fcv * gs[i], gs[i], vv[i] * k.fb2);
+              mm[i] = mn;
+              vv[i] = vn;
+              const float uu = lamb_u(mn, vn, pp[i], k);
+              u[qq * 4 + i] = uu;
+              const bool ok = whole || (i >= lo && i < hi);  // (stage bytes past the chunk are garbage)
+              fp = ok ? fmaf(pp[i], pp[i], fp) : fp;
+              fu = ok ? fmaf(uu, uu, fu) : fu;
+            }
+            if (whole) {
+              store4(d.mp + 4 * qi, mm);
+              store4(d.mp + v_minus_m + 4 * qi, vv);
+            } else if (in) {
+              st4m(d.mp + 4 * qi, mm, lo, hi);
+              st4m(d.mp + v_minus_m + 4 * qi, vv, lo, hi);
+            }
+          } else {
+            if (!held) {
+              const float4 mq = *reinterpret_cast<const float4*>(src + ST::G_BYTES + qi * 16);
+              const float4 vq = *reinterpret_cast<const float4*>(src + ST::G_BYTES + ST::A_BYTES + qi * 16);
+              const float mm[4] = {mq.x, mq.y, mq.z, mq.w}, vv[4] = {vq.x, vq.y, vq.z, vq.w};
+#pragma unroll
+              for (int i = 0; i < 4; ++i) u[qq * 4 + i] = lamb_u(mm[i], vv[i], pp[i], k);
+            }
+            float pn[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) pn[i] = pp[i] - ratio * u[qq * 4 + i];
+            if (whole) store4(d.pp + 4 * qi, pn);
+            else if (in) st4m(d.pp + 4 * qi, pn, lo, hi);
+          }
+        }
+        if (p1 && held) {
+          if (slot < oc.tslots) {
+            tm_st<kFpt>(tbase + uint32_t(slot * kSlotCols), u);
+          } else {
+            uint8_t* sl = slots + size_t(slot - oc.tslots) * (kChunkQ * 16);
+#pragma unroll
+            for (int qq = 0; qq < QPT; ++qq)
+              *reinterpret_cast<float4*>(sl + qq * (NW * 32 * 16) + ctid * 16) =
+                  make_float4(u[qq * 4 + 0], u[qq * 4 + 1], u[qq * 4 + 2], u[qq * 4 + 3]);
+          }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[st]);
+        if (++st == uint32_t(S)) {
+          st = 0;
+          ph ^= 1u;
+        }
+        if (p1) {
+          sp += fp;
+          su += fu;
+          if (j == n1 - 1) finish_p1();
+        }
+      }
+      base2 = base1;
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  edge_barrier(rs, 1);
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  if (warp == 0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kOcTmemCols) : "memory");
+  // every CTA has passed all of its window waits: the last one out zeroes the
+  // counters for the next launch (so a captured graph replays correctly)
+  if (threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(&oc.cnt[K], 1u) == uint32_t(NG) - 1u) {
+      for (int i = 0; i <= K; ++i) oc.cnt[i] = 0u;
+      __threadfence();
+    }
+  }
+}
+
 // ---- Adam, TMA schedule (W = 1): one pass, the producer of lamb_tma_kernel
 // streaming g, m, v, p into the shared-memory ring and NW consumer warps
 // applying adam_elem (EXACT or FAST) and writing m, v, p.
@@ -1908,6 +2401,8 @@ constexpr int64_t kTmaMinBucket = 4096;
 // WINDOWED LAMB: elements per window (COCONET_LAMB_WIN_ELEMS or
 // coconet_lamb_params.lag_elems override it)
 constexpr int64_t kDefaultWindow = int64_t(2) << 20;
+// ONCHIP LAMB in AUTO from this many elements per shard (group size 1)
+constexpr int64_t kOnchipMinElems = int64_t(1) << 20;
 
 int check_state(coconet_ctx* c, const void* ptr, int64_t* off) {
   int rc = heap_offset(c, ptr, off);
@@ -2021,7 +2516,7 @@ int coconet_fused_rs_lamb_ag(coconet_ctx_t c, coconet_tlist_t tl, const void* co
   if (tl->ctx != c) return set_error(COCONET_ERR_INVALID_INPUT, "tensor list belongs to another context");
   if (hp->math != COCONET_MATH_FAST && hp->math != COCONET_MATH_EXACT)
     return set_error(COCONET_ERR_INVALID_INPUT, "bad math");
-  if (hp->sched < COCONET_LAMB_AUTO || hp->sched > COCONET_LAMB_WINDOWED)
+  if (hp->sched < COCONET_LAMB_AUTO || hp->sched > COCONET_LAMB_ONCHIP)
     return set_error(COCONET_ERR_INVALID_INPUT, "bad LAMB schedule");
   // exchange [rank][tensor] (P, U) doubles + ready flags [rank][tensor]
   if (size_t(kMaxRanks) * tl->n_tensors * (2 * sizeof(double) + sizeof(uint32_t)) > kTileFlagsOff)
@@ -2072,7 +2567,86 @@ int coconet_fused_rs_lamb_ag(coconet_ctx_t c, coconet_tlist_t tl, const void* co
     return launch_opt(c, tl, fn, args, false, stream);
   }
   const bool tma_auto = tl->bucket_cap >= (W == 1 ? kTmaMinBucket : 4 * kTmaMinBucket);
-  const int sched = hp->sched == COCONET_LAMB_AUTO ? (tma_auto ? COCONET_LAMB_TMA : COCONET_LAMB_GRID) : hp->sched;
+  // AUTO at group size 1 with large buckets and a large shard: ONCHIP
+  // (BERT-336M: 1.76 ms against TMA's 1.96, profiles/r02_lamb_onchip_probe.json)
+  const bool onchip_auto = W == 1 && tma_auto && tl->shard_elems >= kOnchipMinElems;
+  const int sched = hp->sched != COCONET_LAMB_AUTO ? hp->sched
+                    : onchip_auto                 ? COCONET_LAMB_ONCHIP
+                    : tma_auto                    ? COCONET_LAMB_TMA
+                                                  : COCONET_LAMB_GRID;
+  if (sched == COCONET_LAMB_ONCHIP) {
+    if (W != 1) return set_error(COCONET_ERR_UNSUPPORTED, "the ONCHIP LAMB schedule runs at group size 1");
+    // consumer warps x quads per thread per chunk item: 16 x 2 (4096-element
+    // items, the default), 16 x 1 or 8 x 2 (2048); one CTA per SM
+    const char* ne = getenv("COCONET_LAMB_OC_SHAPE");
+    const int shape = ne ? atoi(ne) : 162;
+    const void* fn = nullptr;
+    int sbytes = 0, threads = 0, chunk_q = 0;
+    auto pick = [&](auto tag_g) {
+      using Gt = decltype(tag_g);
+      auto use = [&](auto kern, auto st_tag) {
+        using STt = decltype(st_tag);
+        fn = reinterpret_cast<const void*>(kern);
+        sbytes = STt::BYTES;
+        threads = STt::THREADS;
+        chunk_q = STt::CHUNK_Q;
+      };
+      if (shape == 161) use(&lamb_onchip_kernel<Gt, 16, 1>, TmaStage<Gt, 16, 1>{});
+      else if (shape == 82) use(&lamb_onchip_kernel<Gt, 8, 2>, TmaStage<Gt, 8, 2>{});
+      else use(&lamb_onchip_kernel<Gt, 16, 2>, TmaStage<Gt, 16, 2>{});
+    };
+    if (g_elem == COCONET_F32) pick(float{});
+    else if (g_elem == COCONET_F16) pick(__half{});
+    else pick(__nv_bfloat16{});
+    // one CTA per SM: a ring of S stages, then as many 8 KB u slots as the
+    // opt-in shared memory leaves, on top of the 32 TMEM slots
+    const char* se = getenv("COCONET_LAMB_OC_STAGES");
+    TmaArgs ta;
+    int optin = 0, per_sm_smem = 0;
+    CN_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, c->device));
+    CN_CUDA(cudaDeviceGetAttribute(&per_sm_smem, cudaDevAttrMaxSharedMemoryPerMultiprocessor, c->device));
+    cudaFuncAttributes fa;
+    CN_CUDA(cudaFuncGetAttributes(&fa, fn));
+    // 1 KB per CTA is reserved by the system
+    const int budget = std::min(optin, per_sm_smem - 1024) - int(fa.sharedSizeBytes) - 128;
+    // the deepest ring that fits (4 stages of 4096-element items at fp16 g:
+    // bytes in flight beat shared-memory u slots, profiles/r02_lamb_onchip_probe.json)
+    const int fit = std::max(2, std::min(8, budget / (sbytes + 16)));
+    ta.stages = se ? std::max(2, std::min(fit, atoi(se))) : std::min(fit, chunk_q == 1024 ? 4 : 5);
+    const int slot_off = (ta.stages * sbytes + 16 * ta.stages + 127) / 128 * 128;
+    const int room = budget - slot_off;
+    const char* xe = getenv("COCONET_LAMB_OC_SMEM_SLOTS");
+    const int slot_bytes = chunk_q * 16;  // u of one chunk item
+    int smem_slots = std::max(0, room / slot_bytes);
+    if (xe) smem_slots = std::max(0, std::min(smem_slots, atoi(xe)));
+    LambOC oc;
+    oc.tslots = kOcTmemCols / (chunk_q / 32);  // chunk_q * 4 floats over 128 lanes
+    oc.cap = oc.tslots + smem_slots;
+    const char* he = getenv("COCONET_LAMB_OC_HEAD");
+    oc.head = std::max(1, std::min(oc.cap / 2, he ? atoi(he) : 1));
+    oc.hold = oc.cap - oc.head;
+    if (const char* ke = getenv("COCONET_LAMB_OC_HOLD")) oc.hold = std::max(1, std::min(oc.hold, atoi(ke)));
+    oc.slot_off = slot_off;
+    const char* ns = getenv("COCONET_LAMB_OC_NOSYNC");
+    oc.nosync = ns && ns[0] == '1';
+    const size_t smem = 128 + size_t(slot_off) + size_t(smem_slots) * slot_bytes;
+    rc = ensure_smem(c, fn, smem);
+    if (rc) return rc;
+    int blocks = 0;
+    rc = coop_blocks(c, fn, threads, smem, tl->group, int64_t(c->sm_count), &blocks);
+    if (rc) return rc;
+    rc = tlist_onchip_plan(tl, blocks, oc.hold, chunk_q);
+    if (rc) return rc;
+    oc.items = tl->d_oc_items;
+    oc.wi = tl->d_oc_wi;
+    oc.tfirst = tl->d_oc_tfirst;
+    oc.titem = tl->d_oc_titem;
+    oc.part = tl->d_oc_part;
+    oc.cnt = tl->d_oc_cnt;
+    oc.K = tl->oc_K;
+    void* args[] = {&a, &k, &ta, &oc};
+    return coop_launch(c, fn, dim3(unsigned(blocks), 1u), dim3(unsigned(threads)), args, smem, stream);
+  }
   if (sched == COCONET_LAMB_WINDOWED) {
     if (W != 1) return set_error(COCONET_ERR_UNSUPPORTED, "the WINDOWED LAMB schedule runs at group size 1");
     const char* we = getenv("COCONET_LAMB_WIN_ELEMS");

@@ -21,6 +21,14 @@ struct Seg {
 using Item = Seg;
 constexpr int64_t kPass2Bit = 0x80;
 
+// One ONCHIP-LAMB chunk item: quads [qa, min(qa + chunk, end of segment)) of
+// the segment (toff, len, sidx) of `tensor`. 32 bytes, read by the producer.
+struct OcItem {
+  int64_t toff, sidx, qa;
+  int len, tensor;
+};
+constexpr int kOcMaxTensors = 256;  // tensors per ONCHIP window (shared-memory ratio table)
+
 __host__ __device__ __forceinline__ int64_t pack_meta(int tensor, int len, int owner) {
   return (int64_t(tensor) << 32) | (int64_t(len & 0xffffff) << 8) | int64_t(owner & 0xff);
 }
@@ -92,6 +100,20 @@ struct coconet_tlist {
   uint32_t* d_win_ready = nullptr; // [K] call number once a window's ratios are published
   uint32_t win_calls = 0;
   int win_blocks = 0;              // grid size the counters were advanced with
+  // ONCHIP LAMB schedule (group size 1): windows of whole tensors sized so that
+  // every CTA holds its share of a window's u on chip (TMEM + shared memory),
+  // built on first use for a grid size / hold depth (tlist_onchip_plan)
+  int oc_blocks = 0, oc_hold = 0, oc_chunk_q = 0, oc_K = 0;
+  int64_t oc_n_items = 0;
+  void* oc_mem = nullptr;
+  coconet::OcItem* d_oc_items = nullptr;  // [n_items] chunk items, tensor-major
+  int64_t* d_oc_wi = nullptr;             // [K+1] item range of each window
+  int* d_oc_tfirst = nullptr;             // [K+1] tensor range of each window
+  int64_t* d_oc_titem = nullptr;          // [n_tensors+1] first item of each tensor
+  double2* d_oc_part = nullptr;           // [n_tensors][blocks] per-CTA (sum p^2, sum u^2)
+  uint32_t* d_oc_cnt = nullptr;           // [K] pass-1 arrivals, [K] CTAs out (zeroed by the last CTA)
+  int oc_max_t = 0;                       // most tensors in one window
+  int64_t oc_spilled = 0;                 // elements of items beyond a CTA's hold (pass 2 re-reads m', v')
 };
 
 namespace coconet {
@@ -101,6 +123,10 @@ int tlist_stream_plan(coconet_tlist* tl, int64_t lag);
 // Builds (or keeps) the WINDOWED-LAMB windows for a target window size and
 // chunk items of chunk_q quads.
 int tlist_window_plan(coconet_tlist* tl, int64_t win_elems, int chunk_q);
+// Builds (or keeps) the ONCHIP-LAMB plan: chunk items of chunk_q quads in
+// tensor order, cut into windows of whole tensors of at most blocks * hold
+// items (a longer tensor is a window alone) and kOcMaxTensors tensors.
+int tlist_onchip_plan(coconet_tlist* tl, int blocks, int hold, int chunk_q);
 int tlist_bind(coconet_tlist* tl, const void* const* a, const void* const* b, int a_elem_bytes,
                int b_elem_bytes, cudaStream_t stream);
 }

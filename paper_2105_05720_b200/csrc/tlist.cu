@@ -212,15 +212,17 @@ int coconet_tlist_plan(int world, int n_tensors, const int64_t* counts, int64_t 
 
 int coconet_tlist_destroy(coconet_tlist_t tl) {
   if (!tl) return COCONET_OK;
-  if (tl->dev_mem || tl->stream_mem || tl->win_mem) cudaDeviceSynchronize();
+  if (tl->dev_mem || tl->stream_mem || tl->win_mem || tl->oc_mem) cudaDeviceSynchronize();
   if (tl->dev_mem) cudaFree(tl->dev_mem);
   if (tl->stream_mem) cudaFree(tl->stream_mem);
   if (tl->win_mem) cudaFree(tl->win_mem);
+  if (tl->oc_mem) cudaFree(tl->oc_mem);
   delete tl;
   return COCONET_OK;
 }
 
 int64_t coconet_tlist_shard_elems(coconet_tlist_t tl) { return tl ? tl->shard_elems : -1; }
+int64_t coconet_tlist_onchip_spilled(coconet_tlist_t tl) { return tl && tl->oc_mem ? tl->oc_spilled : -1; }
 int64_t coconet_tlist_total(coconet_tlist_t tl) { return tl ? tl->total : -1; }
 int64_t coconet_tlist_state_elems(coconet_tlist_t tl) { return tl ? tl->full_state_elems : -1; }
 int64_t coconet_tlist_buckets(coconet_tlist_t tl) { return tl ? tl->n_buckets : -1; }
@@ -449,6 +451,87 @@ int tlist_window_plan(coconet_tlist* tl, int64_t win_elems, int chunk_q) {
   tl->n_items = int64_t(items.size());
   tl->win_calls = 0;
   tl->win_blocks = 0;
+  return COCONET_OK;
+}
+
+// ONCHIP plan. Items are the segments of rank 0's CSR lists (tensor order)
+// cut into chunks of chunk_q quads; item i belongs to CTA i mod blocks, so a
+// window of at most blocks * hold items gives every CTA at most `hold` of
+// them to keep on chip. Windows hold whole tensors: a tensor of more items
+// is a window alone and its CTAs spill the items beyond `hold`.
+int tlist_onchip_plan(coconet_tlist* tl, int blocks, int hold, int chunk_q) {
+  if (tl->oc_mem && tl->oc_blocks == blocks && tl->oc_hold == hold && tl->oc_chunk_q == chunk_q) return COCONET_OK;
+  const int64_t* ptr = tl->csr_ptr.data() + tl->csr_begin[0];
+  std::vector<OcItem> items;
+  std::vector<int64_t> wi{0}, titem{0};
+  std::vector<int> tfirst{0};
+  const int64_t cap = int64_t(blocks) * hold;
+  int max_t = 0;
+  for (int t = 0; t < tl->n_tensors; ++t) {
+    const int64_t before = int64_t(items.size());
+    for (int64_t i = ptr[t]; i < ptr[t + 1]; ++i) {
+      const Seg& sg = tl->table[size_t(tl->csr_idx[size_t(i)])];
+      const int len = meta_len(sg.meta);
+      const int64_t q0 = sg.toff >> 2, q1 = (sg.toff + len + 3) >> 2;
+      for (int64_t qa = q0; qa < q1; qa += chunk_q) items.push_back(OcItem{sg.toff, sg.sidx, qa, len, t});
+    }
+    titem.push_back(int64_t(items.size()));
+    // close the open window before t when t does not fit in it
+    const int64_t wb = wi.back();
+    const int nt = t - tfirst.back();
+    if (nt > 0 && (int64_t(items.size()) - wb > cap || nt >= kOcMaxTensors)) {
+      wi.push_back(before);
+      tfirst.push_back(t);
+      max_t = std::max(max_t, nt);
+    }
+  }
+  if (tl->n_tensors > tfirst.back()) {
+    wi.push_back(int64_t(items.size()));
+    max_t = std::max(max_t, tl->n_tensors - tfirst.back());
+    tfirst.push_back(tl->n_tensors);
+  }
+  const int K = int(wi.size()) - 1;
+  // elements of the items a CTA cannot hold (its j-th item of a window, j >= hold)
+  int64_t spilled = 0;
+  for (int w = 0; w < K; ++w)
+    for (int64_t i = wi[size_t(w)]; i < wi[size_t(w) + 1]; ++i) {
+      const int64_t c = i % blocks;
+      int64_t f = wi[size_t(w)] + ((c - wi[size_t(w)]) % blocks + blocks) % blocks;
+      if ((i - f) / blocks < hold) continue;
+      const OcItem& it = items[size_t(i)];
+      const int64_t e0 = std::max(it.toff, it.qa * 4), e1 = std::min(it.toff + it.len, (it.qa + chunk_q) * 4);
+      spilled += e1 - e0;
+    }
+  if (tl->oc_mem) {
+    cudaDeviceSynchronize();
+    cudaFree(tl->oc_mem);
+    tl->oc_mem = nullptr;
+  }
+  auto al = [](size_t n) { return (std::max<size_t>(n, 1) + 255) / 256 * 256; };
+  const size_t b_items = al(items.size() * sizeof(OcItem)), b_wi = al(wi.size() * sizeof(int64_t));
+  const size_t b_tf = al(tfirst.size() * sizeof(int)), b_ti = al(titem.size() * sizeof(int64_t));
+  const size_t b_part = al(size_t(tl->n_tensors) * blocks * sizeof(double2)), b_cnt = al(size_t(K + 1) * sizeof(uint32_t));
+  CN_CUDA(cudaMalloc(&tl->oc_mem, b_items + b_wi + b_tf + b_ti + b_part + b_cnt));
+  char* p = static_cast<char*>(tl->oc_mem);
+  tl->d_oc_items = reinterpret_cast<OcItem*>(p);
+  tl->d_oc_wi = reinterpret_cast<int64_t*>(p += b_items);
+  tl->d_oc_tfirst = reinterpret_cast<int*>(p += b_wi);
+  tl->d_oc_titem = reinterpret_cast<int64_t*>(p += b_tf);
+  tl->d_oc_part = reinterpret_cast<double2*>(p += b_ti);
+  tl->d_oc_cnt = reinterpret_cast<uint32_t*>(p += b_part);
+  if (!items.empty())
+    CN_CUDA(cudaMemcpy(tl->d_oc_items, items.data(), items.size() * sizeof(OcItem), cudaMemcpyHostToDevice));
+  CN_CUDA(cudaMemcpy(tl->d_oc_wi, wi.data(), wi.size() * sizeof(int64_t), cudaMemcpyHostToDevice));
+  CN_CUDA(cudaMemcpy(tl->d_oc_tfirst, tfirst.data(), tfirst.size() * sizeof(int), cudaMemcpyHostToDevice));
+  CN_CUDA(cudaMemcpy(tl->d_oc_titem, titem.data(), titem.size() * sizeof(int64_t), cudaMemcpyHostToDevice));
+  CN_CUDA(cudaMemset(tl->d_oc_cnt, 0, b_cnt));
+  tl->oc_blocks = blocks;
+  tl->oc_hold = hold;
+  tl->oc_chunk_q = chunk_q;
+  tl->oc_K = K;
+  tl->oc_n_items = int64_t(items.size());
+  tl->oc_max_t = max_t;
+  tl->oc_spilled = spilled;
   return COCONET_OK;
 }
 

@@ -2,7 +2,8 @@
 "parity is not pinned at the sizes that are benched"):
 
 - C2: the bench's exact call - all 398 BERT-336M tensors, 16384-element
-  buckets, fp16 gradients, the AUTO (TMA ring) schedule - at W=1 and at W=8
+  buckets, fp16 gradients, the AUTO schedule (and ONCHIP at W=1, the
+  spilling word embedding included) - at W=1 and at W=8
   virtual ranks, every tensor's p, m and v against the pinned restatement
   co.lamb_oracle (tests/test_oracle_pinned.py pins it to the reference Engine's
   per-tensor LAMB programs bit for bit);
@@ -46,8 +47,8 @@ def _owners(tl, counts, W):
     return own
 
 
-@pytest.mark.parametrize("W", [1, 8])
-def test_lamb_bert336m_bench_call(W):
+@pytest.mark.parametrize("W,sched", [(1, _lib.LAMB_AUTO), (8, _lib.LAMB_AUTO), (1, _lib.LAMB_ONCHIP)])
+def test_lamb_bert336m_bench_call(W, sched):
     counts = bert_large_counts()
     assert sum(counts) == BERT_LARGE_PARAMS and len(counts) == 398
     N = sum(counts)
@@ -68,7 +69,7 @@ def test_lamb_bert336m_bench_call(W):
         m_old = [x.cpu().numpy() for x in _full_state(ctx, tl, m, counts, W)]
         v_old = [x.cpu().numpy() for x in _full_state(ctx, tl, v, counts, W)]
         p_old = [ctx.view(params[i], 0).cpu().numpy() for i in range(len(counts))]
-        hp = LambHParams(lr=1e-3, beta1=0.9, beta2=0.999, t=1.0, eps=1e-6, wd=0.01)  # bench.py's call
+        hp = LambHParams(lr=1e-3, beta1=0.9, beta2=0.999, t=1.0, eps=1e-6, wd=0.01, sched=sched)  # bench.py's call
         fused_rs_lamb_ag(ctx, tl, grads, params, m, v, hp)
         ctx.check()
         m_new = _full_state(ctx, tl, m, counts, W)

@@ -73,7 +73,8 @@ def test_adam_graph_replay_equals_eager(W, math):
     _same(_run(W, f, True), _run(W, f, False))
 
 
-@pytest.mark.parametrize("W,cap,sched", [(1, 16384, _lib.LAMB_TMA), (4, 1024, _lib.LAMB_GRID),
+@pytest.mark.parametrize("W,cap,sched", [(1, 16384, _lib.LAMB_TMA), (1, 16384, _lib.LAMB_ONCHIP),
+                                         (4, 1024, _lib.LAMB_GRID),
                                          (4, 16384, _lib.LAMB_TMA)])
 def test_lamb_graph_replay_equals_eager(W, cap, sched):
     """LAMB has a real cross-rank barrier mid-kernel (the norm exchange)."""
