@@ -647,6 +647,325 @@ __global__ void __launch_bounds__(FUSED ? kFusedThreads : kGemmThreads, 1)
   }
 }
 
+// ---- 2-SM pair GEMM with the B panel resident (plain GEMM, BN = 256) ----
+// At K = 384 a 128 x 256 tile is 25 MFLOP against 288 KB of A and B through
+// L2 -> SM (15.7 TB/s over the chip at the tensor peak); the operand loads
+// and the C stores together cost ~50 us over the MMAs (profiles/r01_gemm_diag.json).
+// Here two CTAs of a cluster run tcgen05.mma.cta_group::2 (M = 256, N = 256):
+// each CTA holds 128 rows of A and 128 columns of B and receives its 128 rows
+// x 256 columns of D in its own TMEM. B stays RESIDENT in shared memory for a
+// whole (rank, column block) panel (K x 128 bf16 = 96 KB at K = 384), so only
+// A streams: 96 KB per 2 x 25 MFLOP, 2.5x less L2 -> SM traffic.
+//   warp 0   producer (each CTA): B half panel on a panel change, A k-blocks
+//            into a 4-stage ring; both CTAs' loads complete on the LEADER's
+//            barriers (cp.async.bulk.tensor .cta_group::2)
+//   warp 1   MMA issuer (leader only); commits multicast to both CTAs
+//   warp 2   TMEM allocator (cta_group::2, both CTAs)
+//   warps 4-7 epilogue (each CTA): TMEM -> bf16 -> swizzled smem -> TMA store;
+//            one remote arrive per CTA on the leader's accumulator-empty barrier
+// Work: units (rank, 256-column block = panel, 256-row block). Pairs take
+// whole panels in rounds (pair p: panels p, p + P, ...) and walk their row
+// blocks in step, so the ~P/ranks pairs on one rank read the same A row block
+// at the same time (one DRAM read, L2 hits for the rest); the panels left
+// over after the last full round are split into equal unit ranges.
+constexpr int kPairMaxStages = 8;
+constexpr int kPairABytes = BM * BK * 2;       // 16 KB: 128 rows x 64 k
+constexpr int kPairBBytes = 2 * kMnBlockBytes;  // 16 KB per k-block: 2 boxes of 64 n x 64 k
+#ifndef COCONET_PAIR_EPI_BUFS
+#define COCONET_PAIR_EPI_BUFS 2
+#endif
+constexpr int kPairEpiBufs = COCONET_PAIR_EPI_BUFS;  // staging buffers per epilogue warp (4 KB each)
+constexpr int kPairEpiBytes = 4 * kPairEpiBufs * 4096;
+constexpr int kPairKMax = 512;
+
+// A stages: what the shared memory leaves after the B panel and the staging
+__host__ __device__ constexpr int pair_stages(int kblocks) {
+  return (227 * 1024 - kblocks * kPairBBytes - kPairEpiBytes - 1024 - 512) / kPairABytes < kPairMaxStages
+             ? (227 * 1024 - kblocks * kPairBBytes - kPairEpiBytes - 1024 - 512) / kPairABytes
+             : kPairMaxStages;
+}
+__host__ __device__ constexpr int pair_smem(int kblocks) {
+  return kblocks * kPairBBytes + pair_stages(kblocks) * kPairABytes + kPairEpiBytes + 1024 + 512;
+}
+
+__device__ __forceinline__ uint32_t mapa_leader(const void* p) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(r) : "r"(smem_u32(p)));
+  return r;
+}
+// Arrive on a barrier of either pair CTA (release at CTA scope, as CUTLASS's
+// ClusterBarrier::arrive(cta_id): .release.cluster compiles to a MEMBAR.ALL.GPU
+// per arrive, which serialised the producer)
+__device__ __forceinline__ void mbar_arrive_cl(uint32_t cl_bar) {
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cl_bar) : "memory");
+}
+// TMA load into this CTA's smem completing on a barrier of either pair CTA,
+// with an L2 eviction policy
+__device__ __forceinline__ void tma_load_2d_pair(void* dst, const CUtensorMap* map, int c0, int c1, uint32_t cl_bar,
+                                                 uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], "
+      "[%1, {%2, %3}], [%4], %5;" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(cl_bar), "l"(policy)
+      : "memory");
+}
+__device__ __forceinline__ void tma_store_2d_hint(const CUtensorMap* map, const void* src, int c0, int c1,
+                                                  uint64_t policy) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group.L2::cache_hint [%0, {%1, %2}], [%3], %4;" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(c0), "r"(c1), "r"(smem_u32(src)), "l"(policy)
+               : "memory");
+}
+__device__ __forceinline__ void mma_f16_pair(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(d),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc)
+      : "memory");
+}
+// arrive on `bar` (same offset) in both pair CTAs once the pair MMAs issued so far retire
+__device__ __forceinline__ void mma_commit_pair(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          smem_u32(bar)),
+      "h"(uint16_t(3))
+      : "memory");
+}
+
+// M = 256 (pair), N = 256, A K-major, B MN-major
+__device__ __forceinline__ uint32_t make_idesc_pair(uint32_t in_fmt) {
+  return (1u << 4) | (in_fmt << 7) | (in_fmt << 10) | (1u << 16) | (uint32_t(256 >> 3) << 17) |
+         (uint32_t(256 >> 4) << 24);
+}
+
+struct PairSched {
+  int P, p, mbs, np, rounds, lu0, lu1;
+  __device__ __forceinline__ PairSched(const GemmArgs& g, int pairs, int pair) : P(pairs), p(pair) {
+    mbs = g.tiles_m / 2;  // 256-row blocks
+    np = g.ranks * g.tiles_n;
+    rounds = np / P;
+    const int left = (np - rounds * P) * mbs;
+    lu0 = int(int64_t(left) * p / P);
+    lu1 = int(int64_t(left) * (p + 1) / P);
+  }
+  __device__ __forceinline__ int count() const { return rounds * mbs + (lu1 - lu0); }
+  __device__ __forceinline__ void unit(const GemmArgs& g, int i, int& r, int& nb, int& mb, int& panel) const {
+    if (i < rounds * mbs) {
+      const int k = i / mbs;
+      mb = i - k * mbs;
+      panel = k * P + p;
+    } else {
+      const int j = lu0 + (i - rounds * mbs);
+      panel = rounds * P + j / mbs;
+      mb = j - (j / mbs) * mbs;
+    }
+    r = panel / g.tiles_n;
+    nb = panel - r * g.tiles_n;
+  }
+};
+
+template <typename TO>
+__global__ void __launch_bounds__(kGemmThreads, 1) gemm_pair_kernel(const __grid_constant__ RankMaps maps, GemmArgs g,
+                                                                    uint32_t in_fmt) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int kblocks = g.K / BK;
+  const int NS = pair_stages(kblocks);
+  uint8_t* bpan = smem;                                // kblocks x 16 KB, B half panel
+  uint8_t* aring = bpan + kblocks * kPairBBytes;       // NS x 16 KB
+  uint8_t* epi = aring + NS * kPairABytes;             // 1024-aligned staging
+  uint64_t* full = reinterpret_cast<uint64_t*>(epi + kPairEpiBytes);  // leader: both A halves of a stage
+  uint64_t* empty = full + NS;                         // both: the pair MMAs on a stage retired
+  uint64_t* bfull = empty + NS;                        // leader: both B halves of a panel
+  uint64_t* bempty = bfull + 1;                        // both: the pair MMAs on a panel retired
+  uint64_t* tfull = bempty + 1;                        // [2] both: accumulator ready
+  uint64_t* tempty = tfull + 2;                        // [2] leader: both epilogues drained it
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t crank = cluster_ctarank();
+  if (warp == 0 && lane == 0) {
+    // full / bfull: the LEADER's producer arrives once with the bytes of both
+    // CTAs' loads; the peer's loads only complete transactions on it
+    for (int s = 0; s < NS; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(bfull, 1);
+    mbar_init(bempty, 1);
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 2);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(kTmemCols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();  // the peer's barriers exist before any remote arrive / multicast commit
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const PairSched ps(g, int(gridDim.x >> 1), int(blockIdx.x >> 1));
+  const int nu = ps.count();
+
+  if (warp == 0) {
+    if (lane == 0) {  // ---- TMA producer (both CTAs)
+      const uint32_t full_l = mapa_leader(full), bfull_l = mapa_leader(bfull);
+      // A row blocks are re-read by the other pairs on the rank: keep them in L2
+      // against the C write stream (stores are evict_first)
+      const uint64_t keep = createpolicy_evict_last();
+      int stage = 0;
+      uint32_t phase = 0;
+      int panel = -1, npanel = 0;
+      for (int u = 0; u < nu; ++u) {
+        int r, nb, mb, pid;
+        ps.unit(g, u, r, nb, mb, pid);
+        if (pid != panel) {
+          if (npanel > 0) mbar_wait(bempty, uint32_t(npanel - 1) & 1u);  // the old panel's MMAs retired
+          if (crank == 0) mbar_expect_tx(bfull, uint32_t(2 * kblocks * kPairBBytes));
+          for (int kb = 0; kb < kblocks; ++kb)
+#pragma unroll
+            for (int j = 0; j < 2; ++j)
+              tma_load_2d_pair(bpan + kb * kPairBBytes + j * kMnBlockBytes, &maps.b[r],
+                               nb * 256 + int(crank) * 128 + j * 64, kb * BK, bfull_l, keep);
+          panel = pid;
+          ++npanel;
+        }
+        for (int kb = 0; kb < kblocks; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          if (g.diag & 2) {  // profiling only: no A loads (MMAs on stale smem)
+            if (crank == 0) mbar_arrive(&full[stage]);
+          } else {
+            if (crank == 0) mbar_expect_tx(&full[stage], uint32_t(2 * kPairABytes));
+            tma_load_2d_pair(aring + stage * kPairABytes, &maps.a[r], kb * BK, mb * 256 + int(crank) * BM,
+                             full_l + uint32_t(stage * 8), keep);
+          }
+          if (++stage == NS) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && crank == 0) {  // ---- MMA issuer (leader)
+      const uint32_t idesc = make_idesc_pair(in_fmt);
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      int panel = -1, npanel = 0;
+      for (int u = 0; u < nu; ++u) {
+        int r, nb, mb, pid;
+        ps.unit(g, u, r, nb, mb, pid);
+        if (pid != panel) {
+          if (npanel > 0) mma_commit_pair(bempty);  // frees the old panel once its MMAs retire
+          mbar_wait(bfull, uint32_t(npanel) & 1u);
+          tc_fence_after();
+          panel = pid;
+          ++npanel;
+        }
+        mbar_wait(&tempty[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d = tmem + uint32_t(acc * kAccStride);
+        for (int kb = 0; kb < kblocks; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint64_t da = sw128_desc(aring + stage * kPairABytes);
+          const uint64_t db = sw128_mn_desc(bpan + kb * kPairBBytes);
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k)
+            mma_f16_pair(d, da + 2 * k, db + uint64_t(k) * ((16 * 128) >> 4), idesc, (kb | k) != 0);
+          mma_commit_pair(&empty[stage]);
+          if (++stage == NS) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        mma_commit_pair(&tfull[acc]);
+        acc ^= 1;
+        if (acc == 0) acc_phase ^= 1;
+      }
+    }
+  } else if (warp >= 4 && warp < 8) {  // ---- epilogue (both CTAs): rows mb*256 + crank*128 + ...
+    const int q = warp & 3;
+    uint8_t* stg = epi + q * kPairEpiBufs * 4096;
+    constexpr int kCols = 128 / int(sizeof(TO));
+    const uint32_t tempty_l = mapa_leader(tempty);
+    const uint64_t stream = createpolicy_evict_first();
+    int acc = 0, buf = 0;
+    uint32_t acc_phase = 0;
+    for (int u = 0; u < nu; ++u) {
+      int r, nb, mb, pid;
+      ps.unit(g, u, r, nb, mb, pid);
+      mbar_wait(&tfull[acc], acc_phase);
+      tc_fence_after();
+      const uint32_t tbase = tmem + (uint32_t(q * 32) << 16) + uint32_t(acc * kAccStride);
+#pragma unroll 1
+      for (int cc = 0; cc < 256 / kCols; ++cc) {
+        // this staging buffer was last read by the store issued kPairEpiBufs chunks ago
+        if (lane == 0) asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(kPairEpiBufs - 1) : "memory");
+        __syncwarp();
+        uint8_t* row = stg + buf * 4096 + lane * 128;
+        uint32_t h[32];
+        if constexpr (sizeof(TO) == 4) {
+          uint32_t v[32];
+          tmem_ld32(tbase + uint32_t(cc * 32), v);
+#pragma unroll
+          for (int i = 0; i < 32; ++i) h[i] = v[i];
+        } else {
+          uint32_t v[32], w[32];
+          tmem_ld32(tbase + uint32_t(cc * 64), v);
+          tmem_ld32(tbase + uint32_t(cc * 64 + 32), w);
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            TO lo = from_f32<TO>(__uint_as_float(v[2 * i])), hi = from_f32<TO>(__uint_as_float(v[2 * i + 1]));
+            h[i] = uint32_t(*reinterpret_cast<uint16_t*>(&lo)) | (uint32_t(*reinterpret_cast<uint16_t*>(&hi)) << 16);
+            TO lo2 = from_f32<TO>(__uint_as_float(w[2 * i])), hi2 = from_f32<TO>(__uint_as_float(w[2 * i + 1]));
+            h[16 + i] =
+                uint32_t(*reinterpret_cast<uint16_t*>(&lo2)) | (uint32_t(*reinterpret_cast<uint16_t*>(&hi2)) << 16);
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+          *reinterpret_cast<uint4*>(row + ((j ^ (lane & 7)) << 4)) =
+              make_uint4(h[4 * j], h[4 * j + 1], h[4 * j + 2], h[4 * j + 3]);
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+        if (lane == 0 && !(g.diag & 1)) {  // diag 1 (profiling only): no C stores
+          tma_store_2d_hint(&maps.c[r], stg + buf * 4096, nb * 256 + cc * kCols, mb * 256 + int(crank) * BM + q * 32,
+                            stream);
+          asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        }
+        if (++buf == kPairEpiBufs) buf = 0;
+      }
+      // this CTA's 128 epilogue threads are done with the accumulator: one
+      // arrive on the leader's barrier (count 2: both CTAs)
+      tc_fence_before();
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+      if (warp == 4 && lane == 0) mbar_arrive_cl(tempty_l + uint32_t(acc * 8));
+      acc ^= 1;
+      if (acc == 0) acc_phase ^= 1;
+    }
+    if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    __syncwarp();
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();  // no CTA leaves (or frees TMEM) while the pair's MMAs, commits or loads may touch it
+  tc_fence_after();
+  if (warp == 2)
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols) : "memory");
+}
+
 // EXACT: C = A x B with fp64 accumulation in k order (eval_matmul).
 struct ExactArgs {
   const float* a[kMaxRanks];
@@ -778,6 +1097,30 @@ int launch_tc_t(coconet_ctx* c, TcPlan* p, uint32_t in_fmt, const OvArgs* ov, cu
   OvArgs none{};
   const OvArgs& o = ov ? *ov : none;
   if constexpr (!FUSED) {
+    // BN = 256 with a B half panel that fits: the 2-SM pair kernel (B resident;
+    // COCONET_GEMM_PAIR=0 disables it)
+    const char* pe = getenv("COCONET_GEMM_PAIR");
+    if (BN == 256 && !(pe && pe[0] == '0') && p->g.tiles_m % 2 == 0 && p->g.K <= kPairKMax) {
+      const int psmem = pair_smem(p->g.K / BK);
+      auto fn = gemm_pair_kernel<TO>;
+      CN_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, psmem));
+      const int units = p->g.ranks * p->g.tiles_n * (p->g.tiles_m / 2);
+      cudaLaunchConfig_t cfg{};
+      cfg.gridDim = dim3(unsigned(2 * std::min(units, c->sm_count / 2)));
+      cfg.blockDim = dim3(kGemmThreads);
+      cfg.dynamicSmemBytes = size_t(psmem);
+      cfg.stream = s;
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeClusterDimension;
+      attr[0].val.clusterDim.x = 2;
+      attr[0].val.clusterDim.y = 1;
+      attr[0].val.clusterDim.z = 1;
+      cfg.attrs = attr;
+      cfg.numAttrs = 1;
+      CN_CUDA(cudaLaunchKernelEx(&cfg, fn, p->maps, p->g, in_fmt));
+      c->launches++;
+      return COCONET_OK;
+    }
     // COCONET_GEMM_MC: 0 = no clusters, a = pairs share A (default), b = pairs
     // share B (less L2 -> SM traffic, but no faster end to end at C3's shape:
     // profiles/r01_gemm_diag.json)
