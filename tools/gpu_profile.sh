@@ -11,7 +11,7 @@ timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --nvtx --n
    --log-file gpurun_out/launches.csv python bench.py --steps 5 --warmup 3 --no-cpu-baseline --no-extras --no-parity --no-baseline > gpurun_out/ncu_bench.log 2>&1; echo "ncu_launches=$?" >> $S
 timeout 900 ncu --set full --clock-control none --import-source on -k "regex:${LAMB_KERNEL:-lamb_onchip}" -s 3 -c 1 \
    -o gpurun_out/prof_lamb -f python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-extras --no-parity --no-baseline > gpurun_out/ncu_lamb.log 2>&1; echo "ncu_lamb=$?" >> $S
-timeout 900 ncu --set full --clock-control none --import-source on -k "regex:gemm_tc" -s 3 -c 1 \
+timeout 900 ncu --set full --clock-control none --import-source on -k "regex:gemm_pair" -s 3 -c 1 \
    -o gpurun_out/prof_gemm -f python tools/pattern_probe.py --only c3 --gemm-only > gpurun_out/ncu_gemm.log 2>&1; echo "ncu_gemm=$?" >> $S
 timeout 900 ncu --set full --clock-control none --import-source on -k "regex:rs_send_ag" -s 8 -c 1 \
    -o gpurun_out/prof_pp -f python tools/pattern_probe.py --only c4 > gpurun_out/ncu_pp.log 2>&1; echo "ncu_pp=$?" >> $S
