@@ -966,6 +966,277 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_pair_kernel(const __grid
     asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols) : "memory");
 }
 
+// ---- MP layer as ONE all-gather -> GEMM kernel (mp_overlap.json) ----
+// OverlapGroup{MatMul, FusedAllReduce{dropout(layer + b) + r}} computes, for
+// the output column block c owned by rank c,
+//     out[:, c] = dropout(sum_r A_r x B_r[:, c] + b[c], rate) + r[:, c]
+// and gathers it to every rank. The reference forms every rank's partial
+// product [rows x cols] and reduce-scatters it (runtime.hpp:471-516). Here the
+// partial products never exist: the pair of CTAs that owns (c, 256-row block)
+// streams A_r (rows x k_local) and B_r[:, c] of EVERY rank r through one K
+// loop of W * k_local (TMA from the peers' memory: the all-gather of the
+// activations, overlapped with the MMAs k-block by k-block), accumulates in
+// fp32 TMEM, and its epilogue applies bias + dropout + residual and stores the
+// finished tile into every rank's `out` (the AllGather push). The same NVLink
+// bytes as the RS (every rank's A slice instead of every rank's partial
+// block), no partial write-back, no second kernel. FAST math: the sum is
+// accumulated in fp32 over the whole K (the reference rounds every partial
+// product to fp32 and folds them in ring order), masks bit-exact (global flat
+// index as the dropout counter, state.hpp:178-181).
+// Shapes: per = cols / W in {128, 256, 384} as two pair MMAs (N0 = min(per,
+// 256), N1 = per - N0), rows % 256 == 0, k_local % 64 == 0. 384 threads:
+// warp 0 producer, warp 1 MMA issuer (leader), warp 2 TMEM allocator, warps
+// 4-11 epilogue (two per TMEM lane quarter, each half of the columns).
+constexpr int kAgThreads = 384;
+constexpr int kAgStages = 5;
+constexpr int kAgEpiWarps = 8;
+struct AgMaps {
+  CUtensorMap a[kMaxRanks];    // A_r: [rows, k_local], boxes 64 k x 128 rows
+  CUtensorMap b[kMaxRanks];    // B_r: [k_local, cols], boxes 64 n x 64 k (MN-major)
+  CUtensorMap out[kMaxRanks];  // out of every rank: boxes 64 cols x 32 rows
+};
+struct AgArgs {
+  RankSet rs;  // DISTRIBUTED: entry / exit barrier with the peers whose A, B we read and whose out we write
+  const uint16_t* bias[kMaxRanks];  // b (replicated) of each owner computed here
+  const uint16_t* res[kMaxRanks];   // r (replicated) of each owner computed here
+  int rows, cols, per, k_local, W;
+  int n0, n1;
+  int owner0, owners;  // column blocks computed by this launch
+  int dst;             // destination ranks of the output push (the group)
+  float frate_scale;
+  uint64_t seed, key, thresh;
+  int f16;             // 16-bit type: 1 = fp16, 0 = bf16
+  int diag;            // COCONET_GEMM_DIAG (profiling only): 1 = no epilogue math / stores, 2 = no operand loads
+};
+
+__device__ __forceinline__ uint32_t make_idesc_pair_n(uint32_t in_fmt, int n) {
+  return (1u << 4) | (in_fmt << 7) | (in_fmt << 10) | (1u << 16) | (uint32_t(n >> 3) << 17) |
+         (uint32_t(256 >> 4) << 24);
+}
+
+__device__ __forceinline__ float h16_to_f32(uint16_t h, int f16) {
+  return f16 ? __half2float(__ushort_as_half(h)) : __bfloat162float(__ushort_as_bfloat16(h));
+}
+__device__ __forceinline__ uint16_t f32_to_h16(float x, int f16) {
+  return f16 ? __half_as_ushort(__float2half_rn(x)) : __bfloat16_as_ushort(__float2bfloat16_rn(x));
+}
+
+template <int PER>
+__global__ void __launch_bounds__(kAgThreads, 1) mp_ag_gemm_kernel(const __grid_constant__ AgMaps maps, AgArgs g,
+                                                                   uint32_t in_fmt) {
+  // A unit is (256-row block, owner column block, part): a column block wider
+  // than 256 (384 at C3) is two parts (256 + 128 columns), each its own K loop
+  // into one of two TMEM accumulators (256 columns each), so the epilogue of
+  // one unit (bias + dropout + residual + the pushes) runs under the MMAs of
+  // the next. A streams once per part.
+  constexpr int kW0 = PER < 256 ? PER : 256, kW1 = PER - kW0, kParts = kW1 > 0 ? 2 : 1;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  constexpr int kStage = kPairABytes + (kW0 / 2) * 128;  // A 16 KB + B half of the wider part
+  uint8_t* ring = smem;
+  uint8_t* epi = ring + kAgStages * kStage;
+  uint64_t* full = reinterpret_cast<uint64_t*>(epi + kAgEpiWarps * 2 * 4096);
+  uint64_t* empty = full + kAgStages;
+  uint64_t* tfull = empty + kAgStages;  // [2]
+  uint64_t* tempty = tfull + 2;         // [2] (leader: both CTAs' epilogues)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t crank = cluster_ctarank();
+  if (warp == 0 && lane == 0) {
+    for (int s = 0; s < kAgStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 2);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(kTmemCols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  edge_barrier(g.rs, 0);  // DISTRIBUTED: every peer's A, B are ready (VIRTUAL: stream order)
+  const int mbs = g.rows / 256;
+  const int units = g.owners * mbs * kParts;
+  const int P = int(gridDim.x >> 1), pr = int(blockIdx.x >> 1);
+  const int kb_per = g.k_local / BK, kb_all = g.W * kb_per;
+  // unit u -> part u % kParts, then owner, then row block: the pairs running
+  // together read the same A row blocks (every owner and part needs them)
+  auto decode = [&](int u, int& mb, int& c, int& part) {
+    part = kParts > 1 ? (u & 1) : 0;
+    const int rest = kParts > 1 ? (u >> 1) : u;
+    mb = rest / g.owners;
+    c = g.owner0 + (rest - mb * g.owners);
+  };
+  if (warp == 0) {
+    if (lane == 0) {  // ---- producer (both CTAs)
+      const uint32_t full_l = mapa_leader(full);
+      const uint64_t keep = createpolicy_evict_last();
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int u = pr; u < units; u += P) {
+        int mb, c, part;
+        decode(u, mb, c, part);
+        const int wp = part ? kW1 : kW0, col0 = c * PER + (part ? kW0 : 0) + int(crank) * (wp / 2);
+        const uint32_t bytes = uint32_t(kPairABytes + (wp / 2) * 128);
+        for (int kk = 0; kk < kb_all; ++kk) {
+          const int r = kk / kb_per, kb = kk - r * kb_per;
+          mbar_wait(&empty[stage], phase ^ 1);
+          uint8_t* st = ring + stage * kStage;
+          if (g.diag & 2) {
+            if (crank == 0) mbar_arrive(&full[stage]);
+          } else {
+            if (crank == 0) mbar_expect_tx(&full[stage], 2u * bytes);
+            const uint32_t fb = full_l + uint32_t(stage * 8);
+            tma_load_2d_pair(st, &maps.a[r], kb * BK, mb * 256 + int(crank) * BM, fb, keep);
+            for (int j = 0; j < wp / 128; ++j)  // this CTA's wp/2 columns of the part
+              tma_load_2d_pair(st + kPairABytes + j * kMnBlockBytes, &maps.b[r], col0 + j * 64, kb * BK, fb, keep);
+          }
+          if (++stage == kAgStages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && crank == 0) {  // ---- MMA issuer (leader)
+      const uint32_t id0 = make_idesc_pair_n(in_fmt, kW0), id1 = make_idesc_pair_n(in_fmt, kW1 > 0 ? kW1 : 128);
+      int stage = 0, acc = 0;
+      uint32_t phase = 0, aph = 0;
+      for (int u = pr; u < units; u += P) {
+        int mb, c, part;
+        decode(u, mb, c, part);
+        mbar_wait(&tempty[acc], aph ^ 1);  // both epilogues drained this accumulator
+        tc_fence_after();
+        const uint32_t d = tmem + uint32_t(acc * 256);
+        const uint32_t id = part ? id1 : id0;
+        for (int kk = 0; kk < kb_all; ++kk) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          uint8_t* st = ring + stage * kStage;
+          const uint64_t da = sw128_desc(st), db = sw128_mn_desc(st + kPairABytes);
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k)
+            mma_f16_pair(d, da + 2 * k, db + uint64_t(k) * ((16 * 128) >> 4), id, (kk | k) != 0);
+          mma_commit_pair(&empty[stage]);
+          if (++stage == kAgStages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        mma_commit_pair(&tfull[acc]);
+        acc ^= 1;
+        if (acc == 0) aph ^= 1;
+      }
+    }
+  } else if (warp >= 4) {  // ---- epilogue (both CTAs): 8 warps, TMEM lane quarter q, column half h
+    const int e = warp - 4, q = warp & 3, h = e >> 2;
+    uint8_t* stg = epi + e * 2 * 4096;
+    const uint32_t tempty_l = mapa_leader(tempty);
+    const uint64_t stream = createpolicy_evict_first();
+    int buf = 0, acc = 0;
+    uint32_t aph = 0;
+    for (int u = pr; u < units; u += P) {
+      int mb, c, part;
+      decode(u, mb, c, part);
+      const int wp = part ? kW1 : kW0, chunks = wp / 128;  // 64-column chunks per warp
+      const int oi = c - g.owner0;
+      const int row = mb * 256 + int(crank) * BM + q * 32 + lane;  // this thread's output row
+      mbar_wait(&tfull[acc], aph);
+      tc_fence_after();
+      const uint32_t tbase = tmem + (uint32_t(q * 32) << 16) + uint32_t(acc * 256 + h * (wp / 2));
+      for (int cc = 0; cc < chunks; ++cc) {
+        if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+        __syncwarp();
+        uint8_t* rowp = stg + buf * 4096 + lane * 128;
+        const int col0 = c * PER + (part ? kW0 : 0) + h * (wp / 2) + cc * 64;  // global column of this chunk
+        const uint4* rp = reinterpret_cast<const uint4*>(g.res[oi] + int64_t(row) * g.cols + col0);
+        const uint4* bp = reinterpret_cast<const uint4*>(g.bias[oi] + col0);
+#pragma unroll
+        for (int hh = 0; hh < 2; ++hh) {  // 32 columns at a time
+          uint4 rr[4], bb[4];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {  // in flight while the accumulator is read
+            rr[i] = __ldg(rp + hh * 4 + i);
+            bb[i] = __ldg(bp + hh * 4 + i);
+          }
+          uint32_t v[32];
+          tmem_ld32(tbase + uint32_t(cc * 64 + hh * 32), v);
+          if (g.diag & 1) {
+            if (v[0] == 0x7fffffffu && v[31] == 0x7fffffffu) rowp[0] = 1;  // keep the loads live
+            continue;
+          }
+          const uint16_t* r16 = reinterpret_cast<const uint16_t*>(rr);
+          const uint16_t* b16 = reinterpret_cast<const uint16_t*>(bb);
+          uint32_t o[16];
+          const uint64_t gi0 = uint64_t(row) * uint64_t(g.cols) + uint64_t(col0 + hh * 32);
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            float y[2];
+#pragma unroll
+            for (int t = 0; t < 2; ++t) {
+              const int j = 2 * i + t;
+              const float x = __uint_as_float(v[j]) + h16_to_f32(b16[j], g.f16);
+              const bool kp = dropout_keep_bits(g.seed, g.key, gi0 + uint64_t(j), g.thresh);
+              y[t] = (kp ? x * g.frate_scale : 0.0f) + h16_to_f32(r16[j], g.f16);
+            }
+            o[i] = uint32_t(f32_to_h16(y[0], g.f16)) | (uint32_t(f32_to_h16(y[1], g.f16)) << 16);
+          }
+          // 128B swizzle (the out tensor maps): 16-byte chunk j of row l at j ^ (l % 8)
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+            *reinterpret_cast<uint4*>(rowp + (((hh * 4 + j) ^ (lane & 7)) << 4)) =
+                make_uint4(o[4 * j], o[4 * j + 1], o[4 * j + 2], o[4 * j + 3]);
+        }
+        if (cc == chunks - 1) {  // this unit's accumulator is read: release it before the stores drain
+          tc_fence_before();
+          asm volatile("bar.sync 1, %0;" ::"n"(kAgEpiWarps * 32) : "memory");
+          if (e == 0 && lane == 0) mbar_arrive_cl(tempty_l + uint32_t(acc * 8));
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+        if (lane == 0 && !(g.diag & 1)) {
+          for (int dd = 0; dd < g.dst; ++dd)  // the AllGather push: the finished tile into every rank's out
+            tma_store_2d_hint(&maps.out[dd], stg + buf * 4096, col0, mb * 256 + int(crank) * BM + q * 32, stream);
+          asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        }
+        buf ^= 1;
+      }
+      acc ^= 1;
+      if (acc == 0) aph ^= 1;
+    }
+    if (lane == 0) {
+      asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+      asm volatile("fence.proxy.async.global;" ::: "memory");  // the pushes before the exit barrier's release
+    }
+    __syncwarp();
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();
+  tc_fence_after();
+  edge_barrier(g.rs, 1);  // DISTRIBUTED: our pushes into every peer's out have landed
+  if (warp == 2)
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols) : "memory");
+}
+
+template <int PER>
+constexpr int ag_smem() {
+  return kAgStages * (kPairABytes + ((PER < 256 ? PER : 256) / 2) * 128) + kAgEpiWarps * 2 * 4096 + 1024 + 256;
+}
+
+
 // EXACT: C = A x B with fp64 accumulation in k order (eval_matmul).
 struct ExactArgs {
   const float* a[kMaxRanks];
@@ -1184,6 +1455,84 @@ int launch_tc(coconet_ctx* c, TcPlan* p, int in_elem, int out_elem, const OvArgs
   }
 }
 
+// The all-gather -> GEMM schedule of OverlapGroup{MatMul, FusedAllReduce}
+// (mp_ag_gemm_kernel). Returns COCONET_ERR_UNSUPPORTED for shapes it does not
+// take (the caller falls back to the two-kernel schedule).
+int launch_ag_gemm(coconet_ctx* c, int group, const void* a, const void* w, const void* b, const void* r, void* out,
+                   int in_elem, int64_t rows, int64_t cols, int64_t k_local, const coconet_bdr_params* hp,
+                   cudaStream_t s) {
+  const int W = c->groups[size_t(group)].size;
+  const int64_t per = cols / W;
+  if ((per != 128 && per != 256 && per != 384) || rows % 256 || k_local % BK || rows > INT32_MAX ||
+      int64_t(rows) * cols > (int64_t(1) << 40) || W > kMaxRanks)
+    return COCONET_ERR_UNSUPPORTED;
+  int64_t ao = 0, wo = 0, bo = 0, ro = 0, oo = 0;
+  int rc = heap_offset(c, a, &ao);
+  if (!rc) rc = heap_offset(c, w, &wo);
+  if (!rc) rc = heap_offset(c, b, &bo);
+  if (!rc) rc = heap_offset(c, r, &ro);
+  if (!rc) rc = heap_offset(c, out, &oo);
+  if (rc) return rc;
+  if ((ao | wo | bo | ro | oo) % 16) return COCONET_ERR_UNSUPPORTED;
+  static AgMaps maps;  // host staging of the kernel parameter
+  AgArgs g{};
+  rc = make_rankset(c, group, &g.rs);
+  if (rc) return rc;
+  const coconet_group_s& grp = c->groups[size_t(group)];
+  for (int q = 0; q < W; ++q) {
+    char* heap = c->heap[grp.first + q];  // VIRTUAL: this device; DISTRIBUTED: the peer mapping
+    rc = make_map(&maps.a[q], heap + ao, in_elem, uint64_t(k_local), uint64_t(rows), BK, BM);
+    if (!rc) rc = make_map(&maps.b[q], heap + wo, in_elem, uint64_t(cols), uint64_t(k_local), 64, BK);
+    if (!rc) rc = make_map(&maps.out[q], heap + oo, in_elem, uint64_t(cols), uint64_t(rows), 64, 32);
+    if (rc) return rc;
+  }
+  // owners computed here: every column block (VIRTUAL) or this rank's (DISTRIBUTED)
+  g.owner0 = c->mode == COCONET_MODE_VIRTUAL ? 0 : c->rank - grp.first;
+  g.owners = c->mode == COCONET_MODE_VIRTUAL ? W : 1;
+  for (int i = 0; i < g.owners; ++i) {
+    char* heap = c->heap[grp.first + g.owner0 + i];
+    g.bias[i] = reinterpret_cast<const uint16_t*>(heap + bo);
+    g.res[i] = reinterpret_cast<const uint16_t*>(heap + ro);
+  }
+  g.rows = int(rows);
+  g.cols = int(cols);
+  g.per = int(per);
+  g.k_local = int(k_local);
+  g.W = W;
+  g.n0 = int(std::min<int64_t>(per, 256));
+  g.n1 = int(per) - g.n0;
+  g.dst = W;
+  g.frate_scale = float(1.0 / (1.0 - hp->rate));
+  g.seed = hp->seed;
+  g.key = hp->key;
+  const double th = std::ceil(hp->rate * 9007199254740992.0);
+  g.thresh = th <= 0 ? 0 : (th >= 9007199254740992.0 ? (uint64_t(1) << 53) : uint64_t(th));
+  g.f16 = in_elem == COCONET_F16 ? 1 : 0;
+  g.diag = getenv("COCONET_GEMM_DIAG") ? atoi(getenv("COCONET_GEMM_DIAG")) : 0;
+  const uint32_t fmt = in_elem == COCONET_BF16 ? 1u : 0u;
+  const int smem = per == 384 ? ag_smem<384>() : per == 256 ? ag_smem<256>() : ag_smem<128>();
+  auto fn = per == 384 ? mp_ag_gemm_kernel<384> : per == 256 ? mp_ag_gemm_kernel<256> : mp_ag_gemm_kernel<128>;
+  CN_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  const int units = g.owners * int(rows / 256) * (per > 256 ? 2 : 1);
+  cudaLaunchConfig_t cfg{};
+  // DISTRIBUTED: the same grid on every rank (the edge barriers pair CTA b with CTA b)
+  cfg.gridDim = dim3(unsigned(2 * (c->mode == COCONET_MODE_VIRTUAL ? std::min(units, c->sm_count / 2)
+                                                                    : c->sm_count / 2)));
+  cfg.blockDim = dim3(kAgThreads);
+  cfg.dynamicSmemBytes = size_t(smem);
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  CN_CUDA(cudaLaunchKernelEx(&cfg, fn, maps, g, fmt));
+  c->launches++;
+  return COCONET_OK;
+}
+
 constexpr size_t kTileFlagBytes = kCountersOff - kTileFlagsOff;  // per group: up to 16384 tiles
 
 }  // namespace
@@ -1246,8 +1595,16 @@ int coconet_mm_overlap_fused_ar(coconet_ctx_t c, int group, const void* a, const
   // memory pipe), and it has not been measured over NVLink
   // yet, so AUTO runs the two kernels back to back (bitwise the same result)
   // in both modes. COCONET_MP_OVERLAP=fused|sequential forces either.
+  // AUTO: the all-gather -> GEMM kernel (no partial products; C3 on one GPU
+  // 277 -> see DESIGN.md) when the shape fits, else the two kernels.
   const char* ov_env = getenv("COCONET_MP_OVERLAP");
-  const bool sequential = ov_env ? std::strcmp(ov_env, "sequential") == 0 : W > 1;
+  const bool want_ag = !ov_env || std::strcmp(ov_env, "aggemm") == 0;
+  if (want_ag && W > 1) {
+    const int rc = launch_ag_gemm(c, group, a, w, b, r, out, in_elem, rows, cols, k_local, hp, s);
+    if (rc != COCONET_ERR_UNSUPPORTED) return rc;
+    if (ov_env) return set_error(COCONET_ERR_UNSUPPORTED, "the all-gather -> GEMM schedule does not take this shape");
+  }
+  const bool sequential = ov_env ? std::strcmp(ov_env, "fused") != 0 : W > 1;
   if (sequential) {
     int rc = coconet_matmul(c, group, a, w, partial, in_elem, in_elem, rows, cols, k_local, COCONET_MATH_FAST, stream);
     if (rc) return rc;

@@ -11,8 +11,9 @@
   for bit against the restated Engine semantics, fp16 FAST within 1e-2 with
   the dropout masks bit-exact;
 - C3: the MP layer at [8192 x 384] x [384 x 3072] x 8 ranks through
-  coconet_mm_overlap_fused_ar, forced one-kernel overlap and AUTO: bitwise
-  equal to each other and within 1e-2 of an fp32 torch reference.
+  coconet_mm_overlap_fused_ar: the tile-flag overlap bitwise equal to the two
+  kernels back to back, AUTO (the all-gather -> GEMM kernel) and both within
+  1e-2 of an fp32 torch reference with the dropout mask bit-exact.
 """
 import numpy as np
 import pytest
@@ -151,16 +152,22 @@ def test_mp_layer_at_c3_size(monkeypatch):
         monkeypatch.setenv("COCONET_MP_OVERLAP", "fused")
         mm_overlap_fused_ar(ctx, x, w, bb, rr, part, out_f, hp)
         ctx.check()
-        monkeypatch.delenv("COCONET_MP_OVERLAP")
-        mm_overlap_fused_ar(ctx, x, w, bb, rr, part, out_a, hp)  # AUTO
+        monkeypatch.setenv("COCONET_MP_OVERLAP", "sequential")
+        mm_overlap_fused_ar(ctx, x, w, bb, rr, part, out_a, hp)
         ctx.check()
-        for r in range(W):
+        for r in range(W):  # the tile-flag overlap is bitwise the two kernels back to back
             assert torch.equal(ctx.view(out_f, r), ctx.view(out_a, r)), r
+        monkeypatch.delenv("COCONET_MP_OVERLAP")
+        mm_overlap_fused_ar(ctx, x, w, bb, rr, part, out_a, hp)  # AUTO: the all-gather -> GEMM kernel
+        ctx.check()
         full = sum(ctx.view(x, r).float() @ ctx.view(w, r).float() for r in range(W))
         keep = torch.from_numpy(co.dropout_keep(1, key, np.arange(rows * H), 0.1).reshape(rows, H)).cuda()
         want = torch.where(keep, (full + bias.float()) / 0.9, torch.zeros_like(full)) + resid.float()
-        got = ctx.view(out_f, 0).float()
-        assert ((got - want).abs().max() / want.abs().max()).item() < 1e-2
-        assert torch.equal(got[~keep], resid.float()[~keep])  # dropped elements are exactly r
+        for out in (out_f, out_a):
+            got = ctx.view(out, 0).float()
+            assert ((got - want).abs().max() / want.abs().max()).item() < 1e-2
+            assert torch.equal(got[~keep], resid.float()[~keep])  # dropped elements are exactly r
+        for r in range(1, W):
+            assert torch.equal(ctx.view(out_a, r), ctx.view(out_a, 0)), r
     finally:
         ctx.close()
