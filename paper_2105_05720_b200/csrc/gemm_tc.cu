@@ -709,6 +709,14 @@ __device__ __forceinline__ void tma_load_2d_pair(void* dst, const CUtensorMap* m
       "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(cl_bar), "l"(policy)
       : "memory");
 }
+__device__ __forceinline__ void tma_load_2d_hint(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar,
+                                                 uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, {%2, "
+      "%3}], [%4], %5;" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar)), "l"(policy)
+      : "memory");
+}
 __device__ __forceinline__ void tma_store_2d_hint(const CUtensorMap* map, const void* src, int c0, int c1,
                                                   uint64_t policy) {
   asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group.L2::cache_hint [%0, {%1, %2}], [%3], %4;" ::"l"(
@@ -988,12 +996,14 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_pair_kernel(const __grid
 // warp 0 producer, warp 1 MMA issuer (leader), warp 2 TMEM allocator, warps
 // 4-11 epilogue (two per TMEM lane quarter, each half of the columns).
 constexpr int kAgThreads = 384;
-constexpr int kAgStages = 5;
+constexpr int kAgStages = 4;
+constexpr int kAgEpiBufs = 3;  // per epilogue warp: residual in, result out, in place
 constexpr int kAgEpiWarps = 8;
 struct AgMaps {
   CUtensorMap a[kMaxRanks];    // A_r: [rows, k_local], boxes 64 k x 128 rows
   CUtensorMap b[kMaxRanks];    // B_r: [k_local, cols], boxes 64 n x 64 k (MN-major)
-  CUtensorMap out[kMaxRanks];  // out of every rank: boxes 64 cols x 32 rows
+  CUtensorMap out[kMaxRanks];  // out of every rank: boxes 64 cols x 128 rows
+  CUtensorMap res[kMaxRanks];  // r (replicated) of each owner computed here: boxes 64 cols x 128 rows
 };
 struct AgArgs {
   RankSet rs;  // DISTRIBUTED: entry / exit barrier with the peers whose A, B we read and whose out we write
@@ -1035,7 +1045,7 @@ __global__ void __launch_bounds__(kAgThreads, 1) mp_ag_gemm_kernel(const __grid_
   constexpr int kStage = kPairABytes + (kW0 / 2) * 128;  // A 16 KB + B half of the wider part
   uint8_t* ring = smem;
   uint8_t* epi = ring + kAgStages * kStage;
-  uint64_t* full = reinterpret_cast<uint64_t*>(epi + kAgEpiWarps * 2 * 4096);
+  uint64_t* full = reinterpret_cast<uint64_t*>(epi + 2 * kAgEpiBufs * 16384);
   uint64_t* empty = full + kAgStages;
   uint64_t* tfull = empty + kAgStages;  // [2]
   uint64_t* tempty = tfull + 2;         // [2] (leader: both CTAs' epilogues)
@@ -1051,6 +1061,8 @@ __global__ void __launch_bounds__(kAgThreads, 1) mp_ag_gemm_kernel(const __grid_
       mbar_init(&tfull[a], 1);
       mbar_init(&tempty[a], 2);
     }
+    uint64_t* rb = reinterpret_cast<uint64_t*>(tmem_slot + 2);  // the epilogue warps' residual loads
+    for (int i = 0; i < 2 * kAgEpiBufs; ++i) mbar_init(&rb[i], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   }
@@ -1141,80 +1153,121 @@ __global__ void __launch_bounds__(kAgThreads, 1) mp_ag_gemm_kernel(const __grid_
       }
     }
   } else if (warp >= 4) {  // ---- epilogue (both CTAs): 8 warps, TMEM lane quarter q, column half h
+    // The 4 warps of a column half h (one per TMEM lane quarter) work on
+    // 128-row x 64-column chunks together: the residual chunk comes in by one
+    // TMA load (one chunk ahead) into a 16 KB staging buffer, every thread
+    // reads its row, adds bias + dropout(accumulator) and writes the result
+    // back in place, and one thread pushes the buffer into every rank's `out`
+    // (8 x 16 KB bulk stores; 4 KB boxes per warp were store-issue bound).
+    // Three buffers per half: load n+1, compute n, stores of n-1 draining.
     const int e = warp - 4, q = warp & 3, h = e >> 2;
-    uint8_t* stg = epi + e * 2 * 4096;
+    const bool lead = q == 0 && lane == 0;  // issues this half's loads and stores
+    uint8_t* hstg = epi + h * kAgEpiBufs * 16384;
+    uint64_t* rbar = reinterpret_cast<uint64_t*>(tmem_slot + 2) + h * kAgEpiBufs;
     const uint32_t tempty_l = mapa_leader(tempty);
     const uint64_t stream = createpolicy_evict_first();
-    int buf = 0, acc = 0;
-    uint32_t aph = 0;
-    for (int u = pr; u < units; u += P) {
-      int mb, c, part;
-      decode(u, mb, c, part);
-      const int wp = part ? kW1 : kW0, chunks = wp / 128;  // 64-column chunks per warp
-      const int oi = c - g.owner0;
-      const int row = mb * 256 + int(crank) * BM + q * 32 + lane;  // this thread's output row
-      mbar_wait(&tfull[acc], aph);
-      tc_fence_after();
-      const uint32_t tbase = tmem + (uint32_t(q * 32) << 16) + uint32_t(acc * 256 + h * (wp / 2));
-      for (int cc = 0; cc < chunks; ++cc) {
-        if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
-        __syncwarp();
-        uint8_t* rowp = stg + buf * 4096 + lane * 128;
-        const int col0 = c * PER + (part ? kW0 : 0) + h * (wp / 2) + cc * 64;  // global column of this chunk
-        const uint4* rp = reinterpret_cast<const uint4*>(g.res[oi] + int64_t(row) * g.cols + col0);
-        const uint4* bp = reinterpret_cast<const uint4*>(g.bias[oi] + col0);
-#pragma unroll
-        for (int hh = 0; hh < 2; ++hh) {  // 32 columns at a time
-          uint4 rr[4], bb[4];
-#pragma unroll
-          for (int i = 0; i < 4; ++i) {  // in flight while the accumulator is read
-            rr[i] = __ldg(rp + hh * 4 + i);
-            bb[i] = __ldg(bp + hh * 4 + i);
-          }
-          uint32_t v[32];
-          tmem_ld32(tbase + uint32_t(cc * 64 + hh * 32), v);
-          if (g.diag & 1) {
-            if (v[0] == 0x7fffffffu && v[31] == 0x7fffffffu) rowp[0] = 1;  // keep the loads live
-            continue;
-          }
-          const uint16_t* r16 = reinterpret_cast<const uint16_t*>(rr);
-          const uint16_t* b16 = reinterpret_cast<const uint16_t*>(bb);
-          uint32_t o[16];
-          const uint64_t gi0 = uint64_t(row) * uint64_t(g.cols) + uint64_t(col0 + hh * 32);
-#pragma unroll
-          for (int i = 0; i < 16; ++i) {
-            float y[2];
-#pragma unroll
-            for (int t = 0; t < 2; ++t) {
-              const int j = 2 * i + t;
-              const float x = __uint_as_float(v[j]) + h16_to_f32(b16[j], g.f16);
-              const bool kp = dropout_keep_bits(g.seed, g.key, gi0 + uint64_t(j), g.thresh);
-              y[t] = (kp ? x * g.frate_scale : 0.0f) + h16_to_f32(r16[j], g.f16);
-            }
-            o[i] = uint32_t(f32_to_h16(y[0], g.f16)) | (uint32_t(f32_to_h16(y[1], g.f16)) << 16);
-          }
-          // 128B swizzle (the out tensor maps): 16-byte chunk j of row l at j ^ (l % 8)
-#pragma unroll
-          for (int j = 0; j < 4; ++j)
-            *reinterpret_cast<uint4*>(rowp + (((hh * 4 + j) ^ (lane & 7)) << 4)) =
-                make_uint4(o[4 * j], o[4 * j + 1], o[4 * j + 2], o[4 * j + 3]);
-        }
-        if (cc == chunks - 1) {  // this unit's accumulator is read: release it before the stores drain
-          tc_fence_before();
-          asm volatile("bar.sync 1, %0;" ::"n"(kAgEpiWarps * 32) : "memory");
-          if (e == 0 && lane == 0) mbar_arrive_cl(tempty_l + uint32_t(acc * 8));
-        }
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        __syncwarp();
-        if (lane == 0 && !(g.diag & 1)) {
-          for (int dd = 0; dd < g.dst; ++dd)  // the AllGather push: the finished tile into every rank's out
-            tma_store_2d_hint(&maps.out[dd], stg + buf * 4096, col0, mb * 256 + int(crank) * BM + q * 32, stream);
-          asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-        }
-        buf ^= 1;
+    struct It {
+      int u, cc, mb, c, part, chunks;
+    };
+    auto first = [&](int u, It& it) {
+      it.u = u;
+      it.cc = 0;
+      if (u < units) {
+        decode(u, it.mb, it.c, it.part);
+        it.chunks = (it.part ? kW1 : kW0) / 128;
       }
-      acc ^= 1;
-      if (acc == 0) aph ^= 1;
+    };
+    auto advance = [&](It& it) {
+      if (++it.cc == it.chunks) first(it.u + P, it);
+    };
+    auto col_of = [&](const It& it) {
+      const int wp = it.part ? kW1 : kW0;
+      return it.c * PER + (it.part ? kW0 : 0) + h * (wp / 2) + it.cc * 64;
+    };
+    auto row0_of = [&](const It& it) { return it.mb * 256 + int(crank) * BM; };
+    auto load_res = [&](const It& it, int b) {  // lead thread
+      mbar_expect_tx(&rbar[b], 16384u);
+      tma_load_2d_hint(hstg + b * 16384, &maps.res[it.c - g.owner0], col_of(it), row0_of(it), &rbar[b], stream);
+    };
+    It cur, nxt;
+    first(pr, cur);
+    nxt = cur;
+    int n = 0;  // chunks processed by this half
+    if (lead && cur.u < units && !(g.diag & 1)) load_res(cur, 0);
+    int acc = 0;
+    uint32_t aph = 0;
+    while (cur.u < units) {
+      const int b = n % kAgEpiBufs;
+      advance(nxt);
+      // prefetch the next chunk's residual: its buffer was last pushed by
+      // chunk n-2 (all but the last committed group have been read)
+      if (lead && nxt.u < units && !(g.diag & 1)) {
+        asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+        load_res(nxt, (n + 1) % kAgEpiBufs);
+      }
+      if (cur.cc == 0) {
+        mbar_wait(&tfull[acc], aph);
+        tc_fence_after();
+      }
+      const int wp = cur.part ? kW1 : kW0;
+      const uint32_t tbase = tmem + (uint32_t(q * 32) << 16) + uint32_t(acc * 256 + h * (wp / 2));
+      const int col0 = col_of(cur), row = row0_of(cur) + q * 32 + lane;
+      const int oi = cur.c - g.owner0;
+      if (!(g.diag & 1)) mbar_wait(&rbar[b], uint32_t(n / kAgEpiBufs) & 1u);
+      uint8_t* rowp = hstg + b * 16384 + (q * 32 + lane) * 128;
+      const uint4* bp = reinterpret_cast<const uint4*>(g.bias[oi] + col0);
+#pragma unroll
+      for (int hh = 0; hh < 2; ++hh) {  // 32 columns at a time
+        uint4 bb[4], rr[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          bb[i] = __ldg(bp + hh * 4 + i);
+          rr[i] = *reinterpret_cast<const uint4*>(rowp + (((hh * 4 + i) ^ (lane & 7)) << 4));
+        }
+        uint32_t v[32];
+        tmem_ld32(tbase + uint32_t(cur.cc * 64 + hh * 32), v);
+        if (g.diag & 1) {
+          if (v[0] == 0x7fffffffu && v[31] == 0x7fffffffu) rowp[0] = 1;  // keep the loads live
+          continue;
+        }
+        const uint16_t* r16 = reinterpret_cast<const uint16_t*>(rr);
+        const uint16_t* b16 = reinterpret_cast<const uint16_t*>(bb);
+        uint32_t o[16];
+        const uint64_t gi0 = uint64_t(row) * uint64_t(g.cols) + uint64_t(col0 + hh * 32);
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          float y[2];
+#pragma unroll
+          for (int t = 0; t < 2; ++t) {
+            const int j = 2 * i + t;
+            const float x = __uint_as_float(v[j]) + h16_to_f32(b16[j], g.f16);
+            const bool kp = dropout_keep_bits(g.seed, g.key, gi0 + uint64_t(j), g.thresh);
+            y[t] = (kp ? x * g.frate_scale : 0.0f) + h16_to_f32(r16[j], g.f16);
+          }
+          o[i] = uint32_t(f32_to_h16(y[0], g.f16)) | (uint32_t(f32_to_h16(y[1], g.f16)) << 16);
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j)  // in place (same swizzled 16-byte slots as the residual)
+          *reinterpret_cast<uint4*>(rowp + (((hh * 4 + j) ^ (lane & 7)) << 4)) =
+              make_uint4(o[4 * j], o[4 * j + 1], o[4 * j + 2], o[4 * j + 3]);
+      }
+      if (cur.cc == cur.chunks - 1) {  // this unit's accumulator is read: release it before the stores drain
+        tc_fence_before();
+        asm volatile("bar.sync 1, %0;" ::"n"(kAgEpiWarps * 32) : "memory");
+        if (e == 0 && lane == 0) mbar_arrive_cl(tempty_l + uint32_t(acc * 8));
+        acc ^= 1;
+        if (acc == 0) aph ^= 1;
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      asm volatile("bar.sync %0, 128;" ::"r"(2 + h) : "memory");  // the half's 128 rows are written
+      if (lead) {
+        if (!(g.diag & 1))
+          for (int dd = 0; dd < g.dst; ++dd)  // the AllGather push: the finished chunk into every rank's out
+            tma_store_2d_hint(&maps.out[dd], hstg + b * 16384, col0, row0_of(cur), stream);
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+      }
+      cur = nxt;
+      ++n;
     }
     if (lane == 0) {
       asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
@@ -1233,7 +1286,7 @@ __global__ void __launch_bounds__(kAgThreads, 1) mp_ag_gemm_kernel(const __grid_
 
 template <int PER>
 constexpr int ag_smem() {
-  return kAgStages * (kPairABytes + ((PER < 256 ? PER : 256) / 2) * 128) + kAgEpiWarps * 2 * 4096 + 1024 + 256;
+  return kAgStages * (kPairABytes + ((PER < 256 ? PER : 256) / 2) * 128) + 2 * kAgEpiBufs * 16384 + 1024 + 512;
 }
 
 
@@ -1483,7 +1536,12 @@ int launch_ag_gemm(coconet_ctx* c, int group, const void* a, const void* w, cons
     char* heap = c->heap[grp.first + q];  // VIRTUAL: this device; DISTRIBUTED: the peer mapping
     rc = make_map(&maps.a[q], heap + ao, in_elem, uint64_t(k_local), uint64_t(rows), BK, BM);
     if (!rc) rc = make_map(&maps.b[q], heap + wo, in_elem, uint64_t(cols), uint64_t(k_local), 64, BK);
-    if (!rc) rc = make_map(&maps.out[q], heap + oo, in_elem, uint64_t(cols), uint64_t(rows), 64, 32);
+    if (!rc) rc = make_map(&maps.out[q], heap + oo, in_elem, uint64_t(cols), uint64_t(rows), 64, 128);
+    if (rc) return rc;
+  }
+  for (int i = 0; i < (c->mode == COCONET_MODE_VIRTUAL ? W : 1); ++i) {
+    char* heap = c->heap[grp.first + (c->mode == COCONET_MODE_VIRTUAL ? i : c->rank - grp.first)];
+    rc = make_map(&maps.res[i], heap + ro, in_elem, uint64_t(cols), uint64_t(rows), 64, 128);
     if (rc) return rc;
   }
   // owners computed here: every column block (VIRTUAL) or this rank's (DISTRIBUTED)

@@ -270,7 +270,9 @@ def _mp_pp_inputs(world, rows, H, r):
 
 
 def _run_mp(ctx, ranks, world, rows, H, fused):
-    """MatMul + fused RS-bias-dropout-residual-AG on `ctx` for `ranks`."""
+    """MatMul + fused RS-bias-dropout-residual-AG on `ctx` for `ranks`:
+    fused=False the two kernels, True the tile-flag one-kernel overlap,
+    "auto" the AUTO schedule (the all-gather -> GEMM kernel)."""
     from paper_2105_05720_b200 import _lib
     from paper_2105_05720_b200.collectives import BdrHParams, fused_rs_bdr_ag, matmul, mm_overlap_fused_ar
     k = H // world
@@ -287,7 +289,10 @@ def _run_mp(ctx, ranks, world, rows, H, fused):
     if ctx.mode == "distributed":
         dist.barrier()
     hp = BdrHParams(0.1, 1, 11617925594314093840, _lib.MATH_FAST)
-    if fused:  # force the one-kernel overlap (AUTO runs the pair back to back)
+    if fused == "auto":
+        os.environ.pop("COCONET_MP_OVERLAP", None)
+        mm_overlap_fused_ar(ctx, xb, wb, bb, rb, part, out, hp)
+    elif fused:  # force the tile-flag one-kernel overlap
         os.environ["COCONET_MP_OVERLAP"] = "fused"
         try:
             mm_overlap_fused_ar(ctx, xb, wb, bb, rb, part, out, hp)
@@ -316,6 +321,7 @@ def _worker_mp_pp(rank, world, port, q):
         dctx = Context(world, mode="distributed", rank=rank, device=0, heap_bytes=256 << 20, timeout_ms=60000)
         got_seq = _run_mp(dctx, [rank], world, rows, H, fused=False)[rank]
         got_ov = _run_mp(dctx, [rank], world, rows, H, fused=True)[rank]
+        got_ag = _run_mp(dctx, [rank], world, rows, H, fused="auto")[rank]
         # PP: stages of world/2 ranks
         S = world // 2
         N = 4096 * S
@@ -338,6 +344,7 @@ def _worker_mp_pp(rank, world, port, q):
         vctx = Context(world, mode="virtual", device=0, heap_bytes=256 << 20)
         want_seq = _run_mp(vctx, list(range(world)), world, rows, H, fused=False)[rank]
         want_ov = _run_mp(vctx, list(range(world)), world, rows, H, fused=True)[rank]
+        want_ag = _run_mp(vctx, list(range(world)), world, rows, H, fused="auto")[rank]
         vg0, vg1 = vctx.group(0, S), vctx.group(S, S)
         vx, vb, vr, vo = (vctx.alloc([N]) for _ in range(4))
         gs = torch.Generator().manual_seed(60)
@@ -352,7 +359,8 @@ def _worker_mp_pp(rank, world, port, q):
         vctx.check()
         want_pp = vctx.view(vo, rank).cpu().clone()
         vctx.close()
-        q.put((rank, torch.equal(got_seq, want_seq), torch.equal(got_ov, want_ov), torch.equal(got_pp, want_pp), None))
+        q.put((rank, torch.equal(got_seq, want_seq), torch.equal(got_ov, want_ov) and torch.equal(got_ag, want_ag),
+               torch.equal(got_pp, want_pp), None))
     except Exception as e:  # report, don't hang the parent
         q.put((rank, False, False, False, repr(e)))
     finally:
@@ -373,7 +381,7 @@ def test_distributed_mp_and_pp_match_virtual(world):
     for rank, ok_seq, ok_ov, ok_pp, err in res:
         assert err is None, err
         assert ok_seq, f"rank {rank}: MatMul + fused RS-BDR-AG differs from VIRTUAL mode"
-        assert ok_ov, f"rank {rank}: overlapped MatMul+AR differs from VIRTUAL mode"
+        assert ok_ov, f"rank {rank}: overlapped MatMul+AR (tile flags or all-gather -> GEMM) differs from VIRTUAL mode"
         assert ok_pp, f"rank {rank}: PP RS->send->AG differs from VIRTUAL mode"
 
 
