@@ -337,14 +337,21 @@ int coconet_matmul(coconet_ctx_t ctx, int group, const void* a, const void* b, v
                    void* stream);
 
 /* OverlapGroup{MatMul, FusedAllReduce(bias+dropout+residual)} (mp_overlap.json,
- * runtime.hpp:517-522). One-kernel schedule: the GEMM publishes a flag per
- * output tile, row tile outermost (every rank publishes row tile i before
- * row tile i+1; the reference's rank-rotated chunk_order, runtime.hpp:46-50,
- * is a cost-model order only), and comm warps start the RS->epilogue->AG of
- * a (row tile, column block) unit as soon as every rank published its tiles.
- * AUTO runs the GEMM then coconet_fused_rs_bdr_ag (bitwise the same result)
- * until the one-kernel schedule is measured faster over NVLink;
- * COCONET_MP_OVERLAP=fused|sequential forces either. */
+ * runtime.hpp:517-522). Three schedules:
+ *  - AUTO (aggemm): ONE all-gather -> GEMM kernel when cols/W is 128, 256 or
+ *    384, rows % 256 == 0 and k_local % 64 == 0. The owner of column block c
+ *    streams every rank's A_r and B_r[:, c] through one K loop (TMA from the
+ *    peers' memory), accumulates in fp32 TMEM, applies bias + dropout (masks
+ *    bit-exact) + residual and pushes the finished tile into every rank's
+ *    `out`. The partial products are never formed, so `partial` is not
+ *    written; results are within 1e-2 of the two-kernel schedule (fp32 sum
+ *    over the whole K instead of 16-bit partials folded in ring order).
+ *  - sequential: coconet_matmul into `partial`, then coconet_fused_rs_bdr_ag.
+ *  - fused: one cooperative kernel, the GEMM publishing a flag per output
+ *    tile (row tile outermost) and comm warps running RS->epilogue->AG per
+ *    (row tile, column block) unit; bitwise equal to sequential.
+ * COCONET_MP_OVERLAP=aggemm|sequential|fused forces one; other shapes run
+ * sequential. */
 int coconet_mm_overlap_fused_ar(coconet_ctx_t ctx, int group, const void* a, const void* w,
                                 const void* b, const void* r, void* partial, void* out,
                                 int in_elem, int64_t rows, int64_t cols, int64_t k_local,
