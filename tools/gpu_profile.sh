@@ -15,3 +15,5 @@ timeout 900 ncu --set full --clock-control none --import-source on -k "regex:gem
    -o gpurun_out/prof_gemm -f python tools/pattern_probe.py --only c3 --gemm-only > gpurun_out/ncu_gemm.log 2>&1; echo "ncu_gemm=$?" >> $S
 timeout 900 ncu --set full --clock-control none --import-source on -k "regex:rs_send_ag" -s 8 -c 1 \
    -o gpurun_out/prof_pp -f python tools/pattern_probe.py --only c4 > gpurun_out/ncu_pp.log 2>&1; echo "ncu_pp=$?" >> $S
+timeout 900 ncu --set full --clock-control none --import-source on -k "regex:mp_ag_gemm" -s 3 -c 1 \
+   -o gpurun_out/prof_ag -f python tools/pattern_probe.py --only c3 > gpurun_out/ncu_ag.log 2>&1; echo "ncu_ag=$?" >> $S
