@@ -1,8 +1,10 @@
 """Small instances of every kernel family for compute-sanitizer (memcheck,
-racecheck, synccheck): LAMB (GRID, TMA, STREAMED; W = 1..4), Adam (LDG, TMA
-at W = 1..3),
-tensor-list AllReduce, Reduce/Broadcast, RS/AG, the MP epilogue, the
-overlapped tcgen05 GEMM + all-reduce, the plain GEMM, and the PP send.
+racecheck, synccheck): LAMB (GRID, TMA, STREAMED; W = 1..4; ONCHIP at W = 1,
+also with a hold of 1 so windows, spills and the TMEM/shared-memory slot ring
+all run), Adam (LDG, TMA at W = 1..3), tensor-list AllReduce,
+Reduce/Broadcast, RS/AG, the MP epilogue, the tile-flag overlapped tcgen05
+GEMM + all-reduce, the all-gather -> GEMM MP kernel (AUTO), the plain GEMM
+(1-SM and the 2-SM pair kernel), and the PP send.
 Usage: compute-sanitizer --tool TOOL python tools/sanitize_cases.py"""
 import os
 import sys
@@ -33,9 +35,18 @@ def dp(W, cap):
             ctx.view(p[i], r).uniform_(0.1, 0.9)
         ctx.view(m, r).zero_()
         ctx.view(v, r).fill_(1e-3)
-    scheds = [_lib.LAMB_GRID, _lib.LAMB_STREAMED, _lib.LAMB_TMA]
+    scheds = [_lib.LAMB_GRID, _lib.LAMB_STREAMED, _lib.LAMB_TMA] + ([_lib.LAMB_ONCHIP] if W == 1 else [])
     for sched in scheds:
         fused_rs_lamb_ag(ctx, tl, g, p, m, v, LambHParams(1e-3, 0.9, 0.999, 1.0, sched=sched, lag_elems=3000))
+    if W == 1:  # ONCHIP with one held item per CTA: several windows, spilled items, slot-ring wrap
+        os.environ["COCONET_LAMB_OC_HOLD"] = "1"
+        os.environ["COCONET_LAMB_OC_STAGES"] = "2"
+        try:
+            tl2 = TensorList(ctx, counts, bucket_cap=cap)
+            fused_rs_lamb_ag(ctx, tl2, g, p, m, v, LambHParams(1e-3, 0.9, 0.999, 1.0, sched=_lib.LAMB_ONCHIP))
+        finally:
+            os.environ.pop("COCONET_LAMB_OC_HOLD")
+            os.environ.pop("COCONET_LAMB_OC_STAGES")
     for math in (_lib.MATH_EXACT, _lib.MATH_FAST):
         fused_rs_adam_ag(ctx, tl, g, p, m, v, AdamHParams(1e-3, 0.9, 0.999, 1.0, 1e-8, False, math, _lib.ALGO_TWO_SHOT))
     out = [ctx.alloc([n], torch.float16) for n in [3000, 77, 5000, 1, 4096]]
@@ -76,6 +87,7 @@ def mp_pp(W):
     os.environ["COCONET_MP_OVERLAP"] = "fused"
     mm_overlap_fused_ar(ctx, x, w, bb, rr, part, out, hp)
     os.environ.pop("COCONET_MP_OVERLAP")
+    mm_overlap_fused_ar(ctx, x, w, bb, rr, part, out, hp)  # AUTO: all-gather -> GEMM at W >= 2
     if W >= 2:
         S = W // 2
         g0, g1 = ctx.group(0, S), ctx.group(S, S)
