@@ -709,14 +709,6 @@ __device__ __forceinline__ void tma_load_2d_pair(void* dst, const CUtensorMap* m
       "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(cl_bar), "l"(policy)
       : "memory");
 }
-__device__ __forceinline__ void tma_load_2d_hint(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar,
-                                                 uint64_t policy) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, {%2, "
-      "%3}], [%4], %5;" ::"r"(smem_u32(dst)),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar)), "l"(policy)
-      : "memory");
-}
 __device__ __forceinline__ void tma_store_2d_hint(const CUtensorMap* map, const void* src, int c0, int c1,
                                                   uint64_t policy) {
   asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group.L2::cache_hint [%0, {%1, %2}], [%3], %4;" ::"l"(
@@ -988,22 +980,21 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_pair_kernel(const __grid
 // finished tile into every rank's `out` (the AllGather push). The same NVLink
 // bytes as the RS (every rank's A slice instead of every rank's partial
 // block), no partial write-back, no second kernel. FAST math: the sum is
-// accumulated in fp32 over the whole K (the reference rounds every partial
-// product to fp32 and folds them in ring order), masks bit-exact (global flat
-// index as the dropout counter, state.hpp:178-181).
-// Shapes: per = cols / W in {128, 256, 384} as two pair MMAs (N0 = min(per,
-// 256), N1 = per - N0), rows % 256 == 0, k_local % 64 == 0. 384 threads:
+// accumulated in fp32 over the whole K and rounded once to 16 bits in the
+// epilogue (the two-kernel schedule rounds every rank's partial product to 16
+// bits and folds them in fp32 ring order), masks bit-exact (global flat index
+// as the dropout counter, state.hpp:178-181).
+// Shapes: per = cols / W in {128, 256, 384} (two pair MMAs per k-step at 384:
+// N = 256 and N = 128), rows % 256 == 0, k_local % 64 == 0. 512 threads:
 // warp 0 producer, warp 1 MMA issuer (leader), warp 2 TMEM allocator, warps
-// 4-11 epilogue (two per TMEM lane quarter, each half of the columns).
-constexpr int kAgThreads = 384;
-constexpr int kAgStages = 4;
-constexpr int kAgEpiBufs = 3;  // per epilogue warp: residual in, result out, in place
-constexpr int kAgEpiWarps = 8;
+// 2-15 epilogue (4-11 also drain TMEM). On one GPU the 8 pushes of every
+// tile (403 MB at C3) bound it: profiles/r02_mp_ag_gemm.json.
+constexpr int kAgStages1 = 3;
+constexpr int kAg1Threads = 512;  // warp 0 producer, 1 MMA, 2-15 epilogue (4-11 also drain TMEM)
 struct AgMaps {
   CUtensorMap a[kMaxRanks];    // A_r: [rows, k_local], boxes 64 k x 128 rows
   CUtensorMap b[kMaxRanks];    // B_r: [k_local, cols], boxes 64 n x 64 k (MN-major)
   CUtensorMap out[kMaxRanks];  // out of every rank: boxes 64 cols x 128 rows
-  CUtensorMap res[kMaxRanks];  // r (replicated) of each owner computed here: boxes 64 cols x 128 rows
 };
 struct AgArgs {
   RankSet rs;  // DISTRIBUTED: entry / exit barrier with the peers whose A, B we read and whose out we write
@@ -1032,37 +1023,35 @@ __device__ __forceinline__ uint16_t f32_to_h16(float x, int f16) {
 }
 
 template <int PER>
-__global__ void __launch_bounds__(kAgThreads, 1) mp_ag_gemm_kernel(const __grid_constant__ AgMaps maps, AgArgs g,
+__global__ void __launch_bounds__(kAg1Threads, 1) mp_ag_gemm_kernel(const __grid_constant__ AgMaps maps, AgArgs g,
                                                                    uint32_t in_fmt) {
-  // A unit is (256-row block, owner column block, part): a column block wider
-  // than 256 (384 at C3) is two parts (256 + 128 columns), each its own K loop
-  // into one of two TMEM accumulators (256 columns each), so the epilogue of
-  // one unit (bias + dropout + residual + the pushes) runs under the MMAs of
-  // the next. A streams once per part.
-  constexpr int kW0 = PER < 256 ? PER : 256, kW1 = PER - kW0, kParts = kW1 > 0 ? 2 : 1;
+  // A unit is (256-row block, owner column block): ONE K loop of W * k_local
+  // into a PER-column TMEM accumulator (two MMAs per k-step at PER = 384:
+  // N = 256 and N = 128). The epilogue first drains the accumulator into a
+  // shared-memory unit buffer (16-bit, one rounding of the fp32 sum) and
+  // releases TMEM at once, so the next unit's MMAs overlap the bias +
+  // dropout + residual pass over that buffer and its pushes.
+  constexpr int kW0 = PER < 256 ? PER : 256, kW1 = PER - kW0;
+  constexpr int kStage = kPairABytes + (PER / 2) * 128;  // A 16 KB + this CTA's PER/2 B columns
+  constexpr int kChunks = PER / 64;                      // 64-column x 128-row chunks of the unit buffer
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  constexpr int kStage = kPairABytes + (kW0 / 2) * 128;  // A 16 KB + B half of the wider part
   uint8_t* ring = smem;
-  uint8_t* epi = ring + kAgStages * kStage;
-  uint64_t* full = reinterpret_cast<uint64_t*>(epi + 2 * kAgEpiBufs * 16384);
-  uint64_t* empty = full + kAgStages;
-  uint64_t* tfull = empty + kAgStages;  // [2]
-  uint64_t* tempty = tfull + 2;         // [2] (leader: both CTAs' epilogues)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint8_t* ubuf = ring + kAgStages1 * kStage;  // 1024-aligned: kStage is a multiple of 1024
+  uint64_t* full = reinterpret_cast<uint64_t*>(ubuf + kChunks * 16384);
+  uint64_t* empty = full + kAgStages1;
+  uint64_t* tfull = empty + kAgStages1;
+  uint64_t* tempty = tfull + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 1);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t crank = cluster_ctarank();
   if (warp == 0 && lane == 0) {
-    for (int s = 0; s < kAgStages; ++s) {
+    for (int s = 0; s < kAgStages1; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
-    for (int a = 0; a < 2; ++a) {
-      mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], 2);
-    }
-    uint64_t* rb = reinterpret_cast<uint64_t*>(tmem_slot + 2);  // the epilogue warps' residual loads
-    for (int i = 0; i < 2 * kAgEpiBufs; ++i) mbar_init(&rb[i], 1);
+    mbar_init(tfull, 1);
+    mbar_init(tempty, 2);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   }
@@ -1079,17 +1068,11 @@ __global__ void __launch_bounds__(kAgThreads, 1) mp_ag_gemm_kernel(const __grid_
   const uint32_t tmem = *tmem_slot;
   edge_barrier(g.rs, 0);  // DISTRIBUTED: every peer's A, B are ready (VIRTUAL: stream order)
   const int mbs = g.rows / 256;
-  const int units = g.owners * mbs * kParts;
+  const int units = g.owners * mbs;
   const int P = int(gridDim.x >> 1), pr = int(blockIdx.x >> 1);
   const int kb_per = g.k_local / BK, kb_all = g.W * kb_per;
-  // unit u -> part u % kParts, then owner, then row block: the pairs running
-  // together read the same A row blocks (every owner and part needs them)
-  auto decode = [&](int u, int& mb, int& c, int& part) {
-    part = kParts > 1 ? (u & 1) : 0;
-    const int rest = kParts > 1 ? (u >> 1) : u;
-    mb = rest / g.owners;
-    c = g.owner0 + (rest - mb * g.owners);
-  };
+  // unit u -> owner u % owners, row block u / owners: the pairs running
+  // together read the same A row blocks (every owner needs them)
   if (warp == 0) {
     if (lane == 0) {  // ---- producer (both CTAs)
       const uint32_t full_l = mapa_leader(full);
@@ -1097,10 +1080,7 @@ __global__ void __launch_bounds__(kAgThreads, 1) mp_ag_gemm_kernel(const __grid_
       int stage = 0;
       uint32_t phase = 0;
       for (int u = pr; u < units; u += P) {
-        int mb, c, part;
-        decode(u, mb, c, part);
-        const int wp = part ? kW1 : kW0, col0 = c * PER + (part ? kW0 : 0) + int(crank) * (wp / 2);
-        const uint32_t bytes = uint32_t(kPairABytes + (wp / 2) * 128);
+        const int mb = u / g.owners, c = g.owner0 + (u - mb * g.owners);
         for (int kk = 0; kk < kb_all; ++kk) {
           const int r = kk / kb_per, kb = kk - r * kb_per;
           mbar_wait(&empty[stage], phase ^ 1);
@@ -1108,13 +1088,19 @@ __global__ void __launch_bounds__(kAgThreads, 1) mp_ag_gemm_kernel(const __grid_
           if (g.diag & 2) {
             if (crank == 0) mbar_arrive(&full[stage]);
           } else {
-            if (crank == 0) mbar_expect_tx(&full[stage], 2u * bytes);
+            if (crank == 0) mbar_expect_tx(&full[stage], uint32_t(2 * kStage));
             const uint32_t fb = full_l + uint32_t(stage * 8);
             tma_load_2d_pair(st, &maps.a[r], kb * BK, mb * 256 + int(crank) * BM, fb, keep);
-            for (int j = 0; j < wp / 128; ++j)  // this CTA's wp/2 columns of the part
-              tma_load_2d_pair(st + kPairABytes + j * kMnBlockBytes, &maps.b[r], col0 + j * 64, kb * BK, fb, keep);
+            uint8_t* sb = st + kPairABytes;
+            for (int j = 0; j < kW0 / 128; ++j)  // part 0: this CTA's kW0/2 columns
+              tma_load_2d_pair(sb + j * kMnBlockBytes, &maps.b[r], c * PER + int(crank) * (kW0 / 2) + j * 64, kb * BK,
+                               fb, keep);
+            sb += (kW0 / 128) * kMnBlockBytes;
+            for (int j = 0; j < kW1 / 128; ++j)  // part 1: this CTA's kW1/2 columns
+              tma_load_2d_pair(sb + j * kMnBlockBytes, &maps.b[r], c * PER + kW0 + int(crank) * (kW1 / 2) + j * 64,
+                               kb * BK, fb, keep);
           }
-          if (++stage == kAgStages) {
+          if (++stage == kAgStages1) {
             stage = 0;
             phase ^= 1;
           }
@@ -1124,152 +1110,138 @@ __global__ void __launch_bounds__(kAgThreads, 1) mp_ag_gemm_kernel(const __grid_
   } else if (warp == 1) {
     if (lane == 0 && crank == 0) {  // ---- MMA issuer (leader)
       const uint32_t id0 = make_idesc_pair_n(in_fmt, kW0), id1 = make_idesc_pair_n(in_fmt, kW1 > 0 ? kW1 : 128);
-      int stage = 0, acc = 0;
-      uint32_t phase = 0, aph = 0;
+      int stage = 0;
+      uint32_t phase = 0, tph = 0;
       for (int u = pr; u < units; u += P) {
-        int mb, c, part;
-        decode(u, mb, c, part);
-        mbar_wait(&tempty[acc], aph ^ 1);  // both epilogues drained this accumulator
+        mbar_wait(tempty, tph ^ 1);  // both CTAs drained the accumulator
         tc_fence_after();
-        const uint32_t d = tmem + uint32_t(acc * 256);
-        const uint32_t id = part ? id1 : id0;
         for (int kk = 0; kk < kb_all; ++kk) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
           uint8_t* st = ring + stage * kStage;
-          const uint64_t da = sw128_desc(st), db = sw128_mn_desc(st + kPairABytes);
+          const uint64_t da = sw128_desc(st);
+          const uint64_t d0 = sw128_mn_desc(st + kPairABytes);
+          const uint64_t d1 = sw128_mn_desc(st + kPairABytes + (kW0 / 128) * kMnBlockBytes);
 #pragma unroll
-          for (int k = 0; k < BK / 16; ++k)
-            mma_f16_pair(d, da + 2 * k, db + uint64_t(k) * ((16 * 128) >> 4), id, (kk | k) != 0);
+          for (int k = 0; k < BK / 16; ++k) {
+            mma_f16_pair(tmem, da + 2 * k, d0 + uint64_t(k) * ((16 * 128) >> 4), id0, (kk | k) != 0);
+            if constexpr (kW1 > 0)
+              mma_f16_pair(tmem + uint32_t(kW0), da + 2 * k, d1 + uint64_t(k) * ((16 * 128) >> 4), id1,
+                           (kk | k) != 0);
+          }
           mma_commit_pair(&empty[stage]);
-          if (++stage == kAgStages) {
+          if (++stage == kAgStages1) {
             stage = 0;
             phase ^= 1;
           }
         }
-        mma_commit_pair(&tfull[acc]);
-        acc ^= 1;
-        if (acc == 0) aph ^= 1;
+        mma_commit_pair(tfull);
+        tph ^= 1;
       }
     }
-  } else if (warp >= 4) {  // ---- epilogue (both CTAs): 8 warps, TMEM lane quarter q, column half h
-    // The 4 warps of a column half h (one per TMEM lane quarter) work on
-    // 128-row x 64-column chunks together: the residual chunk comes in by one
-    // TMA load (one chunk ahead) into a 16 KB staging buffer, every thread
-    // reads its row, adds bias + dropout(accumulator) and writes the result
-    // back in place, and one thread pushes the buffer into every rank's `out`
-    // (8 x 16 KB bulk stores; 4 KB boxes per warp were store-issue bound).
-    // Three buffers per half: load n+1, compute n, stores of n-1 draining.
-    const int e = warp - 4, q = warp & 3, h = e >> 2;
-    const bool lead = q == 0 && lane == 0;  // issues this half's loads and stores
-    uint8_t* hstg = epi + h * kAgEpiBufs * 16384;
-    uint64_t* rbar = reinterpret_cast<uint64_t*>(tmem_slot + 2) + h * kAgEpiBufs;
+  } else {  // ---- epilogue (both CTAs): warps 2-15
+    // Warps 4-11 drain the accumulator (TMEM lane quarter q = warp % 4,
+    // column half h) into the shared-memory unit buffer as 16-bit values and
+    // release TMEM; then all 14 warps run bias + dropout + residual over the
+    // buffer, thread t taking 32-column groups (t % 12 of a 384-wide row), so
+    // the residual loads are coalesced; one thread pushes the unit to every
+    // rank's `out`.
+    constexpr int kEpiThreads = kAg1Threads - 64;  // warps 2..15
+    constexpr int kGroups = PER / 32;              // 32-column groups per row
+    const int et = int(threadIdx.x) - 64;
+    const bool pusher = et == 0;
+    const bool drainer = warp >= 4 && warp < 12;
+    const int q = warp & 3, h = (warp - 4) >> 2;
     const uint32_t tempty_l = mapa_leader(tempty);
     const uint64_t stream = createpolicy_evict_first();
-    struct It {
-      int u, cc, mb, c, part, chunks;
-    };
-    auto first = [&](int u, It& it) {
-      it.u = u;
-      it.cc = 0;
-      if (u < units) {
-        decode(u, it.mb, it.c, it.part);
-        it.chunks = (it.part ? kW1 : kW0) / 128;
-      }
-    };
-    auto advance = [&](It& it) {
-      if (++it.cc == it.chunks) first(it.u + P, it);
-    };
-    auto col_of = [&](const It& it) {
-      const int wp = it.part ? kW1 : kW0;
-      return it.c * PER + (it.part ? kW0 : 0) + h * (wp / 2) + it.cc * 64;
-    };
-    auto row0_of = [&](const It& it) { return it.mb * 256 + int(crank) * BM; };
-    auto load_res = [&](const It& it, int b) {  // lead thread
-      mbar_expect_tx(&rbar[b], 16384u);
-      tma_load_2d_hint(hstg + b * 16384, &maps.res[it.c - g.owner0], col_of(it), row0_of(it), &rbar[b], stream);
-    };
-    It cur, nxt;
-    first(pr, cur);
-    nxt = cur;
-    int n = 0;  // chunks processed by this half
-    if (lead && cur.u < units && !(g.diag & 1)) load_res(cur, 0);
-    int acc = 0;
-    uint32_t aph = 0;
-    while (cur.u < units) {
-      const int b = n % kAgEpiBufs;
-      advance(nxt);
-      // prefetch the next chunk's residual: its buffer was last pushed by
-      // chunk n-2 (all but the last committed group have been read)
-      if (lead && nxt.u < units && !(g.diag & 1)) {
-        asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
-        load_res(nxt, (n + 1) % kAgEpiBufs);
-      }
-      if (cur.cc == 0) {
-        mbar_wait(&tfull[acc], aph);
+    constexpr int kHalf = PER / 2;
+    uint32_t tph = 0;
+    for (int u = pr; u < units; u += P) {
+      const int mb = u / g.owners, c = g.owner0 + (u - mb * g.owners);
+      const int oi = c - g.owner0;
+      const int row0 = mb * 256 + int(crank) * BM;
+      // the unit buffer is free once the previous unit's pushes have read it
+      if (pusher) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+      asm volatile("bar.sync 1, %0;" ::"n"(kEpiThreads) : "memory");
+      if (drainer) {
+        mbar_wait(tfull, tph);
         tc_fence_after();
-      }
-      const int wp = cur.part ? kW1 : kW0;
-      const uint32_t tbase = tmem + (uint32_t(q * 32) << 16) + uint32_t(acc * 256 + h * (wp / 2));
-      const int col0 = col_of(cur), row = row0_of(cur) + q * 32 + lane;
-      const int oi = cur.c - g.owner0;
-      if (!(g.diag & 1)) mbar_wait(&rbar[b], uint32_t(n / kAgEpiBufs) & 1u);
-      uint8_t* rowp = hstg + b * 16384 + (q * 32 + lane) * 128;
-      const uint4* bp = reinterpret_cast<const uint4*>(g.bias[oi] + col0);
+        const int lrow = q * 32 + lane;
+        const uint32_t tbase = tmem + (uint32_t(q * 32) << 16) + uint32_t(h * kHalf);
+#pragma unroll 1
+        for (int s32 = 0; s32 < kHalf / 32; ++s32) {
+          uint32_t v[32];
+          tmem_ld32(tbase + uint32_t(s32 * 32), v);
+          const int col = h * kHalf + s32 * 32;  // column inside the unit
+          uint8_t* rowp = ubuf + (col / 64) * 16384 + lrow * 128;
 #pragma unroll
-      for (int hh = 0; hh < 2; ++hh) {  // 32 columns at a time
-        uint4 bb[4], rr[4];
+          for (int j = 0; j < 4; ++j) {
+            uint32_t w4[4];
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          bb[i] = __ldg(bp + hh * 4 + i);
-          rr[i] = *reinterpret_cast<const uint4*>(rowp + (((hh * 4 + i) ^ (lane & 7)) << 4));
-        }
-        uint32_t v[32];
-        tmem_ld32(tbase + uint32_t(cur.cc * 64 + hh * 32), v);
-        if (g.diag & 1) {
-          if (v[0] == 0x7fffffffu && v[31] == 0x7fffffffu) rowp[0] = 1;  // keep the loads live
-          continue;
-        }
-        const uint16_t* r16 = reinterpret_cast<const uint16_t*>(rr);
-        const uint16_t* b16 = reinterpret_cast<const uint16_t*>(bb);
-        uint32_t o[16];
-        const uint64_t gi0 = uint64_t(row) * uint64_t(g.cols) + uint64_t(col0 + hh * 32);
-#pragma unroll
-        for (int i = 0; i < 16; ++i) {
-          float y[2];
-#pragma unroll
-          for (int t = 0; t < 2; ++t) {
-            const int j = 2 * i + t;
-            const float x = __uint_as_float(v[j]) + h16_to_f32(b16[j], g.f16);
-            const bool kp = dropout_keep_bits(g.seed, g.key, gi0 + uint64_t(j), g.thresh);
-            y[t] = (kp ? x * g.frate_scale : 0.0f) + h16_to_f32(r16[j], g.f16);
+            for (int t = 0; t < 4; ++t)
+              w4[t] = uint32_t(__bfloat16_as_ushort(__float2bfloat16_rn(__uint_as_float(v[8 * j + 2 * t])))) |
+                      (uint32_t(__bfloat16_as_ushort(__float2bfloat16_rn(__uint_as_float(v[8 * j + 2 * t + 1]))))
+                       << 16);
+            *reinterpret_cast<uint4*>(rowp + (((((col % 64) / 8) + j) ^ (lane & 7)) << 4)) =
+                make_uint4(w4[0], w4[1], w4[2], w4[3]);
           }
-          o[i] = uint32_t(f32_to_h16(y[0], g.f16)) | (uint32_t(f32_to_h16(y[1], g.f16)) << 16);
         }
-#pragma unroll
-        for (int j = 0; j < 4; ++j)  // in place (same swizzled 16-byte slots as the residual)
-          *reinterpret_cast<uint4*>(rowp + (((hh * 4 + j) ^ (lane & 7)) << 4)) =
-              make_uint4(o[4 * j], o[4 * j + 1], o[4 * j + 2], o[4 * j + 3]);
-      }
-      if (cur.cc == cur.chunks - 1) {  // this unit's accumulator is read: release it before the stores drain
         tc_fence_before();
-        asm volatile("bar.sync 1, %0;" ::"n"(kAgEpiWarps * 32) : "memory");
-        if (e == 0 && lane == 0) mbar_arrive_cl(tempty_l + uint32_t(acc * 8));
-        acc ^= 1;
-        if (acc == 0) aph ^= 1;
       }
+      asm volatile("bar.sync 1, %0;" ::"n"(kEpiThreads) : "memory");
+      if (warp == 4 && lane == 0) mbar_arrive_cl(tempty_l);  // both CTAs' arrivals release the accumulator
+      // bias + dropout + residual over the buffer, in place
+      if (!(g.diag & 1)) {
+#pragma unroll 1
+        for (int it = et; it < BM * kGroups; it += kEpiThreads) {
+          const int lrow = it / kGroups, grp = it - lrow * kGroups;
+          const int col = grp * 32, gcol = c * PER + col, row = row0 + lrow;
+          uint8_t* rowp = ubuf + (col / 64) * 16384 + lrow * 128;
+          const uint4* rp = reinterpret_cast<const uint4*>(g.res[oi] + int64_t(row) * g.cols + gcol);
+          const uint4* bp = reinterpret_cast<const uint4*>(g.bias[oi] + gcol);
+          uint4 rr[4], bb[4], aa[4];
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            rr[j] = __ldg(rp + j);
+            bb[j] = __ldg(bp + j);
+            aa[j] = *reinterpret_cast<const uint4*>(rowp + (((((col % 64) / 8) + j) ^ (lrow & 7)) << 4));
+          }
+          const uint16_t* r16 = reinterpret_cast<const uint16_t*>(rr);
+          const uint16_t* b16 = reinterpret_cast<const uint16_t*>(bb);
+          const uint16_t* a16 = reinterpret_cast<const uint16_t*>(aa);
+          uint32_t o[16];
+          const uint64_t gi0 = uint64_t(row) * uint64_t(g.cols) + uint64_t(gcol);
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            float y[2];
+#pragma unroll
+            for (int t = 0; t < 2; ++t) {
+              const int j = 2 * i + t;
+              const float x = __bfloat162float(__ushort_as_bfloat16(a16[j])) + h16_to_f32(b16[j], g.f16);
+              const bool kp = dropout_keep_bits(g.seed, g.key, gi0 + uint64_t(j), g.thresh);
+              y[t] = (kp ? x * g.frate_scale : 0.0f) + h16_to_f32(r16[j], g.f16);
+            }
+            o[i] = uint32_t(f32_to_h16(y[0], g.f16)) | (uint32_t(f32_to_h16(y[1], g.f16)) << 16);
+          }
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+            *reinterpret_cast<uint4*>(rowp + (((((col % 64) / 8) + j) ^ (lrow & 7)) << 4)) =
+                make_uint4(o[4 * j], o[4 * j + 1], o[4 * j + 2], o[4 * j + 3]);
+        }
+      }
+      // the AllGather push: the finished unit into every rank's out
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      asm volatile("bar.sync %0, 128;" ::"r"(2 + h) : "memory");  // the half's 128 rows are written
-      if (lead) {
+      asm volatile("bar.sync 1, %0;" ::"n"(kEpiThreads) : "memory");
+      if (pusher) {
         if (!(g.diag & 1))
-          for (int dd = 0; dd < g.dst; ++dd)  // the AllGather push: the finished chunk into every rank's out
-            tma_store_2d_hint(&maps.out[dd], hstg + b * 16384, col0, row0_of(cur), stream);
+          for (int dd = 0; dd < ((g.diag & 8) ? 1 : g.dst); ++dd)  // diag 8 (profiling only): one destination
+            for (int j = 0; j < kChunks; ++j)
+              tma_store_2d_hint(&maps.out[dd], ubuf + j * 16384, c * PER + j * 64, row0, stream);
         asm volatile("cp.async.bulk.commit_group;" ::: "memory");
       }
-      cur = nxt;
-      ++n;
+      tph ^= 1;
     }
-    if (lane == 0) {
+    if (pusher) {
       asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
       asm volatile("fence.proxy.async.global;" ::: "memory");  // the pushes before the exit barrier's release
     }
@@ -1286,8 +1258,9 @@ __global__ void __launch_bounds__(kAgThreads, 1) mp_ag_gemm_kernel(const __grid_
 
 template <int PER>
 constexpr int ag_smem() {
-  return kAgStages * (kPairABytes + ((PER < 256 ? PER : 256) / 2) * 128) + 2 * kAgEpiBufs * 16384 + 1024 + 512;
+  return kAgStages1 * (kPairABytes + (PER / 2) * 128) + (PER / 64) * 16384 + 1024 + 512;
 }
+
 
 
 // EXACT: C = A x B with fp64 accumulation in k order (eval_matmul).
@@ -1539,11 +1512,6 @@ int launch_ag_gemm(coconet_ctx* c, int group, const void* a, const void* w, cons
     if (!rc) rc = make_map(&maps.out[q], heap + oo, in_elem, uint64_t(cols), uint64_t(rows), 64, 128);
     if (rc) return rc;
   }
-  for (int i = 0; i < (c->mode == COCONET_MODE_VIRTUAL ? W : 1); ++i) {
-    char* heap = c->heap[grp.first + (c->mode == COCONET_MODE_VIRTUAL ? i : c->rank - grp.first)];
-    rc = make_map(&maps.res[i], heap + ro, in_elem, uint64_t(cols), uint64_t(rows), 64, 128);
-    if (rc) return rc;
-  }
   // owners computed here: every column block (VIRTUAL) or this rank's (DISTRIBUTED)
   g.owner0 = c->mode == COCONET_MODE_VIRTUAL ? 0 : c->rank - grp.first;
   g.owners = c->mode == COCONET_MODE_VIRTUAL ? W : 1;
@@ -1571,12 +1539,12 @@ int launch_ag_gemm(coconet_ctx* c, int group, const void* a, const void* w, cons
   const int smem = per == 384 ? ag_smem<384>() : per == 256 ? ag_smem<256>() : ag_smem<128>();
   auto fn = per == 384 ? mp_ag_gemm_kernel<384> : per == 256 ? mp_ag_gemm_kernel<256> : mp_ag_gemm_kernel<128>;
   CN_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-  const int units = g.owners * int(rows / 256) * (per > 256 ? 2 : 1);
+  const int units = g.owners * int(rows / 256);
   cudaLaunchConfig_t cfg{};
   // DISTRIBUTED: the same grid on every rank (the edge barriers pair CTA b with CTA b)
   cfg.gridDim = dim3(unsigned(2 * (c->mode == COCONET_MODE_VIRTUAL ? std::min(units, c->sm_count / 2)
                                                                     : c->sm_count / 2)));
-  cfg.blockDim = dim3(kAgThreads);
+  cfg.blockDim = dim3(kAg1Threads);
   cfg.dynamicSmemBytes = size_t(smem);
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
