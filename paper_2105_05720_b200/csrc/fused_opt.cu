@@ -1400,7 +1400,7 @@ struct LambOC {
   double2* part;         // [n_tensors][G]
   uint32_t* cnt;         // [K] pass-1 arrivals per window, [K] CTAs out; zero between launches
   int K;
-  int hold, cap, head, tslots;
+  int hold, cap, head, head2, tslots;
   int slot_off;  // byte offset of the shared-memory u slots from the ring base
   int nosync;    // profiling only (COCONET_LAMB_OC_NOSYNC=1): skip the window waits, results invalid
 };
@@ -1418,31 +1418,38 @@ __device__ __forceinline__ int oc_count(int64_t b, int64_t e, int c, int G) {
 // The per-window item order shared by the producer and the consumers:
 // head P1 items, then P2 and P1 alternating. next() = 0 done, 1 P1 (j), 2 P2 (j).
 struct OcSeq {
-  int n1, n2, h, j1, j2;
-  bool p2_turn;
-  __device__ __forceinline__ void start(int n2_, int n1_, int head) {
+  int n1, n2, h, h2, j1, j2;
+  __device__ __forceinline__ void start(int n2_, int n1_, int head, int head2) {
     n1 = n1_;
     n2 = n2_;
     h = min(head, n1);
+    h2 = min(head2, n1 - h);
     j1 = j2 = 0;
-    p2_turn = true;
   }
+  // P1 item j1 (held) reuses the slot of P2 item j1 - h, so P2 runs at
+  // least j1 - h + 1 items ahead of it; after the head this alternates
   __device__ __forceinline__ int next(int& j) {
-    if (j1 < h) {
+    if (j1 < h + h2) {
       j = j1++;
       return 1;
     }
     if (j2 >= n2 && j1 >= n1) return 0;
-    if (j2 < n2 && (p2_turn || j1 >= n1)) {
+    if (j2 < n2 && (j1 >= n1 || j2 < j1 - h + 1)) {
       j = j2++;
-      p2_turn = false;
       return 2;
     }
     j = j1++;
-    p2_turn = true;
     return 1;
   }
 };
+
+// Item j of a CTA's n items of a window keeps its u on chip unless it is past
+// the hold or one of the head2 items after the head (run early as cover for
+// the previous window's norm wait, without a slot: they take the spilled path)
+__device__ __forceinline__ bool oc_held(int j, int n, int hold, int head, int head2) {
+  const int h = min(head, n), h2 = min(head2, n - h);
+  return j < hold && !(j >= h && j < h + h2);
+}
 
 // 32 items of one stream (P1 or P2) of this CTA, loaded by the producer warp
 // at once (lane l: item first + l*G) and handed out with shuffles.
@@ -1600,7 +1607,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) lamb_onchip_kernel(OptArgs a
       const int n1 = kk + 1 < K ? oc_count(w1b, w1e, cta, NG) : 0;
       const int64_t f2 = oc_first(w2b, cta, NG), f1 = oc_first(w1b, cta, NG);
       OcSeq seq;
-      seq.start(n2, n1, oc.head);
+      seq.start(n2, n1, oc.head, oc.head2);
       bool spill_ok = false;
       int j, kind;
       while ((kind = seq.next(j)) != 0) {
@@ -1611,7 +1618,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) lamb_onchip_kernel(OptArgs a
         }
         const OcDesc d = oc_get(p1 ? b1 : b2, j & 31);
         if (lane == 0) {
-          const bool held = j < oc.hold;
+          const bool held = oc_held(j, p1 ? n1 : n2, oc.hold, oc.head, oc.head2);
           if (!p1 && !held && !spill_ok) {  // m', v' of this window stored (generic proxy) by our consumers
             // window kk+2 is not issued yet, so its barrier is at most one phase ahead
             mbar_wait(&s_p1done[kk & 1], uint32_t(kk >> 1) & 1u);
@@ -1675,7 +1682,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) lamb_onchip_kernel(OptArgs a
       if (base1 >= oc.cap) base1 -= oc.cap;
       const int t2 = kk >= 0 ? oc.tfirst[kk] : 0;
       OcSeq seq;
-      seq.start(n2, n1, oc.head);
+      seq.start(n2, n1, oc.head, oc.head2);
       int cur_t = -1;  // P1 tensor whose thread partials are open
       float sp = 0.f, su = 0.f;
       // flush the open tensor's CTA partial: fixed-order sum of the NW warps
@@ -1745,7 +1752,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) lamb_onchip_kernel(OptArgs a
           if (cur_t >= 0) flush();
           cur_t = d.tensor;
         }
-        const bool held = j < oc.hold;
+        const bool held = oc_held(j, p1 ? n1 : n2, oc.hold, oc.head, oc.head2);
         int slot = (p1 ? base1 : base2) + j;
         if (slot >= oc.cap) slot -= oc.cap;
         const uint8_t* src = stage0 + size_t(st) * ST::BYTES;
@@ -2626,6 +2633,8 @@ int coconet_fused_rs_lamb_ag(coconet_ctx_t c, coconet_tlist_t tl, const void* co
     oc.head = std::max(1, std::min(oc.cap / 2, he ? atoi(he) : 1));
     oc.hold = oc.cap - oc.head;
     if (const char* ke = getenv("COCONET_LAMB_OC_HOLD")) oc.hold = std::max(1, std::min(oc.hold, atoi(ke)));
+    const char* h2e = getenv("COCONET_LAMB_OC_HEAD2");
+    oc.head2 = h2e ? std::max(0, std::min(8, atoi(h2e))) : 0;
     oc.slot_off = slot_off;
     const char* ns = getenv("COCONET_LAMB_OC_NOSYNC");
     oc.nosync = ns && ns[0] == '1';

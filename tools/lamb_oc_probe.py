@@ -27,6 +27,7 @@ def main():
     ap.add_argument("--stages", default="4")
     ap.add_argument("--slots", default="")
     ap.add_argument("--shapes", default="162", help="consumer warps x quads per thread: 162, 161, 82")
+    ap.add_argument("--head2s", default="")
     ap.add_argument("--out", default="")
     args = ap.parse_args()
     counts = bert_large_counts()
@@ -54,11 +55,13 @@ def main():
         for h in args.heads.split(","):
             for s in args.stages.split(","):
                 for x in (args.slots.split(",") if args.slots else [None]):
-                    configs.append((f"onchip_shape{w}_head{h}_stages{s}" + (f"_slots{x}" if x else ""),
-                                    _lib.LAMB_ONCHIP, h, s, x, w))
+                    for h2 in (args.head2s.split(",") if args.head2s else [None]):
+                        configs.append((f"onchip_shape{w}_head{h}_stages{s}" + (f"_slots{x}" if x else "")
+                                        + (f"_head2_{h2}" if h2 else ""), _lib.LAMB_ONCHIP, h, s, x, w, h2))
     for name, sched, head, stages, slots, *wr in configs:
         for k, val in (("COCONET_LAMB_OC_HEAD", head), ("COCONET_LAMB_OC_STAGES", stages),
-                       ("COCONET_LAMB_OC_SMEM_SLOTS", slots), ("COCONET_LAMB_OC_SHAPE", wr[0] if wr else None)):
+                       ("COCONET_LAMB_OC_SMEM_SLOTS", slots), ("COCONET_LAMB_OC_SHAPE", wr[0] if wr else None),
+                       ("COCONET_LAMB_OC_HEAD2", wr[1] if len(wr) > 1 else None)):
             if val is None:
                 os.environ.pop(k, None)
             else:
