@@ -71,10 +71,21 @@ template <typename T> struct Vec16 {
   static constexpr int V = 16 / int(sizeof(T));
   uint4 raw;
   __device__ __forceinline__ void load_cg(const T* p) { raw = __ldcg(reinterpret_cast<const uint4*>(p)); }
+  // streamed once: evict-first
+  __device__ __forceinline__ void load_cs(const T* p) { raw = __ldcs(reinterpret_cast<const uint4*>(p)); }
   __device__ __forceinline__ void load(const T* p) { raw = __ldg(reinterpret_cast<const uint4*>(p)); }
   __device__ __forceinline__ float get(int i) const { return to_f32(reinterpret_cast<const T*>(&raw)[i]); }
 };
 
+template <typename T>
+__device__ __forceinline__ void store16_cs(T* p, const float (&o)[16 / sizeof(T)]) {
+  constexpr int V = 16 / int(sizeof(T));
+  uint4 raw;
+  T* h = reinterpret_cast<T*>(&raw);
+#pragma unroll
+  for (int i = 0; i < V; ++i) h[i] = from_f32<T>(o[i]);
+  __stcs(reinterpret_cast<uint4*>(p), raw);
+}
 template <typename T>
 __device__ __forceinline__ void store16(T* p, const float (&o)[16 / sizeof(T)]) {
   constexpr int V = 16 / int(sizeof(T));
@@ -161,10 +172,10 @@ __global__ void __launch_bounds__(kThreads) rs_send_ag_kernel(BdrArgs a, BdrK k)
           int src = me + 1 + j;
           src -= src >= S ? S : 0;
           src -= src >= S ? S : 0;
-          x[j].load(reinterpret_cast<const T*>(s_base[src] + a.x_off) + gi);
+          x[j].load_cs(reinterpret_cast<const T*>(s_base[src] + a.x_off) + gi);
         }
-        bv.load(reinterpret_cast<const T*>(s_base[me] + a.b_off) + gi);
-        rv.load(reinterpret_cast<const T*>(s_base[me] + a.r_off) + gi);
+        bv.load_cs(reinterpret_cast<const T*>(s_base[me] + a.b_off) + gi);
+        rv.load_cs(reinterpret_cast<const T*>(s_base[me] + a.r_off) + gi);
         float o[VN];
 #pragma unroll
         for (int i = 0; i < VN; ++i) {
@@ -177,7 +188,7 @@ __global__ void __launch_bounds__(kThreads) rs_send_ag_kernel(BdrArgs a, BdrK k)
 #pragma unroll
         for (int j = 0; j < kS; ++j) {
           if (j >= U - S) break;
-          store16(reinterpret_cast<T*>(s_base[S + j] + a.out_off) + gi, o);
+          store16_cs(reinterpret_cast<T*>(s_base[S + j] + a.out_off) + gi, o);
         }
       }
     } else {
