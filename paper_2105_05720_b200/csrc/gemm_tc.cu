@@ -1500,7 +1500,7 @@ int launch_ag_gemm(coconet_ctx* c, int group, const void* a, const void* w, cons
   if (!rc) rc = heap_offset(c, out, &oo);
   if (rc) return rc;
   if ((ao | wo | bo | ro | oo) % 16) return COCONET_ERR_UNSUPPORTED;
-  static AgMaps maps;  // host staging of the kernel parameter
+  AgMaps maps;  // the kernel parameter (3 KB of tensor maps), copied at launch
   AgArgs g{};
   rc = make_rankset(c, group, &g.rs);
   if (rc) return rc;
