@@ -338,8 +338,9 @@ int coconet_matmul(coconet_ctx_t ctx, int group, const void* a, const void* b, v
 
 /* OverlapGroup{MatMul, FusedAllReduce(bias+dropout+residual)} (mp_overlap.json,
  * runtime.hpp:517-522). Three schedules:
- *  - AUTO (aggemm): ONE all-gather -> GEMM kernel when cols/W is 128, 256 or
- *    384, rows % 256 == 0 and k_local % 64 == 0. The owner of column block c
+ *  - AUTO (aggemm): ONE all-gather -> GEMM kernel when cols/W is a multiple
+ *    of 128 (run as 384-, 256- or 128-column sub-blocks), rows % 256 == 0 and
+ *    k_local % 64 == 0. The owner of column block c
  *    streams every rank's A_r and B_r[:, c] through one K loop (TMA from the
  *    peers' memory), accumulates in fp32 TMEM, applies bias + dropout (masks
  *    bit-exact) + residual and pushes the finished tile into every rank's

@@ -984,8 +984,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_pair_kernel(const __grid
 // epilogue (the two-kernel schedule rounds every rank's partial product to 16
 // bits and folds them in fp32 ring order), masks bit-exact (global flat index
 // as the dropout counter, state.hpp:178-181).
-// Shapes: per = cols / W in {128, 256, 384} (two pair MMAs per k-step at 384:
-// N = 256 and N = 128), rows % 256 == 0, k_local % 64 == 0. 512 threads:
+// Shapes: per = cols / W a multiple of 128, run as sub-blocks of PER = 384,
+// 256 or 128 columns (two pair MMAs per k-step at 384: N = 256 and N = 128),
+// rows % 256 == 0, k_local % 64 == 0. 512 threads:
 // warp 0 producer, warp 1 MMA issuer (leader), warp 2 TMEM allocator, warps
 // 2-15 epilogue (4-11 also drain TMEM). On one GPU the 8 pushes of every
 // tile (403 MB at C3) bound it: profiles/r02_mp_ag_gemm.json.
@@ -1068,11 +1069,19 @@ __global__ void __launch_bounds__(kAg1Threads, 1) mp_ag_gemm_kernel(const __grid
   const uint32_t tmem = *tmem_slot;
   edge_barrier(g.rs, 0);  // DISTRIBUTED: every peer's A, B are ready (VIRTUAL: stream order)
   const int mbs = g.rows / 256;
-  const int units = g.owners * mbs;
+  const int nsub = g.per / PER;  // PER-column sub-blocks of an owner's column block
+  const int units = g.owners * mbs * nsub;
   const int P = int(gridDim.x >> 1), pr = int(blockIdx.x >> 1);
   const int kb_per = g.k_local / BK, kb_all = g.W * kb_per;
-  // unit u -> owner u % owners, row block u / owners: the pairs running
-  // together read the same A row blocks (every owner needs them)
+  // unit u -> (row block, owner, sub-block), row-block-major: the pairs
+  // running together read the same A row blocks (every owner needs them)
+  auto decode = [&](int u, int& mb, int& c, int& cb) {
+    const int per_mb = g.owners * nsub;
+    mb = u / per_mb;
+    const int rem = u - mb * per_mb;
+    c = g.owner0 + rem / nsub;
+    cb = c * g.per + (rem - (rem / nsub) * nsub) * PER;  // first output column of the unit
+  };
   if (warp == 0) {
     if (lane == 0) {  // ---- producer (both CTAs)
       const uint32_t full_l = mapa_leader(full);
@@ -1080,7 +1089,8 @@ __global__ void __launch_bounds__(kAg1Threads, 1) mp_ag_gemm_kernel(const __grid
       int stage = 0;
       uint32_t phase = 0;
       for (int u = pr; u < units; u += P) {
-        const int mb = u / g.owners, c = g.owner0 + (u - mb * g.owners);
+        int mb, c, cb;
+        decode(u, mb, c, cb);
         for (int kk = 0; kk < kb_all; ++kk) {
           const int r = kk / kb_per, kb = kk - r * kb_per;
           mbar_wait(&empty[stage], phase ^ 1);
@@ -1093,11 +1103,11 @@ __global__ void __launch_bounds__(kAg1Threads, 1) mp_ag_gemm_kernel(const __grid
             tma_load_2d_pair(st, &maps.a[r], kb * BK, mb * 256 + int(crank) * BM, fb, keep);
             uint8_t* sb = st + kPairABytes;
             for (int j = 0; j < kW0 / 128; ++j)  // part 0: this CTA's kW0/2 columns
-              tma_load_2d_pair(sb + j * kMnBlockBytes, &maps.b[r], c * PER + int(crank) * (kW0 / 2) + j * 64, kb * BK,
+              tma_load_2d_pair(sb + j * kMnBlockBytes, &maps.b[r], cb + int(crank) * (kW0 / 2) + j * 64, kb * BK,
                                fb, keep);
             sb += (kW0 / 128) * kMnBlockBytes;
             for (int j = 0; j < kW1 / 128; ++j)  // part 1: this CTA's kW1/2 columns
-              tma_load_2d_pair(sb + j * kMnBlockBytes, &maps.b[r], c * PER + kW0 + int(crank) * (kW1 / 2) + j * 64,
+              tma_load_2d_pair(sb + j * kMnBlockBytes, &maps.b[r], cb + kW0 + int(crank) * (kW1 / 2) + j * 64,
                                kb * BK, fb, keep);
           }
           if (++stage == kAgStages1) {
@@ -1157,7 +1167,8 @@ __global__ void __launch_bounds__(kAg1Threads, 1) mp_ag_gemm_kernel(const __grid
     constexpr int kHalf = PER / 2;
     uint32_t tph = 0;
     for (int u = pr; u < units; u += P) {
-      const int mb = u / g.owners, c = g.owner0 + (u - mb * g.owners);
+      int mb, c, cb;
+      decode(u, mb, c, cb);
       const int oi = c - g.owner0;
       const int row0 = mb * 256 + int(crank) * BM;
       // the unit buffer is free once the previous unit's pushes have read it
@@ -1195,7 +1206,7 @@ __global__ void __launch_bounds__(kAg1Threads, 1) mp_ag_gemm_kernel(const __grid
 #pragma unroll 1
         for (int it = et; it < BM * kGroups; it += kEpiThreads) {
           const int lrow = it / kGroups, grp = it - lrow * kGroups;
-          const int col = grp * 32, gcol = c * PER + col, row = row0 + lrow;
+          const int col = grp * 32, gcol = cb + col, row = row0 + lrow;
           uint8_t* rowp = ubuf + (col / 64) * 16384 + lrow * 128;
           const uint4* rp = reinterpret_cast<const uint4*>(g.res[oi] + int64_t(row) * g.cols + gcol);
           const uint4* bp = reinterpret_cast<const uint4*>(g.bias[oi] + gcol);
@@ -1236,7 +1247,7 @@ __global__ void __launch_bounds__(kAg1Threads, 1) mp_ag_gemm_kernel(const __grid
         if (!(g.diag & 1))
           for (int dd = 0; dd < ((g.diag & 8) ? 1 : g.dst); ++dd)  // diag 8 (profiling only): one destination
             for (int j = 0; j < kChunks; ++j)
-              tma_store_2d_hint(&maps.out[dd], ubuf + j * 16384, c * PER + j * 64, row0, stream);
+              tma_store_2d_hint(&maps.out[dd], ubuf + j * 16384, cb + j * 64, row0, stream);
         asm volatile("cp.async.bulk.commit_group;" ::: "memory");
       }
       tph ^= 1;
@@ -1489,7 +1500,9 @@ int launch_ag_gemm(coconet_ctx* c, int group, const void* a, const void* w, cons
                    cudaStream_t s) {
   const int W = c->groups[size_t(group)].size;
   const int64_t per = cols / W;
-  if ((per != 128 && per != 256 && per != 384) || rows % 256 || k_local % BK || rows > INT32_MAX ||
+  // sub-block width: 384, 256 or 128 columns (the TMEM accumulator)
+  const int sbw = per % 384 == 0 ? 384 : per % 256 == 0 ? 256 : per % 128 == 0 ? 128 : 0;
+  if (!sbw || rows % 256 || k_local % BK || rows > INT32_MAX ||
       int64_t(rows) * cols > (int64_t(1) << 40) || W > kMaxRanks)
     return COCONET_ERR_UNSUPPORTED;
   int64_t ao = 0, wo = 0, bo = 0, ro = 0, oo = 0;
@@ -1525,8 +1538,8 @@ int launch_ag_gemm(coconet_ctx* c, int group, const void* a, const void* w, cons
   g.per = int(per);
   g.k_local = int(k_local);
   g.W = W;
-  g.n0 = int(std::min<int64_t>(per, 256));
-  g.n1 = int(per) - g.n0;
+  g.n0 = std::min(sbw, 256);
+  g.n1 = sbw - g.n0;
   g.dst = W;
   g.frate_scale = float(1.0 / (1.0 - hp->rate));
   g.seed = hp->seed;
@@ -1536,10 +1549,10 @@ int launch_ag_gemm(coconet_ctx* c, int group, const void* a, const void* w, cons
   g.f16 = in_elem == COCONET_F16 ? 1 : 0;
   g.diag = getenv("COCONET_GEMM_DIAG") ? atoi(getenv("COCONET_GEMM_DIAG")) : 0;
   const uint32_t fmt = in_elem == COCONET_BF16 ? 1u : 0u;
-  const int smem = per == 384 ? ag_smem<384>() : per == 256 ? ag_smem<256>() : ag_smem<128>();
-  auto fn = per == 384 ? mp_ag_gemm_kernel<384> : per == 256 ? mp_ag_gemm_kernel<256> : mp_ag_gemm_kernel<128>;
+  const int smem = sbw == 384 ? ag_smem<384>() : sbw == 256 ? ag_smem<256>() : ag_smem<128>();
+  auto fn = sbw == 384 ? mp_ag_gemm_kernel<384> : sbw == 256 ? mp_ag_gemm_kernel<256> : mp_ag_gemm_kernel<128>;
   CN_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-  const int units = g.owners * int(rows / 256);
+  const int units = g.owners * int(rows / 256) * int(per / sbw);
   cudaLaunchConfig_t cfg{};
   // DISTRIBUTED: the same grid on every rank (the edge barriers pair CTA b with CTA b)
   cfg.gridDim = dim3(unsigned(2 * (c->mode == COCONET_MODE_VIRTUAL ? std::min(units, c->sm_count / 2)
