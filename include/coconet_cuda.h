@@ -77,7 +77,20 @@ enum coconet_math { COCONET_MATH_EXACT = 0, COCONET_MATH_FAST = 1 };
 /* Collective algorithm (paper §6.1 crossover):
  * TWO_SHOT = reduce-scatter pull + all-gather push (sliced state),
  * ONE_SHOT = every rank pulls all peers (replicated state), AUTO = by size. */
-enum coconet_algo { COCONET_ALGO_AUTO = 0, COCONET_ALGO_TWO_SHOT = 1, COCONET_ALGO_ONE_SHOT = 2 };
+enum coconet_algo { COCONET_ALGO_AUTO = 0, COCONET_ALGO_TWO_SHOT = 1, COCONET_ALGO_ONE_SHOT = 2,
+                    /* NVLS: two-shot through the NVSwitch multicast view of the heaps (multimem.ld_reduce
+                     * for the reduce-scatter, multimem.st for the all-gather); explicit only, needs
+                     * coconet_nvls_setup. The switch sums in its own order: results are within fp32
+                     * rounding of TWO_SHOT, not bitwise. */
+                    COCONET_ALGO_NVLS = 3 };
+
+/* Symmetric-heap backing (coconet_init_ex). CUDAMALLOC: one cudaMalloc per rank,
+ * peers through CUDA IPC. CUMEM: cuMemCreate + cuMemMap, peers import a POSIX
+ * descriptor (fetched over a Unix socket). CUMEM_NVLS: a CUMEM heap sized to the
+ * multicast granularity, ready for coconet_nvls_setup. DEFAULT reads the
+ * environment variable COCONET_HEAP (cudamalloc | cumem | nvls; unset = cudamalloc). */
+enum coconet_heap_kind { COCONET_HEAP_DEFAULT = 0, COCONET_HEAP_CUDAMALLOC = 1, COCONET_HEAP_CUMEM = 2,
+                         COCONET_HEAP_CUMEM_NVLS = 3 };
 
 typedef struct coconet_ctx* coconet_ctx_t;
 typedef struct coconet_tlist* coconet_tlist_t;
@@ -91,12 +104,27 @@ const char* coconet_status_name(int status);
  * DISTRIBUTED: this process is `rank`; call coconet_exchange_handles next. */
 int coconet_init(coconet_ctx_t* out, int mode, int rank, int world, int device,
                  size_t heap_bytes_per_rank);
+/* coconet_init with an explicit heap kind (enum coconet_heap_kind). */
+int coconet_init_ex(coconet_ctx_t* out, int mode, int rank, int world, int device,
+                    size_t heap_bytes_per_rank, int heap_kind);
+int coconet_heap_kind(coconet_ctx_t ctx); /* the resolved kind, -1 for a null ctx */
 int coconet_finalize(coconet_ctx_t ctx);
 int coconet_world(coconet_ctx_t ctx, int* world, int* rank, int* mode);
 /* DISTRIBUTED bootstrap: export this rank's heap handle (`*len` bytes), then
  * pass the allgathered blob (world * len bytes, rank order) to open peers. */
 int coconet_heap_handle(coconet_ctx_t ctx, void* handle_out, size_t* len);
 int coconet_open_peers(coconet_ctx_t ctx, const void* all_handles, size_t len_per_rank);
+/* NVLS (NVSwitch multicast). coconet_nvls_supported: 1 if `device` can join a
+ * `world`-device multicast object, else 0 with the reason in `why`.
+ * coconet_nvls_setup: collective, stages 0, 1, 2 in order after
+ * coconet_open_peers with a process barrier after each (0: rank 0 creates the
+ * multicast object; 1: the others import it, every rank adds its device; 2:
+ * every rank binds its heap and maps the multicast range). Then
+ * coconet_nvls_mapped is 1 and COCONET_ALGO_NVLS runs on the world group.
+ * Replaces the AllReduce data path runtime.hpp:384-395 with in-switch sums. */
+int coconet_nvls_supported(int device, int world, char* why, size_t why_len);
+int coconet_nvls_setup(coconet_ctx_t ctx, int stage);
+int coconet_nvls_mapped(coconet_ctx_t ctx);
 /* Symmetric allocation: same offset on every rank; 256-byte aligned. */
 /* Deterministic first-fit over a free list (256-byte granules, neighbours
  * coalesced on free): alloc/free are collective - every rank issues the same

@@ -30,7 +30,7 @@ CUDA_LIB = PKG / "libcoconet_cuda.so"
 ENGINE_LIB = PKG / "libcoconet_engine.so"
 
 CU_SOURCES = ["context.cu", "tlist.cu", "fused_opt.cu", "gen.cu", "collectives.cu",
-              "fused_bdr.cu", "gemm_tc.cu", "pointwise.cu", "unfused.cu"]
+              "fused_bdr.cu", "gemm_tc.cu", "pointwise.cu", "unfused.cu", "heap_cumem.cu"]
 
 
 def _run(cmd, cwd=None):

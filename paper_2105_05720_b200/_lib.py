@@ -15,7 +15,9 @@ LIB_PATH = PKG / "libcoconet_cuda.so"
 F32, F16, BF16 = 0, 1, 2
 SUM, MAX, MIN = 0, 1, 2
 MATH_EXACT, MATH_FAST = 0, 1
-ALGO_AUTO, ALGO_TWO_SHOT, ALGO_ONE_SHOT = 0, 1, 2
+ALGO_AUTO, ALGO_TWO_SHOT, ALGO_ONE_SHOT, ALGO_NVLS = 0, 1, 2, 3
+HEAP_DEFAULT, HEAP_CUDAMALLOC, HEAP_CUMEM, HEAP_CUMEM_NVLS = 0, 1, 2, 3
+HEAP_KINDS = {"default": HEAP_DEFAULT, "cudamalloc": HEAP_CUDAMALLOC, "cumem": HEAP_CUMEM, "nvls": HEAP_CUMEM_NVLS}
 LAMB_AUTO, LAMB_GRID, LAMB_STREAMED, LAMB_TMA, LAMB_WINDOWED, LAMB_ONCHIP = 0, 1, 2, 3, 4, 5
 MODE_VIRTUAL, MODE_DISTRIBUTED = 0, 1
 MAX_RANKS = 8
@@ -71,6 +73,11 @@ _SIGNATURES = {
     "coconet_last_error": (C.c_char_p, []),
     "coconet_status_name": (C.c_char_p, [_I]),
     "coconet_init": (_I, [C.POINTER(_P), _I, _I, _I, _I, _SZ]),
+    "coconet_init_ex": (_I, [C.POINTER(_P), _I, _I, _I, _I, _SZ, _I]),
+    "coconet_heap_kind": (_I, [_P]),
+    "coconet_nvls_supported": (_I, [_I, _I, C.c_char_p, _SZ]),
+    "coconet_nvls_setup": (_I, [_P, _I]),
+    "coconet_nvls_mapped": (_I, [_P]),
     "coconet_finalize": (_I, [_P]),
     "coconet_world": (_I, [_P, C.POINTER(_I), C.POINTER(_I), C.POINTER(_I)]),
     "coconet_heap_handle": (_I, [_P, _P, C.POINTER(_SZ)]),

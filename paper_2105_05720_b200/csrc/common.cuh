@@ -41,6 +41,7 @@ struct RankSet {
   int me;                 // distributed: own group rank; virtual: -1
   int group;              // group id (flag region)
   uint32_t epoch;         // per-group call counter (flag value of this launch)
+  char* mc;               // NVLS multicast view of every rank's heap (world group), or null
   int* status;            // host-mapped status word (watchdog)
   unsigned long long timeout_ns;
 

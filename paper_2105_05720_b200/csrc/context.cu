@@ -8,6 +8,7 @@
 // a kernel reaches rank q's copy as heap[q] + offset — a local address in
 // VIRTUAL mode, an NVLink peer mapping (CUDA IPC) in DISTRIBUTED mode.
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 
@@ -55,6 +56,8 @@ int make_rankset(coconet_ctx* c, int group, RankSet* rs) {
   rs->group = group;
   rs->epoch = ++g.epoch;
   if (rs->epoch == 0) rs->epoch = ++g.epoch;  // 0 is the "never signalled" value
+  // the multicast range spans the world group's heaps only
+  rs->mc = group == 0 && c->mc_base ? c->mc_base : nullptr;
   rs->status = c->status_dev;
   rs->timeout_ns = c->timeout_ns;
   return COCONET_OK;
@@ -138,7 +141,23 @@ const char* coconet_status_name(int s) {
 
 int coconet_init(coconet_ctx_t* out, int mode, int rank, int world, int device,
                  size_t heap_bytes_per_rank) {
+  return coconet_init_ex(out, mode, rank, world, device, heap_bytes_per_rank, COCONET_HEAP_DEFAULT);
+}
+
+int coconet_init_ex(coconet_ctx_t* out, int mode, int rank, int world, int device,
+                    size_t heap_bytes_per_rank, int heap_kind) {
   if (!out) return set_error(COCONET_ERR_INVALID_INPUT, "null ctx out");
+  if (heap_kind == COCONET_HEAP_DEFAULT) {  // COCONET_HEAP=cumem|nvls|cudamalloc
+    const char* e = getenv("COCONET_HEAP");
+    heap_kind = !e ? COCONET_HEAP_CUDAMALLOC
+                : !strcmp(e, "cumem") ? COCONET_HEAP_CUMEM
+                : !strcmp(e, "nvls") ? COCONET_HEAP_CUMEM_NVLS
+                                     : COCONET_HEAP_CUDAMALLOC;
+  }
+  if (heap_kind < COCONET_HEAP_CUDAMALLOC || heap_kind > COCONET_HEAP_CUMEM_NVLS)
+    return set_error(COCONET_ERR_INVALID_INPUT, "unknown heap kind");
+  if (heap_kind == COCONET_HEAP_CUMEM_NVLS && mode != COCONET_MODE_DISTRIBUTED)
+    return set_error(COCONET_ERR_UNSUPPORTED, "an NVLS heap spans one GPU per rank (DISTRIBUTED mode)");
   *out = nullptr;
   if (world < 1 || world > kMaxRanks)
     return set_error(COCONET_ERR_NO_SUCH_RANK, "world size must be in [1, " + std::to_string(kMaxRanks) + "]");
@@ -151,18 +170,36 @@ int coconet_init(coconet_ctx_t* out, int mode, int rank, int world, int device,
   c->world = world;
   c->rank = mode == COCONET_MODE_VIRTUAL ? 0 : rank;
   c->device = device;
+  c->heap_kind = heap_kind;
   c->heap_bytes = ((heap_bytes_per_rank + kReservedBytes + 4095) / 4096) * 4096;
   cudaError_t e = cudaSetDevice(device);
   if (e != cudaSuccess) {
     delete c;
     return cuda_fail(e, "cudaSetDevice");
   }
+  const bool cumem = heap_kind != COCONET_HEAP_CUDAMALLOC;
+  if (cumem) {
+    int rc = cumem_round(c, &c->heap_bytes);
+    if (rc) {
+      delete c;
+      return rc;
+    }
+  }
   cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, device);
   int nlocal = mode == COCONET_MODE_VIRTUAL ? world : 1;
   for (int i = 0; i < nlocal; ++i) {
     int r = mode == COCONET_MODE_VIRTUAL ? i : rank;
-    e = cudaMalloc(&c->heap[r], c->heap_bytes);
-    if (e == cudaSuccess) e = cudaMemset(c->heap[r], 0, kReservedBytes);
+    if (cumem) {
+      int rc = cumem_create(c, r);
+      if (rc) {
+        coconet_finalize(c);
+        return rc;
+      }
+      e = cudaMemset(c->heap[r], 0, kReservedBytes);
+    } else {
+      e = cudaMalloc(&c->heap[r], c->heap_bytes);
+      if (e == cudaSuccess) e = cudaMemset(c->heap[r], 0, kReservedBytes);
+    }
     if (e != cudaSuccess) {
       coconet_finalize(c);
       return cuda_fail(e, "heap cudaMalloc");
@@ -175,7 +212,7 @@ int coconet_init(coconet_ctx_t* out, int mode, int rank, int world, int device,
     return cuda_fail(e, "status cudaHostAlloc");
   }
   *c->status_host = 0;
-  if (mode == COCONET_MODE_DISTRIBUTED) {
+  if (mode == COCONET_MODE_DISTRIBUTED && !cumem) {
     e = cudaIpcGetMemHandle(&c->my_handle, c->heap[rank]);
     if (e != cudaSuccess) {
       coconet_finalize(c);
@@ -198,6 +235,7 @@ int coconet_init(coconet_ctx_t* out, int mode, int rank, int world, int device,
 int coconet_finalize(coconet_ctx_t c) {
   if (!c) return COCONET_OK;
   cudaDeviceSynchronize();
+  cumem_release(c);  // cuMem heaps and the multicast mapping (no-op otherwise)
   for (int r = 0; r < kMaxRanks; ++r) {
     if (!c->heap[r]) continue;
     if (c->peer_mapped[r])
@@ -222,6 +260,7 @@ int coconet_world(coconet_ctx_t c, int* world, int* rank, int* mode) {
 int coconet_heap_handle(coconet_ctx_t c, void* handle_out, size_t* len) {
   if (!c || c->mode != COCONET_MODE_DISTRIBUTED)
     return set_error(COCONET_ERR_INVALID_INPUT, "heap handles exist in DISTRIBUTED mode only");
+  if (c->heap_kind != COCONET_HEAP_CUDAMALLOC) return cumem_export(c, handle_out, len);
   if (len) {
     if (handle_out && *len < sizeof(cudaIpcMemHandle_t))
       return set_error(COCONET_ERR_INVALID_INPUT, "handle buffer too small");
@@ -234,6 +273,7 @@ int coconet_heap_handle(coconet_ctx_t c, void* handle_out, size_t* len) {
 int coconet_open_peers(coconet_ctx_t c, const void* all, size_t len_per_rank) {
   if (!c || c->mode != COCONET_MODE_DISTRIBUTED)
     return set_error(COCONET_ERR_INVALID_INPUT, "open_peers is DISTRIBUTED-only");
+  if (c->heap_kind != COCONET_HEAP_CUDAMALLOC) return cumem_import(c, all, len_per_rank);
   if (len_per_rank != sizeof(cudaIpcMemHandle_t))
     return set_error(COCONET_ERR_INVALID_INPUT, "bad handle length");
   const char* blob = static_cast<const char*>(all);

@@ -340,6 +340,157 @@ __global__ void __launch_bounds__(kThreads, 2) adam_kernel(OptArgs a, AdamK k) {
   edge_barrier(rs, 1);  // peers done reading our g and writing our p
 }
 
+// ---- NVLS (COCONET_ALGO_NVLS): the two-shot schedule through the multicast
+// view of the world group's heaps (rs.mc, heap_cumem.cu). The reduce-scatter
+// pull of W peers' quads becomes ONE multimem.ld_reduce (the NVSwitch sums
+// the W copies and returns the total), and the all-gather push to W peers ONE
+// multimem.st (the switch writes every copy). Per GPU per direction that is
+// (W+1)/W*N*bytes on NVLink against 2(W-1)/W*N for the P2P two-shot. Quads
+// cut by a segment edge are pushed rank by rank (no 16-bit scalar multimem
+// store). The switch's summation order is its own: results are within fp32
+// rounding of TWO_SHOT (16-bit g: the sum is returned rounded to the element
+// type). fence.proxy.alias orders the multicast accesses against the unicast
+// ones of the same memory at both barriers.
+template <typename G>
+__device__ __forceinline__ void mc_ld_reduce4(const char* addr, float o[4]) {
+  if constexpr (sizeof(G) == 4) {
+    asm volatile("multimem.ld_reduce.relaxed.sys.global.add.v4.f32 {%0,%1,%2,%3}, [%4];"
+                 : "=f"(o[0]), "=f"(o[1]), "=f"(o[2]), "=f"(o[3])
+                 : "l"(addr)
+                 : "memory");
+  } else {
+    uint32_t r[2];
+    if constexpr (std::is_same<G, __half>::value)
+      asm volatile("multimem.ld_reduce.relaxed.sys.global.add.acc::f32.v2.f16x2 {%0,%1}, [%2];"
+                   : "=r"(r[0]), "=r"(r[1])
+                   : "l"(addr)
+                   : "memory");
+    else
+      asm volatile("multimem.ld_reduce.relaxed.sys.global.add.acc::f32.v2.bf16x2 {%0,%1}, [%2];"
+                   : "=r"(r[0]), "=r"(r[1])
+                   : "l"(addr)
+                   : "memory");
+    const G* h = reinterpret_cast<const G*>(r);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) o[i] = to_f32(h[i]);
+  }
+}
+
+// Whole quad to every rank through the multicast address; a partial quad
+// (lo > 0 or hi < 4) rank by rank through the unicast peer mappings.
+template <typename T>
+__device__ __forceinline__ void mc_st4(char* mc, char* const* base, int W, int64_t off, const float v[4], int lo,
+                                       int hi) {
+  if (lo == 0 && hi == 4) {
+    if constexpr (sizeof(T) == 4) {
+      asm volatile("multimem.st.relaxed.sys.global.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(mc + off), "f"(v[0]),
+                   "f"(v[1]), "f"(v[2]), "f"(v[3])
+                   : "memory");
+    } else {
+      T h[4] = {from_f32<T>(v[0]), from_f32<T>(v[1]), from_f32<T>(v[2]), from_f32<T>(v[3])};
+      const uint2 u = *reinterpret_cast<const uint2*>(h);
+      asm volatile("multimem.st.relaxed.sys.global.v2.f32 [%0], {%1,%2};" ::"l"(mc + off), "r"(u.x), "r"(u.y)
+                   : "memory");
+    }
+  } else {
+    for (int j = 0; j < W; ++j) st4m(reinterpret_cast<T*>(base[j] + off), v, lo, hi);
+  }
+}
+
+__device__ __forceinline__ void fence_proxy_alias() { asm volatile("fence.proxy.alias;" ::: "memory"); }
+
+template <typename G, int MATH>
+__device__ __forceinline__ void adam_quads_nvls(char* const* s_base, char* mc, const SegD& d, int64_t qs,
+                                                int64_t qe, float* m, float* v, const char* pme, int W, int lane,
+                                                const AdamK& k) {
+  constexpr int U = 2;
+  for (int64_t qb = qs + lane; qb < qe; qb += 32 * U) {
+    float g[U][4], mm[U][4], vv[U][4], pp[U][4];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t q = min(qb + 32 * u, qe - 1);
+      const int64_t e0 = q << 2;
+      const int64_t si = d.sidx + (e0 - d.toff);
+      mc_ld_reduce4<G>(mc + d.aoff + e0 * int64_t(sizeof(G)), g[u]);
+      ld4(m + si, mm[u]);
+      ld4(v + si, vv[u]);
+      ld4(reinterpret_cast<const float*>(pme + d.boff) + e0, pp[u]);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t q = qb + 32 * u;
+      if (q < qe) {
+        const int64_t e0 = q << 2;
+        int lo, hi;
+        quad_range(d, e0, lo, hi);
+        const int64_t si = d.sidx + (e0 - d.toff);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) adam_elem<MATH>(g[u][i], mm[u][i], vv[u][i], pp[u][i], k);
+        st4m(m + si, mm[u], lo, hi);
+        st4m(v + si, vv[u], lo, hi);
+        mc_st4<float>(mc, s_base, W, d.boff + e0 * 4, pp[u], lo, hi);
+      }
+    }
+  }
+}
+
+template <typename G, int MATH>
+__global__ void __launch_bounds__(kThreads, 2) adam_nvls_kernel(OptArgs a, AdamK k) {
+  __shared__ char* s_base[kMaxRanks];
+  const RankSet& rs = a.rs;
+  if (threadIdx.x < kMaxRanks) s_base[threadIdx.x] = threadIdx.x < rs.world ? rs.base[threadIdx.x] : nullptr;
+  const int W = rs.world, me = rs.rank();
+  if (!edge_barrier(rs, 0)) return;  // peers' gradients are complete
+  fence_proxy_alias();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t sb = a.seg_begin[me], se = a.seg_begin[me + 1];
+  float* m = reinterpret_cast<float*>(s_base[me] + a.m_off);
+  float* v = reinterpret_cast<float*>(s_base[me] + a.v_off);
+  const int64_t wid = int64_t(blockIdx.x) * kWarps + warp, wstride = int64_t(gridDim.x) * kWarps;
+  const int P = a.parts;
+  for (int64_t it = wid; it < (se - sb) * P; it += wstride) {
+    const Seg sg = a.segs[sb + it / P];
+    const int part = int(it % P);
+    const int tens = meta_tensor(sg.meta);
+    const SegD d{sg.toff, sg.sidx, a.offs[tens], a.offs[a.n_tensors + tens], meta_len(sg.meta), meta_owner(sg.meta),
+                 tens};
+    const int64_t q0 = d.toff >> 2, nq = ((d.toff + d.len + 3) >> 2) - q0;
+    adam_quads_nvls<G, MATH>(s_base, rs.mc, d, q0 + nq * part / P, q0 + nq * (part + 1) / P, m, v, s_base[me], W,
+                             lane, k);
+  }
+  fence_proxy_alias();
+  edge_barrier(rs, 1);  // peers done reading our g and writing our p
+}
+
+// Tensor-list AllReduce (SUM) through the switch: rank r reduces its own
+// chunk with multimem.ld_reduce and stores the total into every rank's out.
+template <typename T>
+__global__ void __launch_bounds__(kThreads, 2) allreduce_nvls_kernel(OptArgs a) {
+  __shared__ char* s_base[kMaxRanks];
+  const RankSet& rs = a.rs;
+  if (threadIdx.x < kMaxRanks) s_base[threadIdx.x] = threadIdx.x < rs.world ? rs.base[threadIdx.x] : nullptr;
+  const int W = rs.world, me = rs.rank();
+  if (!edge_barrier(rs, 0)) return;
+  fence_proxy_alias();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (SegIter it(a.segs, a.offs, a.n_tensors, a.seg_begin[me] + int64_t(blockIdx.x) * kWarps + warp,
+                  a.seg_begin[me + 1], int64_t(gridDim.x) * kWarps);
+       it.valid(); it.next()) {
+    const SegD d = it.get();
+    const int64_t q0 = d.toff >> 2, q1 = (d.toff + d.len + 3) >> 2;
+    for (int64_t q = q0 + lane; q < q1; q += 32) {
+      const int64_t e0 = q << 2;
+      float acc[4];
+      mc_ld_reduce4<T>(rs.mc + d.aoff + e0 * int64_t(sizeof(T)), acc);
+      int lo, hi;
+      quad_range(d, e0, lo, hi);
+      mc_st4<T>(rs.mc, s_base, W, d.boff + e0 * int64_t(sizeof(T)), acc, lo, hi);
+    }
+  }
+  fence_proxy_alias();
+  edge_barrier(rs, 1);
+}
+
 // Tensor-list AllReduce (x -> out). TWO_SHOT = pull-RS of the own chunk +
 // push-AG; ONE_SHOT = pull everything, write own copy (out != x).
 template <typename T, int RED, bool ONE_SHOT, int WT, int U>
@@ -2343,6 +2494,12 @@ const void* adam_pick(int math, bool os, int W) {
   return os ? adam_w<G, COCONET_MATH_FAST, true>(W) : adam_w<G, COCONET_MATH_FAST, false>(W);
 }
 
+template <typename G>
+const void* adam_nvls_pick(int math) {
+  return math == COCONET_MATH_EXACT ? reinterpret_cast<const void*>(&adam_nvls_kernel<G, COCONET_MATH_EXACT>)
+                                    : reinterpret_cast<const void*>(&adam_nvls_kernel<G, COCONET_MATH_FAST>);
+}
+
 template <typename T, int RED, bool OS>
 const void* ar_w(int W) {
   switch (W) {
@@ -2432,7 +2589,11 @@ int coconet_fused_rs_adam_ag(coconet_ctx_t c, coconet_tlist_t tl, const void* co
     return set_error(COCONET_ERR_INVALID_INPUT, "bad math mode");
   cudaStream_t stream = static_cast<cudaStream_t>(stream_);
   const int W = c->groups[size_t(tl->group)].size;
-  const bool os = resolve_one_shot(hp->algo, tl, W);
+  const bool nvls = hp->algo == COCONET_ALGO_NVLS;
+  if (nvls && (!c->mc_base || tl->group != 0))
+    return set_error(COCONET_ERR_UNSUPPORTED, "COCONET_ALGO_NVLS needs coconet_nvls_setup on the world group "
+                                              "(coconet_nvls_supported reports why it is unavailable)");
+  const bool os = !nvls && resolve_one_shot(hp->algo, tl, W);
   int64_t m_off = 0, v_off = 0;
   int rc = check_state(c, m_shard, &m_off);
   if (!rc) rc = check_state(c, v_shard, &v_off);
@@ -2465,7 +2626,7 @@ int coconet_fused_rs_adam_ag(coconet_ctx_t c, coconet_tlist_t tl, const void* co
   // 0 keeps the LDG kernel, 1 forces the ring whatever the bucket size.
   const char* te = getenv("COCONET_ADAM_TMA");
   const bool tma = te ? te[0] == '1' : tl->bucket_cap >= (W == 1 ? kTmaMinBucket : 4 * kTmaMinBucket);
-  if (!os && tma) {
+  if (!os && !nvls && tma) {
     const void* fn = nullptr;
     int sbytes = 0, threads = 0;
     auto pick = [&](auto tag_g) {
@@ -2501,7 +2662,10 @@ int coconet_fused_rs_adam_ag(coconet_ctx_t c, coconet_tlist_t tl, const void* co
     void* args[] = {&a, &k, &ta};
     return coop_launch(c, fn, dim3(unsigned(blocks), unsigned(lr)), dim3(unsigned(threads)), args, smem, stream);
   }
-  const void* fn = g_elem == COCONET_F32   ? adam_pick<float>(hp->math, os, W)
+  const void* fn = nvls ? (g_elem == COCONET_F32   ? adam_nvls_pick<float>(hp->math)
+                           : g_elem == COCONET_F16 ? adam_nvls_pick<__half>(hp->math)
+                                                   : adam_nvls_pick<__nv_bfloat16>(hp->math))
+                   : g_elem == COCONET_F32 ? adam_pick<float>(hp->math, os, W)
                    : g_elem == COCONET_F16 ? adam_pick<__half>(hp->math, os, W)
                                            : adam_pick<__nv_bfloat16>(hp->math, os, W);
   // split segments while the resident grid has idle warps (small lists)
@@ -2789,7 +2953,13 @@ int coconet_allreduce(coconet_ctx_t c, coconet_tlist_t tl, const void* const* x,
   if (elem < COCONET_F32 || elem > COCONET_BF16) return set_error(COCONET_ERR_INVALID_INPUT, "bad elem");
   cudaStream_t stream = static_cast<cudaStream_t>(stream_);
   const int W = c->groups[size_t(tl->group)].size;
-  bool os = resolve_one_shot(algo, tl, W);
+  const bool nvls = algo == COCONET_ALGO_NVLS;
+  if (nvls && (!c->mc_base || tl->group != 0))
+    return set_error(COCONET_ERR_UNSUPPORTED, "COCONET_ALGO_NVLS needs coconet_nvls_setup on the world group "
+                                              "(coconet_nvls_supported reports why it is unavailable)");
+  if (nvls && reducer != COCONET_SUM)
+    return set_error(COCONET_ERR_UNSUPPORTED, "COCONET_ALGO_NVLS reduces with SUM only");
+  bool os = !nvls && resolve_one_shot(algo, tl, W);
   bool in_place = false;
   for (int i = 0; i < tl->n_tensors; ++i) in_place |= (x[i] == out[i]);
   if (in_place) os = false;  // one-shot reads every peer's whole input while writing
@@ -2800,7 +2970,10 @@ int coconet_allreduce(coconet_ctx_t c, coconet_tlist_t tl, const void* const* x,
   if (rc) return rc;
   OptArgs a;
   fill_args(tl, &a, rs, 0, 0);
-  const void* fn = elem == COCONET_F32   ? ar_pick<float>(reducer, os, W)
+  const void* fn = nvls ? (elem == COCONET_F32   ? reinterpret_cast<const void*>(&allreduce_nvls_kernel<float>)
+                           : elem == COCONET_F16 ? reinterpret_cast<const void*>(&allreduce_nvls_kernel<__half>)
+                                                 : reinterpret_cast<const void*>(&allreduce_nvls_kernel<__nv_bfloat16>))
+                   : elem == COCONET_F32 ? ar_pick<float>(reducer, os, W)
                    : elem == COCONET_F16 ? ar_pick<__half>(reducer, os, W)
                                          : ar_pick<__nv_bfloat16>(reducer, os, W);
   void* args[] = {&a};

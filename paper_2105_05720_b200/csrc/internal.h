@@ -1,6 +1,7 @@
 // Host-side internals of libcoconet_cuda (context, groups, errors, launches).
 #pragma once
 
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -19,6 +20,8 @@ struct coconet_group_s {
 
 #include "symm_heap.h"
 
+struct FdServer;
+
 struct coconet_ctx {
   int mode = COCONET_MODE_VIRTUAL;
   int world = 1;
@@ -29,6 +32,20 @@ struct coconet_ctx {
   char* heap[coconet::kMaxRanks] = {};
   bool peer_mapped[coconet::kMaxRanks] = {};
   cudaIpcMemHandle_t my_handle{};
+  // cuMem heap (heap_kind CUMEM / CUMEM_NVLS, heap_cumem.cu): physical
+  // allocation handles (own ranks and imported peers), the exported POSIX
+  // descriptor and the socket server that hands it to peers
+  int heap_kind = COCONET_HEAP_CUDAMALLOC;
+  CUmemGenericAllocationHandle cm_handle[coconet::kMaxRanks] = {};
+  bool cm_mapped[coconet::kMaxRanks] = {};
+  int cm_fd = -1;
+  FdServer* fdsrv = nullptr;
+  char peer_srv[coconet::kMaxRanks][64] = {};  // peers' descriptor servers (DISTRIBUTED)
+  // NVLS multicast object over the world group's heaps (coconet_nvls_setup)
+  CUmemGenericAllocationHandle mc_handle = 0;
+  int mc_stage = 0;  // 0 none, 1 created/imported, 2 device added, 3 bound + mapped
+  int mc_fd = -1;
+  char* mc_base = nullptr;
   SymmHeap alloc;  // user region [kReservedBytes, heap_bytes)
   int* status_host = nullptr;  // host-mapped watchdog word
   int* status_dev = nullptr;
@@ -82,5 +99,14 @@ int coop_launch(coconet_ctx* c, const void* func, dim3 grid, dim3 block, void** 
                 size_t smem, cudaStream_t stream);
 
 bool valid_group(const coconet_ctx* c, int group);
+
+// cuMem heap (heap_cumem.cu). cumem_create maps a fresh heap for local rank
+// slot r; export/import move it between processes as a POSIX descriptor.
+int cumem_create(coconet_ctx* c, int r);
+int cumem_export(coconet_ctx* c, void* blob_out, size_t* len);
+int cumem_import(coconet_ctx* c, const void* blob, size_t len_per_rank);
+void cumem_release(coconet_ctx* c);
+// heap bytes rounded to what the kind requires (allocation / multicast granularity)
+int cumem_round(coconet_ctx* c, size_t* bytes);
 
 }  // namespace coconet

@@ -85,7 +85,8 @@ class SymmBuffer:
 
 class Context:
     def __init__(self, world: int, mode: str = "virtual", rank: int = 0, device: int = 0,
-                 heap_bytes: int = 1 << 30, process_group=None, timeout_ms: int | None = None):
+                 heap_bytes: int = 1 << 30, process_group=None, timeout_ms: int | None = None,
+                 heap: str = "default"):
         self.lib = load()
         self.world = int(world)
         self.mode = mode
@@ -95,12 +96,18 @@ class Context:
         h = C.c_void_p()
         torch.cuda.set_device(self.device)
         torch.cuda.init()
-        check(self.lib.coconet_init(C.byref(h), m, self.rank, self.world, self.device, heap_bytes))
+        if heap not in _lib.HEAP_KINDS:
+            raise ValueError(f"heap must be one of {sorted(_lib.HEAP_KINDS)}")
+        check(self.lib.coconet_init_ex(C.byref(h), m, self.rank, self.world, self.device, heap_bytes,
+                                       _lib.HEAP_KINDS[heap]))
         self.handle = h
+        self.heap_kind = {v: k for k, v in _lib.HEAP_KINDS.items()}[int(self.lib.coconet_heap_kind(h))]
         if timeout_ms is not None:
             check(self.lib.coconet_set_timeout_ms(h, int(timeout_ms)))
         if mode == "distributed":
             self._open_peers(process_group)
+            if self.heap_kind == "nvls":
+                self._nvls_setup(process_group)
         self._heap_bytes = None
         self._heaps: dict[int, torch.Tensor] = {}
         self._bases: dict[int, int] = {}
@@ -117,6 +124,19 @@ class Context:
         blob = exchange_blobs(bytes(buf), self.world, pg)
         check(self.lib.coconet_open_peers(self.handle, C.c_char_p(blob), n.value))
         dist.barrier(group=pg)
+
+    def _nvls_setup(self, pg):
+        """coconet_nvls_setup's three collective stages, a process barrier after each."""
+        import torch.distributed as dist
+
+        for stage in range(3):
+            check(self.lib.coconet_nvls_setup(self.handle, stage))
+            dist.barrier(group=pg)
+
+    @property
+    def nvls(self) -> bool:
+        """True when the world group's heaps are mapped through an NVSwitch multicast object."""
+        return bool(self.lib.coconet_nvls_mapped(self.handle))
 
     def close(self):
         if self.handle:
@@ -193,3 +213,11 @@ class Context:
 
     def launch_count(self) -> int:
         return int(self.lib.coconet_launch_count(self.handle))
+
+
+def nvls_supported(device: int = 0, world: int = 8) -> tuple[bool, str]:
+    """(supported, reason) for an NVSwitch multicast object over `world` GPUs."""
+    lib = load()
+    why = C.create_string_buffer(256)
+    ok = bool(lib.coconet_nvls_supported(int(device), int(world), why, 256))
+    return ok, why.value.decode()

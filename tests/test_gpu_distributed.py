@@ -32,7 +32,7 @@ def _inputs(W, counts):
     return g, p, m, v
 
 
-def _worker(rank, world, port, counts, q):
+def _worker(rank, world, port, counts, q, heap="cudamalloc"):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -43,7 +43,9 @@ def _worker(rank, world, port, counts, q):
         from paper_2105_05720_b200.runtime import Context
 
         torch.cuda.set_device(0)
-        ctx = Context(world, mode="distributed", rank=rank, device=0, heap_bytes=64 << 20, timeout_ms=60000)
+        ctx = Context(world, mode="distributed", rank=rank, device=0, heap_bytes=64 << 20, timeout_ms=60000,
+                      heap=heap)
+        assert ctx.heap_kind == heap
         tl = TensorList(ctx, counts)
         g, p, m, v = _inputs(world, counts)
         gb = [ctx.alloc([n]) for n in counts]
@@ -114,13 +116,16 @@ def _worker(rank, world, port, counts, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2, 4])
-def test_distributed_processes_share_one_gpu(world):
+@pytest.mark.parametrize("world,heap", [(2, "cudamalloc"), (4, "cudamalloc"), (2, "cumem"), (4, "cumem")])
+def test_distributed_processes_share_one_gpu(world, heap):
+    """heap="cumem": the heaps are cuMemCreate allocations whose POSIX
+    descriptors the processes pass over Unix sockets (heap_cumem.cu) instead
+    of CUDA IPC handles; results must be the same bits."""
     counts = [3000, 1024, 77, 5000]
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, counts, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, counts, q, heap)) for r in range(world)]
     for p in procs:
         p.start()
     res = [q.get(timeout=300) for _ in range(world)]
