@@ -267,11 +267,14 @@ enum coconet_lamb_sched {
                                (lag_elems = window size), pass 2 of a window one window after
                                its pass 1 so its m, v, p re-reads hit L2; per-window arrival
                                counters instead of grid-wide syncs. m, v bit-identical to TMA */
-  COCONET_LAMB_ONCHIP = 5 /* group size 1: pass 1 keeps u = m'/(sqrt(v')+eps) + wd*p on chip
+  COCONET_LAMB_ONCHIP = 5, /* group size 1: pass 1 keeps u = m'/(sqrt(v')+eps) + wd*p on chip
                              (TMEM + shared memory of one CTA per SM) for windows of whole
                              tensors, so pass 2 reads only p (30 B/element at fp16 g against
                              38); items beyond a CTA's on-chip capacity take TMA's pass 2.
                              m, v bit-identical to TMA */
+  COCONET_LAMB_NVLS = 6 /* GRID's two passes with the RS pull as one multimem.ld_reduce and the AG
+                           push as one multimem.st through the NVSwitch multicast view
+                           (coconet_nvls_setup; world group only; never chosen by AUTO) */
 };
 
 int coconet_fused_rs_lamb_ag(coconet_ctx_t ctx, coconet_tlist_t tl, const void* const* g,

@@ -18,7 +18,7 @@ MATH_EXACT, MATH_FAST = 0, 1
 ALGO_AUTO, ALGO_TWO_SHOT, ALGO_ONE_SHOT, ALGO_NVLS = 0, 1, 2, 3
 HEAP_DEFAULT, HEAP_CUDAMALLOC, HEAP_CUMEM, HEAP_CUMEM_NVLS = 0, 1, 2, 3
 HEAP_KINDS = {"default": HEAP_DEFAULT, "cudamalloc": HEAP_CUDAMALLOC, "cumem": HEAP_CUMEM, "nvls": HEAP_CUMEM_NVLS}
-LAMB_AUTO, LAMB_GRID, LAMB_STREAMED, LAMB_TMA, LAMB_WINDOWED, LAMB_ONCHIP = 0, 1, 2, 3, 4, 5
+LAMB_AUTO, LAMB_GRID, LAMB_STREAMED, LAMB_TMA, LAMB_WINDOWED, LAMB_ONCHIP, LAMB_NVLS = 0, 1, 2, 3, 4, 5, 6
 MODE_VIRTUAL, MODE_DISTRIBUTED = 0, 1
 MAX_RANKS = 8
 

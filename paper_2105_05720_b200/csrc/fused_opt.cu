@@ -572,7 +572,10 @@ __device__ __forceinline__ double trust_ratio(double P, double U, const LambK& k
 //  deterministic) -> pushed into every peer's exchange area -> flag barrier
 //  -> totals combined in rank order (state.hpp:163-167)
 //  pass 2: trust ratio -> p update -> AG push.
-template <typename G, int WT, int U>
+// NV (COCONET_LAMB_NVLS, WT = 0): the RS pull is one multimem.ld_reduce per
+// quad and the AG push one multimem.st through the multicast view (rs.mc);
+// the per-tensor partials still go rank by rank (2 doubles per tensor).
+template <typename G, int WT, int U, bool NV = false>
 __global__ void __launch_bounds__(kThreads, 2) lamb_kernel(OptArgs a, LambK k) {
   __shared__ char* s_base[kMaxRanks];
   const RankSet& rs = a.rs;
@@ -582,6 +585,7 @@ __global__ void __launch_bounds__(kThreads, 2) lamb_kernel(OptArgs a, LambK k) {
   // No early return before the grid syncs: a CTA whose barrier timed out
   // skips its work but still arrives, so the grid cannot deadlock.
   const bool ok = edge_barrier(rs, 0);
+  if constexpr (NV) fence_proxy_alias();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t sb = a.seg_begin[me], se = ok ? a.seg_begin[me + 1] : sb;
   float* m = reinterpret_cast<float*>(s_base[me] + a.m_off);
@@ -596,14 +600,15 @@ __global__ void __launch_bounds__(kThreads, 2) lamb_kernel(OptArgs a, LambK k) {
     const int64_t q0 = d.toff >> 2, q1 = (d.toff + d.len + 3) >> 2;
     float sp = 0.f, su = 0.f;  // <=1024 squares per segment: fp32 is ample
     for (int64_t qb = q0 + lane; qb < q1; qb += 32 * U) {
-      float g[U][Ranks<WT>::kMax][4], mm[U][4], vv[U][4], pp[U][4];
+      float g[U][NV ? 1 : Ranks<WT>::kMax][4], mm[U][4], vv[U][4], pp[U][4];
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         const int64_t q = min(qb + 32 * u, q1 - 1);  // clamped, unconditional loads
         {
           const int64_t e0 = q << 2;
           const int64_t si = d.sidx + (e0 - d.toff);
-          ring_load4<G, COCONET_SUM, WT>(s_base, d.aoff + e0 * int64_t(sizeof(G)), me, W, g[u]);
+          if constexpr (NV) mc_ld_reduce4<G>(rs.mc + d.aoff + e0 * int64_t(sizeof(G)), g[u][0]);
+          else ring_load4<G, COCONET_SUM, WT>(s_base, d.aoff + e0 * int64_t(sizeof(G)), me, W, g[u]);
           ld4(m + si, mm[u]);
           ld4(v + si, vv[u]);
           ld4(reinterpret_cast<const float*>(pme + d.boff) + e0, pp[u]);
@@ -618,7 +623,12 @@ __global__ void __launch_bounds__(kThreads, 2) lamb_kernel(OptArgs a, LambK k) {
           quad_range(d, e0, lo, hi);
           const int64_t si = d.sidx + (e0 - d.toff);
           float gs[4];
-          ring_fold4<COCONET_SUM, WT>(g[u], W, gs);
+          if constexpr (NV) {
+#pragma unroll
+            for (int i = 0; i < 4; ++i) gs[i] = g[u][0][i];
+          } else {
+            ring_fold4<COCONET_SUM, WT>(g[u], W, gs);
+          }
           float fp = 0.f, fu = 0.f;
 #pragma unroll
           for (int i = 0; i < 4; ++i) {
@@ -707,13 +717,18 @@ __global__ void __launch_bounds__(kThreads, 2) lamb_kernel(OptArgs a, LambK k) {
           float pn[4];
 #pragma unroll
           for (int i = 0; i < 4; ++i) pn[i] = pp[u][i] - ratio * lamb_u(mm[u][i], vv[u][i], pp[u][i], k);
+          if constexpr (NV) {
+            mc_st4<float>(rs.mc, s_base, W, poff + e0 * 4, pn, lo, hi);
+          } else {
 #pragma unroll
-          for (int j = 0; j < Ranks<WT>::kMax; ++j)
-            if (Ranks<WT>::has(j, W)) st4m(reinterpret_cast<float*>(s_base[j] + poff) + e0, pn, lo, hi);
+            for (int j = 0; j < Ranks<WT>::kMax; ++j)
+              if (Ranks<WT>::has(j, W)) st4m(reinterpret_cast<float*>(s_base[j] + poff) + e0, pn, lo, hi);
+          }
         }
       }
     }
   }
+  if constexpr (NV) fence_proxy_alias();
   edge_barrier(rs, 1);
 }
 
@@ -2687,7 +2702,7 @@ int coconet_fused_rs_lamb_ag(coconet_ctx_t c, coconet_tlist_t tl, const void* co
   if (tl->ctx != c) return set_error(COCONET_ERR_INVALID_INPUT, "tensor list belongs to another context");
   if (hp->math != COCONET_MATH_FAST && hp->math != COCONET_MATH_EXACT)
     return set_error(COCONET_ERR_INVALID_INPUT, "bad math");
-  if (hp->sched < COCONET_LAMB_AUTO || hp->sched > COCONET_LAMB_ONCHIP)
+  if (hp->sched < COCONET_LAMB_AUTO || hp->sched > COCONET_LAMB_NVLS)
     return set_error(COCONET_ERR_INVALID_INPUT, "bad LAMB schedule");
   // exchange [rank][tensor] (P, U) doubles + ready flags [rank][tensor]
   if (size_t(kMaxRanks) * tl->n_tensors * (2 * sizeof(double) + sizeof(uint32_t)) > kTileFlagsOff)
@@ -2730,6 +2745,8 @@ int coconet_fused_rs_lamb_ag(coconet_ctx_t c, coconet_tlist_t tl, const void* co
   // AUTO: the TMA ring with buckets of >= kTmaMinBucket elements at W = 1,
   // >= 4x that across ranks (BERT-336M, W = 2/8 virtual: TMA wins at 16384,
   // GRID at 4096; profiles/r01_lamb_w_probe.json), GRID otherwise
+  if (hp->math == COCONET_MATH_EXACT && hp->sched == COCONET_LAMB_NVLS)
+    return set_error(COCONET_ERR_UNSUPPORTED, "COCONET_LAMB_NVLS runs FAST math (the switch sums in its own order)");
   if (hp->math == COCONET_MATH_EXACT) {  // one schedule: the read-only pass 1 of lamb_exact_kernel
     const void* fn = g_elem == COCONET_F32   ? lamb_exact_pick<float>(W)
                      : g_elem == COCONET_F16 ? lamb_exact_pick<__half>(W)
@@ -2911,6 +2928,16 @@ int coconet_fused_rs_lamb_ag(coconet_ctx_t c, coconet_tlist_t tl, const void* co
     if (rc) return rc;
     void* args[] = {&a, &k, &ta};
     return coop_launch(c, fn, dim3(unsigned(blocks), unsigned(lr)), dim3(unsigned(threads)), args, smem, stream);
+  }
+  if (sched == COCONET_LAMB_NVLS) {
+    if (!c->mc_base || tl->group != 0)
+      return set_error(COCONET_ERR_UNSUPPORTED, "COCONET_LAMB_NVLS needs coconet_nvls_setup on the world group "
+                                                "(coconet_nvls_supported reports why it is unavailable)");
+    const void* fn = g_elem == COCONET_F32   ? reinterpret_cast<const void*>(&lamb_kernel<float, 0, 2, true>)
+                     : g_elem == COCONET_F16 ? reinterpret_cast<const void*>(&lamb_kernel<__half, 0, 2, true>)
+                                             : reinterpret_cast<const void*>(&lamb_kernel<__nv_bfloat16, 0, 2, true>);
+    void* args[] = {&a, &k};
+    return launch_opt(c, tl, fn, args, false, stream);
   }
   if (sched == COCONET_LAMB_GRID) {
     const void* fn = g_elem == COCONET_F32   ? lamb_pick<float>(W)

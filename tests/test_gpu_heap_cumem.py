@@ -12,7 +12,8 @@ import torch
 
 from oracle import coconet_oracle as co
 from paper_2105_05720_b200 import _lib
-from paper_2105_05720_b200.collectives import AdamHParams, TensorList, allreduce, fused_rs_adam_ag
+from paper_2105_05720_b200.collectives import (AdamHParams, LambHParams, TensorList, allreduce, fused_rs_adam_ag,
+                                               fused_rs_lamb_ag)
 from paper_2105_05720_b200.runtime import Context, nvls_supported
 from tests.dp_util import DPWorkload, dsl_scalars
 
@@ -84,6 +85,8 @@ def test_nvls_gate_reports_and_refuses():
     with pytest.raises(_lib.CoconetError, match="Unsupported"):
         wl.adam(AdamHParams(lr=sc["lr"], beta1=sc["beta1"], beta2=sc["beta2"], t=sc["t"],
                             math=_lib.MATH_FAST, algo=_lib.ALGO_NVLS))
+    with pytest.raises(_lib.CoconetError, match="Unsupported"):
+        wl.lamb(LambHParams(lr=0.01, beta1=0.9, beta2=0.999, t=1.0, sched=_lib.LAMB_NVLS))
     tl = TensorList(ctx, [4096])
     x, o = [ctx.alloc([4096])], [ctx.alloc([4096])]
     with pytest.raises(_lib.CoconetError, match="Unsupported"):
@@ -125,8 +128,20 @@ def _nvls_worker(rank, world, port, counts, q):
                                                                    _lib.MATH_FAST, algo))
             allreduce(ctx, tl, gb, ob, algo=algo)
             ctx.check()
-            res[algo] = ([ctx.view(b).cpu().numpy() for b in pb], [ctx.view(b).cpu().numpy() for b in ob])
-        dev = max(co.max_rel_deviation(a, b) for k in (0, 1)
+            got_p = [ctx.view(b).cpu().numpy() for b in pb]
+            # LAMB: GRID across ranks against its NVLS schedule
+            for t in range(len(counts)):
+                ctx.view(pb[t]).copy_(torch.from_numpy(p[t]))
+            ctx.view(mb).zero_()
+            ctx.view(vb).zero_()
+            torch.cuda.synchronize()
+            dist.barrier()
+            fused_rs_lamb_ag(ctx, tl, gb, pb, mb, vb, LambHParams(
+                lr=0.01, beta1=0.9, beta2=0.999, t=1.0,
+                sched=_lib.LAMB_NVLS if algo == _lib.ALGO_NVLS else _lib.LAMB_GRID))
+            ctx.check()
+            res[algo] = (got_p, [ctx.view(b).cpu().numpy() for b in ob], [ctx.view(b).cpu().numpy() for b in pb])
+        dev = max(co.max_rel_deviation(a, b) for k in (0, 1, 2)
                   for a, b in zip(res[_lib.ALGO_NVLS][k], res[_lib.ALGO_TWO_SHOT][k]))
         dist.barrier()
         ctx.close()
@@ -138,8 +153,9 @@ def _nvls_worker(rank, world, port, counts, q):
 
 
 def test_nvls_adam_and_allreduce_match_two_shot():
-    """COCONET_ALGO_NVLS (multimem.ld_reduce RS + multimem.st AG) within fp32
-    rounding of the P2P two-shot, one process per GPU."""
+    """COCONET_ALGO_NVLS / COCONET_LAMB_NVLS (multimem.ld_reduce RS +
+    multimem.st AG) within fp32 rounding of the P2P two-shot, one process per
+    GPU: fused Adam, AllReduce and fused LAMB."""
     import socket
 
     import torch.multiprocessing as mp
