@@ -585,11 +585,14 @@ def run_coconet(args):
             "unfused_baseline": baseline,
             "extras": extras,
         }
-        print(json.dumps(line))
-    if ctx.handle:
-        ctx.close()
-    if distributed:
-        dist.destroy_process_group()
+        print(json.dumps(line), flush=True)
+    try:  # teardown after the line is out: a failure here must not cost the measurement
+        if ctx.handle:
+            ctx.close()
+        if distributed:
+            dist.destroy_process_group()
+    except Exception as e:
+        print(f"teardown: {e!r}", file=sys.stderr)
 
 
 def adam_vs_torch(ctx, counts, event_time):

@@ -155,6 +155,11 @@ def exported_symbols() -> list[str]:
     return list(_SIGNATURES)
 
 
+def last_error() -> str:
+    """Thread-local message of the last failed call (coconet_last_error)."""
+    return load().coconet_last_error().decode(errors="replace")
+
+
 def check(status: int) -> None:
     if status != 0:
         msg = load().coconet_last_error().decode(errors="replace")

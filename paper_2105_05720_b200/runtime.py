@@ -126,12 +126,21 @@ class Context:
         dist.barrier(group=pg)
 
     def _nvls_setup(self, pg):
-        """coconet_nvls_setup's three collective stages, a process barrier after each."""
+        """coconet_nvls_setup's three collective stages. After each, the ranks
+        agree on success (a MAX all-reduce of the status instead of a bare
+        barrier), so a stage that fails on one rank raises on every rank and
+        no rank is left waiting in a later collective."""
         import torch.distributed as dist
 
+        dev = "cuda" if dist.get_backend(pg) == "nccl" else "cpu"
         for stage in range(3):
-            check(self.lib.coconet_nvls_setup(self.handle, stage))
-            dist.barrier(group=pg)
+            rc = int(self.lib.coconet_nvls_setup(self.handle, stage))
+            msg = _lib.last_error() if rc else ""
+            flag = torch.tensor([rc], dtype=torch.int32, device=dev)
+            dist.all_reduce(flag, op=dist.ReduceOp.MAX, group=pg)
+            if int(flag.item()):
+                raise _lib.CoconetError(rc or int(flag.item()),
+                                        f"NVLS setup stage {stage}: " + (msg or "failed on another rank"))
 
     @property
     def nvls(self) -> bool:

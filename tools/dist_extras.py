@@ -295,14 +295,122 @@ def c5(ctx, out, nvl_peak):
     out["c5"] = res
 
 
-def run_all(ctx, nvl_peak, tc_peak, only=("c1", "c3", "c4", "c5")):
+def _max_rel_dev(a, b) -> float:
+    """max |a - b| over the largest magnitude of either (the tests' measure), on the device."""
+    a, b = torch.as_tensor(a).double().flatten(), torch.as_tensor(b).double().flatten()
+    if a.numel() == 0:
+        return 0.0
+    scale = max(1e-12, float(a.abs().max()), float(b.abs().max()))
+    return float((a - b).abs().max()) / scale
+
+
+def nvls(ctx, out, nvl_peak):
+    """NVLS (NVSwitch multicast) against the P2P two-shot on the same inputs:
+    fused Adam (C1 size and 2^26), the tensor-list AllReduce (2^26 fp32) and
+    fused LAMB on the BERT-336M list (fp16 g). Runs only when every rank can
+    create a multicast object (coconet_nvls_supported); the setup fails on all
+    ranks together (runtime.Context._nvls_setup). Reported beside two-shot:
+    time, and the max relative deviation from two-shot's result after one
+    call from identical state (the switch sums in its own order)."""
+    from paper_2105_05720_b200.collectives import LambHParams, allreduce, fused_rs_lamb_ag
+    from paper_2105_05720_b200.runtime import Context, nvls_supported
+    from paper_2105_05720_b200.workloads import bert_large_counts
+
+    W, r = ctx.world, ctx.rank
+    ok, why = nvls_supported(ctx.device, W)
+    if share_mode() or max_over(0.0 if ok else 1.0) > 0:
+        out["nvls"] = {"unavailable": why or "multicast unsupported on another rank (or share mode)"}
+        return
+    counts = bert_large_counts()
+    n_l = sum(counts)
+    heap = 2 * (n_l * 6 + 2 * (n_l // W + (1 << 20)) * 4) + (3 << 30)
+    nctx = Context(W, mode="distributed", rank=r, device=ctx.device, heap_bytes=heap, heap="nvls")
+    res = {"workload": f"W={W}: Adam fp32 2^20 / 2^26, AllReduce fp32 2^26, LAMB BERT-336M fp16 g",
+           "mode": "NVLS: multimem.ld_reduce RS + multimem.st AG through the NVSwitch",
+           "p2p_two_shot_nvlink_bytes_per_rank_dir_per_elem_fp32": 2 * (W - 1) / W * 4,
+           "nvls_nvlink_bytes_per_rank_dir_per_elem_fp32": (W + 1) / W * 4}
+    try:
+        for n in (1 << 20, 1 << 26):
+            tl = TensorList(nctx, [n])
+            g, p = nctx.alloc([n]), nctx.alloc([n])
+            m, v = nctx.alloc([tl.state_elems]), nctx.alloc([tl.state_elems])
+            got = {}
+            for algo, an in ((_lib.ALGO_TWO_SHOT, "two_shot"), (_lib.ALGO_NVLS, "nvls")):
+                def reset():
+                    torch.manual_seed(r)
+                    nctx.view(g).normal_()
+                    torch.manual_seed(100)
+                    nctx.view(p).uniform_(0.1, 0.9)
+                    nctx.view(m).zero_()
+                    nctx.view(v).fill_(1e-3)
+                    torch.cuda.synchronize()
+                    dist.barrier()
+                hp = AdamHParams(1e-3, 0.9, 0.999, 1.0, 1e-8, False, _lib.MATH_FAST, algo)
+                reset()
+                fused_rs_adam_ag(nctx, tl, [g], [p], m, v, hp)
+                nctx.check()
+                got[an] = nctx.view(p).clone()
+                res[f"adam_{n}_{an}_us"] = dtime(lambda: fused_rs_adam_ag(nctx, tl, [g], [p], m, v, hp),
+                                                 steps=20) * 1e3
+            res[f"adam_{n}_nvls_max_rel_dev"] = max_over(_max_rel_dev(got["nvls"], got["two_shot"]))
+            res[f"adam_{n}_nvls_speedup"] = res[f"adam_{n}_two_shot_us"] / res[f"adam_{n}_nvls_us"]
+            if n == 1 << 26:
+                o = nctx.alloc([n])
+                outs = {}
+                for algo, an in ((_lib.ALGO_TWO_SHOT, "two_shot"), (_lib.ALGO_NVLS, "nvls")):
+                    allreduce(nctx, tl, [g], [o], algo=algo)
+                    nctx.check()
+                    outs[an] = nctx.view(o).clone()
+                    res[f"allreduce_{n}_{an}_us"] = dtime(lambda: allreduce(nctx, tl, [g], [o], algo=algo),
+                                                          steps=20) * 1e3
+                res[f"allreduce_{n}_nvls_max_rel_dev"] = max_over(_max_rel_dev(
+                    outs["nvls"], outs["two_shot"]))
+                res[f"allreduce_{n}_nvls_speedup"] = res[f"allreduce_{n}_two_shot_us"] / res[f"allreduce_{n}_nvls_us"]
+                nctx.free(o)
+            for b in (g, p, m, v):
+                nctx.free(b)
+            tl.close()
+        # LAMB, BERT-336M list, fp16 g: the default schedule across ranks (TMA) vs NVLS
+        tl = TensorList(nctx, counts, bucket_cap=16384)
+        gs = [nctx.alloc([n], torch.float16) for n in counts]
+        ps = [nctx.alloc([n]) for n in counts]
+        m, v = nctx.alloc([tl.shard_elems]), nctx.alloc([tl.shard_elems])
+        got = {}
+        for sched, sn in ((_lib.LAMB_AUTO, "auto"), (_lib.LAMB_NVLS, "nvls")):
+            torch.manual_seed(r)
+            for x in gs:
+                nctx.view(x).normal_()
+            torch.manual_seed(100)
+            for x in ps:
+                nctx.view(x).uniform_(0.1, 0.9)
+            nctx.view(m).zero_()
+            nctx.view(v).fill_(1e-3)
+            torch.cuda.synchronize()
+            dist.barrier()
+            hp = LambHParams(lr=1e-3, beta1=0.9, beta2=0.999, t=1.0, sched=sched)
+            fused_rs_lamb_ag(nctx, tl, gs, ps, m, v, hp)
+            nctx.check()
+            got[sn] = torch.cat([nctx.view(x) for x in ps])
+            res[f"lamb_bert_{sn}_ms"] = dtime(lambda: fused_rs_lamb_ag(nctx, tl, gs, ps, m, v, hp), steps=10)
+        res["lamb_bert_nvls_max_rel_dev"] = max_over(_max_rel_dev(got["nvls"], got["auto"]))
+        res["lamb_bert_nvls_speedup"] = res["lamb_bert_auto_ms"] / res["lamb_bert_nvls_ms"]
+        tl.close()
+    finally:
+        out["nvls"] = res
+        torch.cuda.synchronize()
+        dist.barrier()
+        nctx.close()
+
+
+def run_all(ctx, nvl_peak, tc_peak, only=("c1", "c3", "c4", "c5", "nvls")):
     """Runs the configs (collective). Returns the dict rank 0 reports."""
     out = {"mode": "DISTRIBUTED, one process per GPU" + (" (share mode: all ranks on GPU 0, gloo)" if share_mode()
                                                            else ", peers over NVLink, NCCL for the baselines"),
            "nvlink_peak_gbs": nvl_peak}
     for name in only:
         fn = {"c1": lambda: c1(ctx, out, nvl_peak), "c3": lambda: c3(ctx, out, nvl_peak, tc_peak),
-              "c4": lambda: c4(ctx, out, nvl_peak), "c5": lambda: c5(ctx, out, nvl_peak)}[name]
+              "c4": lambda: c4(ctx, out, nvl_peak), "c5": lambda: c5(ctx, out, nvl_peak),
+              "nvls": lambda: nvls(ctx, out, nvl_peak)}[name]
         try:
             fn()
         except Exception as e:
@@ -326,7 +434,7 @@ def main():
         dist.init_process_group("gloo")
     else:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    only = tuple(sys.argv[1].split(",")) if len(sys.argv) > 1 else ("c1", "c3", "c4", "c5")
+    only = tuple(sys.argv[1].split(",")) if len(sys.argv) > 1 else ("c1", "c3", "c4", "c5", "nvls")
     n5 = C5_PARAMS // (64 if share_mode() else 1)
     ctx = Context(world, mode="distributed", rank=rank, device=local,
                   heap_bytes=2 * n5 * 4 + 2 * (n5 // world + (1 << 20)) * 4 + (2 << 30))
