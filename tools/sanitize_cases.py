@@ -4,7 +4,8 @@ also with a hold of 1 so windows, spills and the TMEM/shared-memory slot ring
 all run), Adam (LDG, TMA at W = 1..3), tensor-list AllReduce,
 Reduce/Broadcast, RS/AG, the MP epilogue, the tile-flag overlapped tcgen05
 GEMM + all-reduce, the all-gather -> GEMM MP kernel (AUTO), the plain GEMM
-(1-SM and the 2-SM pair kernel), and the PP send.
+(1-SM and the 2-SM pair kernel), and the PP send; the DP cases also on a
+cuMem-backed heap.
 Usage: compute-sanitizer --tool TOOL python tools/sanitize_cases.py"""
 import os
 import sys
@@ -22,9 +23,9 @@ from paper_2105_05720_b200.collectives import (AdamHParams, BdrHParams, LambHPar
 from paper_2105_05720_b200.runtime import Context  # noqa: E402
 
 
-def dp(W, cap):
+def dp(W, cap, heap="default"):
     counts = [3000, 77, 5000, 1, 4096]
-    ctx = Context(W, heap_bytes=32 << 20, timeout_ms=20000)
+    ctx = Context(W, heap_bytes=32 << 20, timeout_ms=20000, heap=heap)
     tl = TensorList(ctx, counts, bucket_cap=cap)
     g = [ctx.alloc([n], torch.float16) for n in counts]
     p = [ctx.alloc([n]) for n in counts]
@@ -104,6 +105,7 @@ def mp_pp(W):
 if __name__ == "__main__":
     for W, cap in ((1, 1024), (1, 4096), (2, 1024), (4, 512), (2, 16384), (3, 16384)):  # 16384: Adam TMA at W>1
         dp(W, cap)
+    dp(2, 1024, heap="cumem")  # the cuMem-backed heap (csrc/heap_cumem.cu)
     for W in (2, 4):
         rooted_axis(W)
     for W in (1, 2, 4):
