@@ -1247,6 +1247,25 @@ __device__ __forceinline__ void wait_equal(const uint32_t* p, uint32_t want, con
   asm volatile("fence.acq_rel.gpu;" ::: "memory");
 }
 
+// The ONCHIP window protocol's poll: acquire loads (no trailing gpu-scope
+// fence: a fence waits for this thread's outstanding stores, microseconds
+// under a saturated HBM; profiles/r02_lamb_onchip_trace.json). The caller
+// shares what it observed with bar.sync.
+__device__ __forceinline__ void wait_equal_acq(const uint32_t* p, uint32_t want, const RankSet& rs) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  if (v == want) return;
+  const unsigned long long t0 = globaltimer();
+  for (int i = 1;; ++i) {
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    if (v == want) return;
+    if ((i & 255) == 0 && globaltimer() - t0 > rs.timeout_ns) {
+      atomicCAS(rs.status, 0, COCONET_ERR_TIMEOUT);
+      return;
+    }
+  }
+}
+
 // Chunk descriptor handed from the producer to the consumers with its stage.
 struct ChunkD {
   int64_t toff, sidx, aoff, boff, item;  // item < 0: end of this CTA's phase
@@ -1569,6 +1588,9 @@ struct LambOC {
   int hold, cap, head, head2, tslots;
   int slot_off;  // byte offset of the shared-memory u slots from the ring base
   int nosync;    // profiling only (COCONET_LAMB_OC_NOSYNC=1): skip the window waits, results invalid
+  // profiling only (COCONET_LAMB_OC_TRACE=<heap offset>): per (window, CTA)
+  // globaltimer at [0] pass 1 finished, [1] pass-2 wait reached, [2] released
+  unsigned long long* trace;
 };
 
 __device__ __forceinline__ int64_t oc_first(int64_t b, int c, int G) {
@@ -1882,8 +1904,12 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) lamb_onchip_kernel(OptArgs a
         if (lane == 0) mbar_arrive(&s_p1done[(kk + 1) & 1]);
         asm volatile("bar.sync 1, %0;" ::"n"(NW * 32) : "memory");
         if (ctid == 0) {
-          __threadfence();
-          atomicAdd(&oc.cnt[kk + 1], 1u);
+          if (oc.trace) oc.trace[(int64_t(kk + 1) * NG + cta) * 4 + 0] = globaltimer();
+          // release: this thread's part[] stores (the flush) before the arrival
+          if (oc.nosync == 2)  // profiling only: relaxed arrival (no ordering of part[]), to time the release
+            asm volatile("red.relaxed.gpu.global.add.u32 [%0], 1;" ::"l"(&oc.cnt[kk + 1]) : "memory");
+          else
+            asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(&oc.cnt[kk + 1]) : "memory");
         }
       };
       if (kk + 1 < K && n1 == 0) finish_p1();
@@ -1892,7 +1918,9 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) lamb_onchip_kernel(OptArgs a
         const bool p1 = kind == 1;
         if (!p1 && j == 0) {
           // window kk's norms: every CTA's pass 1 is in, reduce in CTA order
-          if (ctid == 0 && !oc.nosync) wait_equal(&oc.cnt[kk], uint32_t(NG), rs);
+          if (ctid == 0 && oc.trace) oc.trace[(int64_t(kk) * NG + cta) * 4 + 1] = globaltimer();
+          if (ctid == 0 && oc.nosync != 1) wait_equal_acq(&oc.cnt[kk], uint32_t(NG), rs);
+          if (ctid == 0 && oc.trace) oc.trace[(int64_t(kk) * NG + cta) * 4 + 2] = globaltimer();
           asm volatile("bar.sync 1, %0;" ::"n"(NW * 32) : "memory");
           const int t2e = oc.tfirst[kk + 1];
           for (int t = t2 + warp; t < t2e; t += NW) {
@@ -2818,7 +2846,9 @@ int coconet_fused_rs_lamb_ag(coconet_ctx_t c, coconet_tlist_t tl, const void* co
     oc.head2 = h2e ? std::max(0, std::min(8, atoi(h2e))) : 0;
     oc.slot_off = slot_off;
     const char* ns = getenv("COCONET_LAMB_OC_NOSYNC");
-    oc.nosync = ns && ns[0] == '1';
+    oc.nosync = ns ? atoi(ns) : 0;
+    const char* tr = getenv("COCONET_LAMB_OC_TRACE");
+    oc.trace = tr ? reinterpret_cast<unsigned long long*>(rs.base[0] + atoll(tr)) : nullptr;
     const size_t smem = 128 + size_t(slot_off) + size_t(smem_slots) * slot_bytes;
     rc = ensure_smem(c, fn, smem);
     if (rc) return rc;
