@@ -1735,7 +1735,7 @@ __device__ __forceinline__ void mbar_wait_lazy(uint64_t* bar, uint32_t parity) {
 }
 
 template <typename G, int NW, int QPT>
-__global__ void __launch_bounds__((NW + 1) * 32, 1) lamb_onchip_kernel(OptArgs a, LambK k, TmaArgs ta, LambOC oc) {
+__global__ void __launch_bounds__((NW + 2) * 32, 1) lamb_onchip_kernel(OptArgs a, LambK k, TmaArgs ta, LambOC oc) {
   using ST = TmaStage<G, NW, QPT>;
   constexpr int kChunkQ = ST::CHUNK_Q;
   constexpr int kFpt = QPT * 4;               // u floats per consumer thread per chunk
@@ -1746,9 +1746,18 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) lamb_onchip_kernel(OptArgs a
   __shared__ char* s_base[kMaxRanks];
   __shared__ float s_red[2][NW][2];
   __shared__ __align__(16) OcStage s_desc[kMaxStages];
-  __shared__ float s_ratio[kOcMaxTensors];
+  __shared__ float s_ratio[3][kOcMaxTensors];  // window % 3
   __shared__ uint32_t s_tmem;
   __shared__ __align__(8) uint64_t s_p1done[2];  // window parity: one phase per two windows
+  // per-tensor release: the consumers hand every finished tensor's CTA
+  // partial (P, U, tensor) to the sync warp through this queue; the sync warp
+  // publishes it, counts the arrival and turns globally complete tensors into
+  // ratios, announced per window as (window << 16) | ratios ready
+  constexpr int kQN = 32;
+  __shared__ __align__(16) float4 s_q[kQN];
+  __shared__ volatile uint32_t s_qhead, s_qtail;
+  __shared__ volatile int s_p1windows;  // windows whose pass 1 this CTA completed (monotonic)
+  __shared__ volatile uint32_t s_ready[3];
   const RankSet& rs = a.rs;
   if (threadIdx.x < kMaxRanks) s_base[threadIdx.x] = threadIdx.x < rs.world ? rs.base[threadIdx.x] : nullptr;
   const int S = ta.stages;
@@ -1764,6 +1773,9 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) lamb_onchip_kernel(OptArgs a
     }
     mbar_init(&s_p1done[0], NW);
     mbar_init(&s_p1done[1], NW);
+    s_qhead = s_qtail = 0u;
+    s_p1windows = 0;
+    s_ready[0] = s_ready[1] = s_ready[2] = 0xffffffffu;
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   }
@@ -1854,6 +1866,81 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) lamb_onchip_kernel(OptArgs a
         }
       }
     }
+  } else if (warp == NW + 1) {
+    // ---------------- sync warp: per-tensor release of the norms
+    uint32_t qt = 0;
+    int w = 0, tn = K > 0 ? oc.tfirst[0] : 0;
+    unsigned long long t_last = globaltimer();
+    while (w < K) {
+      bool moved = false;
+      // every decision is lane 0's, broadcast: the warp stays converged for the shuffles
+      const uint32_t qh = __shfl_sync(0xffffffffu, s_qhead, 0);
+      if (qh != qt) {  // publish this CTA's finished tensors (at most kQN = 32 entries: one per lane)
+        moved = true;
+        __threadfence_block();
+        int te_ = -1;
+        if (uint32_t(lane) < qh - qt) {
+          const float4 e = s_q[(qt + uint32_t(lane)) % kQN];
+          te_ = __float_as_int(e.z);
+          oc.part[int64_t(te_) * NG + cta] = make_double2(double(e.x), double(e.y));
+        }
+        __threadfence();  // the partials before the arrivals (only this warp's own stores are pending)
+        if (te_ >= 0) atomicAdd(&oc.cnt[K + 1 + te_], 1u);
+        __syncwarp();
+        qt = qh;
+        if (lane == 0) s_qtail = qt;
+      }
+      // window w's ratios in tensor order. Buffer w % 3 is free once this
+      // CTA finished pass 1 of window w - 1, which orders it after its pass 2
+      // of window w - 3 (the last reader of that buffer). A monotonic count,
+      // not the s_p1done parity: that barrier may already be a phase further.
+      const int te = oc.tfirst[w + 1];
+      if (tn >= te) {
+        ++w;
+        moved = true;
+      } else if (__shfl_sync(0xffffffffu, int(w < 3 || s_p1windows >= w), 0)) {
+        // lanes probe the next 32 tensors' arrival counters at once
+        const int tp = tn + lane;
+        bool done_l = false;
+        if (tp < te) {
+          const int nl = int(min(oc.titem[tp + 1] - oc.titem[tp], int64_t(NG)));
+          uint32_t c;
+          asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(c) : "l"(&oc.cnt[K + 1 + tp]) : "memory");
+          done_l = c == uint32_t(nl);
+        }
+        const uint32_t mask = __ballot_sync(0xffffffffu, done_l);
+        const int nb = mask == 0xffffffffu ? 32 : __ffs(~mask) - 1;  // complete tensors in a row
+        const int tb = oc.tfirst[w], buf = w % 3;
+        for (int b = 0; b < nb; ++b, ++tn) {
+          const int64_t i0 = oc.titem[tn];
+          const int n = int(min(oc.titem[tn + 1] - i0, int64_t(NG)));
+          const int c0 = int(i0 % NG);
+          double P = 0.0, U = 0.0;
+          for (int r = lane; r < n; r += 32) {
+            const int cc = c0 + r >= NG ? c0 + r - NG : c0 + r;
+            const double2 pu = __ldcg(&oc.part[int64_t(tn) * NG + cc]);
+            P += pu.x;
+            U += pu.y;
+          }
+          P = warp_sum(P);
+          U = warp_sum(U);
+          if (lane == 0) {
+            s_ratio[buf][tn - tb] = float(trust_ratio(P, U, k));
+            __threadfence_block();
+            s_ready[buf] = (uint32_t(w) << 16) | uint32_t(tn - tb + 1);
+            if (oc.trace && tn + 1 == te) oc.trace[(int64_t(w) * NG + cta) * 4 + 2] = globaltimer();
+          }
+          __syncwarp();
+        }
+        moved |= nb > 0;
+      }
+      if (moved) {
+        t_last = globaltimer();
+      } else {
+        __nanosleep(32);
+        if (globaltimer() - t_last > 10000000000ull) __trap();  // watchdog: a CTA never arrived
+      }
+    }
   } else {
     // ---------------- consumers
     const int ctid = threadIdx.x;
@@ -1888,7 +1975,11 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) lamb_onchip_kernel(OptArgs a
             tp += s_red[red][w][0];
             tu += s_red[red][w][1];
           }
-          oc.part[int64_t(cur_t) * NG + cta] = make_double2(double(tp), double(tu));
+          const uint32_t h = s_qhead;
+          while (h - s_qtail >= uint32_t(kQN)) __nanosleep(32);  // full: the sync warp drains it
+          s_q[h % kQN] = make_float4(tp, tu, __int_as_float(cur_t), 0.f);
+          __threadfence_block();
+          s_qhead = h + 1;
         }
         red ^= 1;
         sp = su = 0.f;
@@ -1903,43 +1994,12 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) lamb_onchip_kernel(OptArgs a
         __syncwarp();
         if (lane == 0) mbar_arrive(&s_p1done[(kk + 1) & 1]);
         asm volatile("bar.sync 1, %0;" ::"n"(NW * 32) : "memory");
-        if (ctid == 0) {
-          if (oc.trace) oc.trace[(int64_t(kk + 1) * NG + cta) * 4 + 0] = globaltimer();
-          // release: this thread's part[] stores (the flush) before the arrival
-          if (oc.nosync == 2)  // profiling only: relaxed arrival (no ordering of part[]), to time the release
-            asm volatile("red.relaxed.gpu.global.add.u32 [%0], 1;" ::"l"(&oc.cnt[kk + 1]) : "memory");
-          else
-            asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(&oc.cnt[kk + 1]) : "memory");
-        }
+        if (ctid == 0) s_p1windows = kk + 2;  // every consumer warp is past pass 1 of window kk + 1
       };
       if (kk + 1 < K && n1 == 0) finish_p1();
       int j, kind;
       while ((kind = seq.next(j)) != 0) {
         const bool p1 = kind == 1;
-        if (!p1 && j == 0) {
-          // window kk's norms: every CTA's pass 1 is in, reduce in CTA order
-          if (ctid == 0 && oc.trace) oc.trace[(int64_t(kk) * NG + cta) * 4 + 1] = globaltimer();
-          if (ctid == 0 && oc.nosync != 1) wait_equal_acq(&oc.cnt[kk], uint32_t(NG), rs);
-          if (ctid == 0 && oc.trace) oc.trace[(int64_t(kk) * NG + cta) * 4 + 2] = globaltimer();
-          asm volatile("bar.sync 1, %0;" ::"n"(NW * 32) : "memory");
-          const int t2e = oc.tfirst[kk + 1];
-          for (int t = t2 + warp; t < t2e; t += NW) {
-            const int64_t i0 = oc.titem[t];
-            const int n = int(min(oc.titem[t + 1] - i0, int64_t(NG)));
-            const int c0 = int(i0 % NG);
-            double P = 0.0, U = 0.0;
-            for (int r = lane; r < n; r += 32) {
-              const int c = c0 + r >= NG ? c0 + r - NG : c0 + r;
-              const double2 pu = __ldcg(&oc.part[int64_t(t) * NG + c]);
-              P += pu.x;
-              U += pu.y;
-            }
-            P = warp_sum(P);
-            U = warp_sum(U);
-            if (lane == 0) s_ratio[t - t2] = float(trust_ratio(P, U, k));
-          }
-          asm volatile("bar.sync 1, %0;" ::"n"(NW * 32) : "memory");
-        }
         mbar_wait_lazy(&full[st], ph);
         const OcStage d = s_desc[st];
         if (p1 && d.tensor != cur_t) {
@@ -1963,7 +2023,20 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) lamb_onchip_kernel(OptArgs a
             }
           }
         }
-        const float ratio = p1 ? 0.f : s_ratio[d.tensor - t2];
+        float ratio = 0.f;
+        if (!p1) {  // this tensor's ratio: published by the sync warp once every CTA's pass 1 of it is in
+          const uint32_t want = uint32_t(d.tensor - t2);
+          if (oc.nosync != 1) {
+            uint32_t rv = s_ready[kk % 3];
+            for (int i = 1; (rv >> 16) != uint32_t(kk) || (rv & 0xffffu) <= want; ++i) {
+              __nanosleep(20);
+              rv = s_ready[kk % 3];
+              if ((i & 1023) == 0 && failed(rs)) break;
+            }
+            __threadfence_block();
+          }
+          ratio = s_ratio[kk % 3][want];
+        }
         float fp = 0.f, fu = 0.f;
 #pragma unroll
         for (int qq = 0; qq < QPT; ++qq) {
@@ -2058,7 +2131,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) lamb_onchip_kernel(OptArgs a
   if (threadIdx.x == 0) {
     __threadfence();
     if (atomicAdd(&oc.cnt[K], 1u) == uint32_t(NG) - 1u) {
-      for (int i = 0; i <= K; ++i) oc.cnt[i] = 0u;
+      for (int i = 0; i <= K + a.n_tensors; ++i) oc.cnt[i] = 0u;
       __threadfence();
     }
   }
@@ -2804,7 +2877,7 @@ int coconet_fused_rs_lamb_ag(coconet_ctx_t c, coconet_tlist_t tl, const void* co
         using STt = decltype(st_tag);
         fn = reinterpret_cast<const void*>(kern);
         sbytes = STt::BYTES;
-        threads = STt::THREADS;
+        threads = STt::THREADS + 32;  // + the sync warp
         chunk_q = STt::CHUNK_Q;
       };
       if (shape == 161) use(&lamb_onchip_kernel<Gt, 16, 1>, TmaStage<Gt, 16, 1>{});

@@ -27,7 +27,7 @@ struct OcItem {
   int64_t toff, sidx, qa;
   int len, tensor;
 };
-constexpr int kOcMaxTensors = 256;  // tensors per ONCHIP window (shared-memory ratio table)
+constexpr int kOcMaxTensors = 96;  // tensors per ONCHIP window (shared-memory ratio table)
 
 __host__ __device__ __forceinline__ int64_t pack_meta(int tensor, int len, int owner) {
   return (int64_t(tensor) << 32) | (int64_t(len & 0xffffff) << 8) | int64_t(owner & 0xff);

@@ -510,7 +510,7 @@ int tlist_onchip_plan(coconet_tlist* tl, int blocks, int hold, int chunk_q) {
   auto al = [](size_t n) { return (std::max<size_t>(n, 1) + 255) / 256 * 256; };
   const size_t b_items = al(items.size() * sizeof(OcItem)), b_wi = al(wi.size() * sizeof(int64_t));
   const size_t b_tf = al(tfirst.size() * sizeof(int)), b_ti = al(titem.size() * sizeof(int64_t));
-  const size_t b_part = al(size_t(tl->n_tensors) * blocks * sizeof(double2)), b_cnt = al(size_t(K + 1) * sizeof(uint32_t));
+  const size_t b_part = al(size_t(tl->n_tensors) * blocks * sizeof(double2)), b_cnt = al(size_t(K + 1 + tl->n_tensors) * sizeof(uint32_t));
   CN_CUDA(cudaMalloc(&tl->oc_mem, b_items + b_wi + b_tf + b_ti + b_part + b_cnt));
   char* p = static_cast<char*>(tl->oc_mem);
   tl->d_oc_items = reinterpret_cast<OcItem*>(p);
