@@ -1570,13 +1570,15 @@ __global__ void __launch_bounds__((NW + 1) * 32, 2) lamb_win_kernel(OptArgs a, L
 // of P1(k+1), then P2(k) and the rest of P1(k+1) alternating, so the wait for
 // window k's norms is covered by pass-1 work and the ring always mixes heavy
 // (22 B) and light (8 B) items. Held items take ring slots in order
-// (live <= hold + head = cap). Norms: each CTA sums its items of a tensor
-// (thread partials, then the 8 warps in fixed order) into part[t][cta]; a
-// window's pass 1 is complete when its arrival counter reaches the grid size
-// (cumulative over calls: no reset kernel), after which every CTA reduces the
-// partials of the window's tensors in CTA order (deterministic) into a
-// shared-memory ratio table. m', v' are TMA's bit for bit; u is the same
-// lamb_u of the same fp32 m', v', p; only the norm summation order differs.
+// (live <= hold + head = cap). Norms, released per tensor: each CTA sums
+// its items of a tensor (thread partials, then the warps in fixed order) and
+// queues the CTA partial to its sync warp, which stores it to part[t][cta],
+// counts the arrival on the tensor's counter and, once a tensor's arrivals
+// are complete, reduces its partials in CTA order (deterministic) into a
+// shared-memory ratio table; pass 2 of a tensor waits for its own ratio only.
+// Counters are zeroed by the last CTA out (graph replay). m', v' are TMA's
+// bit for bit; u is the same lamb_u of the same fp32 m', v', p; only the
+// norm summation order differs.
 struct LambOC {
   const OcItem* items;
   const int64_t* wi;     // [K+1]

@@ -4,7 +4,9 @@ pass-2 norm wait and when it was released (COCONET_LAMB_OC_TRACE = heap
 offset of the trace buffer). BERT-336M list, W=1, fp16 g, 16384-element
 buckets. Prints the per-window finish skew across CTAs, the wait each CTA
 saw and the release latency after the last arrival.
-Usage: python tools/lamb_trace_probe.py"""
+The per-window fields belong to the per-window protocol (commit cf562ce);
+since the per-tensor release only [2] (the window's last ratio ready in the
+CTA) is recorded. Usage: python tools/lamb_trace_probe.py"""
 import json
 import os
 import statistics
