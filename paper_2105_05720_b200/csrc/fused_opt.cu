@@ -1911,6 +1911,7 @@ __global__ void __launch_bounds__((NW + 2) * 32, 1) lamb_onchip_kernel(OptArgs a
           done_l = c == uint32_t(nl);
         }
         const uint32_t mask = __ballot_sync(0xffffffffu, done_l);
+        __syncwarp();  // orders the acquiring lanes' loads before every lane's partial reads
         const int nb = mask == 0xffffffffu ? 32 : __ffs(~mask) - 1;  // complete tensors in a row
         const int tb = oc.tfirst[w], buf = w % 3;
         for (int b = 0; b < nb; ++b, ++tn) {
@@ -2932,6 +2933,8 @@ int coconet_fused_rs_lamb_ag(coconet_ctx_t c, coconet_tlist_t tl, const void* co
     if (rc) return rc;
     rc = tlist_onchip_plan(tl, blocks, oc.hold, chunk_q);
     if (rc) return rc;
+    if (tl->oc_K >= 0xffff)
+      return set_error(COCONET_ERR_UNSUPPORTED, "ONCHIP LAMB: more than 65534 windows (use the TMA schedule)");
     oc.items = tl->d_oc_items;
     oc.wi = tl->d_oc_wi;
     oc.tfirst = tl->d_oc_tfirst;
