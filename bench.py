@@ -40,7 +40,7 @@ NVLINK_GBS = 770.0  # B200_PROFILING.md's measured peer copy per direction (900 
 BUCKET_CAP = 16384  # N=1: segments of the TMA LAMB schedule
 BUCKET_CAP_MULTI = 16384  # N>1: the TMA schedule across ranks is fastest at 16384
 # (W=2/8 virtual, profiles/r01_lamb_w_probe.json); GRID would prefer 4096
-E2E_GROUPS = 16  # tensor groups pipelined against PCIe in the e2e measurement
+E2E_GROUPS = int(os.environ.get("COCONET_E2E_GROUPS", "16"))  # tensor groups pipelined against PCIe (e2e)
 CPU_SAMPLE = 10 << 20  # elements per core for cpu_baseline: ~15 s of CPU work on the B200 host (4M took 6 s)
 
 

@@ -7,6 +7,7 @@ rank). See include/coconet_cuda.h for the reference routine each one replaces.
 from __future__ import annotations
 
 import ctypes as C
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -327,6 +328,14 @@ class LambHostPipeline:
             m = ctx.alloc([tl.shard_elems], torch.float32)
             v = ctx.alloc([tl.shard_elems], torch.float32)
             self.groups.append(dict(tl=tl, grads=grads, params=params, lo=lo, hi=hi, m=m, v=v))
+        # launch order: the smallest group first (the D2H stream starts
+        # early) and the next smallest last (the final D2H, which nothing
+        # overlaps, is short); the rest in list order
+        if len(self.groups) > 2 and os.environ.get("COCONET_E2E_ORDER", "small_ends") == "small_ends":
+            by_size = sorted(range(len(self.groups)), key=lambda i: self.groups[i]["hi"] - self.groups[i]["lo"])
+            first, last = by_size[0], by_size[1]
+            mid = [i for i in range(len(self.groups)) if i not in (first, last)]
+            self.groups = [self.groups[i] for i in [first] + mid + [last]]
         self.g_flat, self.p_flat = g_flat, p_flat
         self.h2d = torch.cuda.Stream(device=ctx.device)
         self.d2h = torch.cuda.Stream(device=ctx.device)
