@@ -76,6 +76,14 @@ struct FdServer {
       if (r <= 0) continue;
       const int cfd = accept4(sock, nullptr, nullptr, SOCK_CLOEXEC);
       if (cfd < 0) continue;
+      // abstract sockets are visible to every process of the network
+      // namespace: hand descriptors (device memory) to the same user only
+      ucred cr{};
+      socklen_t crl = sizeof(cr);
+      if (getsockopt(cfd, SOL_SOCKET, SO_PEERCRED, &cr, &crl) != 0 || cr.uid != getuid()) {
+        close(cfd);
+        continue;
+      }
       uint32_t slot = 0;
       pollfd pc{cfd, POLLIN, 0};
       if (poll(&pc, 1, 2000) == 1 && recv(cfd, &slot, sizeof(slot), MSG_WAITALL) == ssize_t(sizeof(slot))) {

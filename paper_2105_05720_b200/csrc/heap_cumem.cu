@@ -320,6 +320,7 @@ int coconet_nvls_setup(coconet_ctx_t c, int stage) {
   CN_CU(drv().cuDeviceGet(&dev, c->device));
   if (stage == 0) {
     if (c->rank == 0) {
+      if (!c->fdsrv) return set_error(COCONET_ERR_INVALID_INPUT, "call coconet_open_peers before coconet_nvls_setup");
       CUmulticastObjectProp p{};
       p.numDevices = unsigned(c->world);
       p.size = c->heap_bytes;
@@ -332,7 +333,6 @@ int coconet_nvls_setup(coconet_ctx_t c, int stage) {
         return cu_fail(r, "cuMemExportToShareableHandle(multicast)");
       }
       c->mc_fd = fd;
-      if (!c->fdsrv) return set_error(COCONET_ERR_INVALID_INPUT, "call coconet_open_peers before coconet_nvls_setup");
       c->fdsrv->set(1, fd);
       c->mc_stage = 1;
     } else {
