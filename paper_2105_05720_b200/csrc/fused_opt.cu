@@ -2686,6 +2686,7 @@ constexpr int64_t kTmaMinBucket = 4096;
 constexpr int64_t kDefaultWindow = int64_t(2) << 20;
 // ONCHIP LAMB in AUTO from this many elements per shard (group size 1)
 constexpr int64_t kOnchipMinElems = int64_t(1) << 20;
+constexpr int kOcHead2 = 1;  // spilled cover items per window (COCONET_LAMB_OC_HEAD2 overrides)
 
 int check_state(coconet_ctx* c, const void* ptr, int64_t* off) {
   int rc = heap_offset(c, ptr, off);
@@ -2919,7 +2920,10 @@ int coconet_fused_rs_lamb_ag(coconet_ctx_t c, coconet_tlist_t tl, const void* co
     oc.hold = oc.cap - oc.head;
     if (const char* ke = getenv("COCONET_LAMB_OC_HOLD")) oc.hold = std::max(1, std::min(oc.hold, atoi(ke)));
     const char* h2e = getenv("COCONET_LAMB_OC_HEAD2");
-    oc.head2 = h2e ? std::max(0, std::min(8, atoi(h2e))) : 0;
+    // one spilled cover item per window by default: it keeps the ring busy
+    // while a pass-2 tensor's ratio is still out (-0.7% per step on BERT-336M,
+    // profiles/r02_lamb_onchip_head_sweep.txt); its elements re-read m', v'
+    oc.head2 = h2e ? std::max(0, std::min(8, atoi(h2e))) : kOcHead2;
     oc.slot_off = slot_off;
     const char* ns = getenv("COCONET_LAMB_OC_NOSYNC");
     oc.nosync = ns ? atoi(ns) : 0;
@@ -2931,7 +2935,7 @@ int coconet_fused_rs_lamb_ag(coconet_ctx_t c, coconet_tlist_t tl, const void* co
     int blocks = 0;
     rc = coop_blocks(c, fn, threads, smem, tl->group, int64_t(c->sm_count), &blocks);
     if (rc) return rc;
-    rc = tlist_onchip_plan(tl, blocks, oc.hold, chunk_q);
+    rc = tlist_onchip_plan(tl, blocks, oc.hold, chunk_q, oc.head, oc.head2);
     if (rc) return rc;
     if (tl->oc_K >= 0xffff)
       return set_error(COCONET_ERR_UNSUPPORTED, "ONCHIP LAMB: more than 65534 windows (use the TMA schedule)");

@@ -103,7 +103,7 @@ struct coconet_tlist {
   // ONCHIP LAMB schedule (group size 1): windows of whole tensors sized so that
   // every CTA holds its share of a window's u on chip (TMEM + shared memory),
   // built on first use for a grid size / hold depth (tlist_onchip_plan)
-  int oc_blocks = 0, oc_hold = 0, oc_chunk_q = 0, oc_K = 0;
+  int oc_blocks = 0, oc_hold = 0, oc_chunk_q = 0, oc_K = 0, oc_head = 0, oc_head2 = 0;
   int64_t oc_n_items = 0;
   void* oc_mem = nullptr;
   coconet::OcItem* d_oc_items = nullptr;  // [n_items] chunk items, tensor-major
@@ -126,7 +126,9 @@ int tlist_window_plan(coconet_tlist* tl, int64_t win_elems, int chunk_q);
 // Builds (or keeps) the ONCHIP-LAMB plan: chunk items of chunk_q quads in
 // tensor order, cut into windows of whole tensors of at most blocks * hold
 // items (a longer tensor is a window alone) and kOcMaxTensors tensors.
-int tlist_onchip_plan(coconet_tlist* tl, int blocks, int hold, int chunk_q);
+// head / head2: the kernel's cover items (oc_held), so the spilled count
+// includes the head2 cover items that take the m', v' re-read path
+int tlist_onchip_plan(coconet_tlist* tl, int blocks, int hold, int chunk_q, int head = 1, int head2 = 0);
 int tlist_bind(coconet_tlist* tl, const void* const* a, const void* const* b, int a_elem_bytes,
                int b_elem_bytes, cudaStream_t stream);
 }

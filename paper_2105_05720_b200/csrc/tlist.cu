@@ -459,8 +459,10 @@ int tlist_window_plan(coconet_tlist* tl, int64_t win_elems, int chunk_q) {
 // window of at most blocks * hold items gives every CTA at most `hold` of
 // them to keep on chip. Windows hold whole tensors: a tensor of more items
 // is a window alone and its CTAs spill the items beyond `hold`.
-int tlist_onchip_plan(coconet_tlist* tl, int blocks, int hold, int chunk_q) {
-  if (tl->oc_mem && tl->oc_blocks == blocks && tl->oc_hold == hold && tl->oc_chunk_q == chunk_q) return COCONET_OK;
+int tlist_onchip_plan(coconet_tlist* tl, int blocks, int hold, int chunk_q, int head, int head2) {
+  if (tl->oc_mem && tl->oc_blocks == blocks && tl->oc_hold == hold && tl->oc_chunk_q == chunk_q &&
+      tl->oc_head == head && tl->oc_head2 == head2)
+    return COCONET_OK;
   const int64_t* ptr = tl->csr_ptr.data() + tl->csr_begin[0];
   std::vector<OcItem> items;
   std::vector<int64_t> wi{0}, titem{0};
@@ -491,13 +493,17 @@ int tlist_onchip_plan(coconet_tlist* tl, int blocks, int hold, int chunk_q) {
     tfirst.push_back(tl->n_tensors);
   }
   const int K = int(wi.size()) - 1;
-  // elements of the items a CTA cannot hold (its j-th item of a window, j >= hold)
+  // elements of the items a CTA does not hold (its j-th of n items of a
+  // window: j >= hold, or one of the head2 cover items after the head; the
+  // kernel's oc_held)
   int64_t spilled = 0;
   for (int w = 0; w < K; ++w)
     for (int64_t i = wi[size_t(w)]; i < wi[size_t(w) + 1]; ++i) {
       const int64_t c = i % blocks;
       int64_t f = wi[size_t(w)] + ((c - wi[size_t(w)]) % blocks + blocks) % blocks;
-      if ((i - f) / blocks < hold) continue;
+      const int64_t j = (i - f) / blocks, n = (wi[size_t(w) + 1] - 1 - f) / blocks + 1;
+      const int64_t h = std::min<int64_t>(head, n), h2 = std::min<int64_t>(head2, n - h);
+      if (j < hold && !(j >= h && j < h + h2)) continue;
       const OcItem& it = items[size_t(i)];
       const int64_t e0 = std::max(it.toff, it.qa * 4), e1 = std::min(it.toff + it.len, (it.qa + chunk_q) * 4);
       spilled += e1 - e0;
@@ -527,6 +533,8 @@ int tlist_onchip_plan(coconet_tlist* tl, int blocks, int hold, int chunk_q) {
   CN_CUDA(cudaMemset(tl->d_oc_cnt, 0, b_cnt));
   tl->oc_blocks = blocks;
   tl->oc_hold = hold;
+  tl->oc_head = head;
+  tl->oc_head2 = head2;
   tl->oc_chunk_q = chunk_q;
   tl->oc_K = K;
   tl->oc_n_items = int64_t(items.size());
