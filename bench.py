@@ -492,7 +492,8 @@ def run_coconet(args):
     shard = N / W
     # per-rank HBM bytes: W=1 the ONCHIP schedule (AUTO) moves
     # 30 B/elem (pass 1: g 2 + m, v, p 12 read, m', v' 8 written; pass 2: p 4 +
-    # 4) plus 8 B for every element whose u did not fit on chip (its pass 2
+    # 4) plus 8 B for every element whose u is not held on chip (past the hold,
+    # or a per-window cover item; its pass 2
     # re-reads m', v'); the two-pass TMA schedule 38 B/elem. W>1 (TMA): the
     # shard's 38 B minus its g read / p write (served by the peers' HBM) plus
     # this rank's whole g read by its owners (2N) and whole p written by them (4N)

@@ -186,7 +186,8 @@ int coconet_tlist_chunk(coconet_tlist_t tl, int r, int64_t* lo, int64_t* hi);
 int64_t coconet_tlist_segments(coconet_tlist_t tl, int r, int64_t* tensor, int64_t* toff,
                                int64_t* len, int64_t* sidx, int64_t cap);
 /* ONCHIP-LAMB plan of the last ONCHIP launch on this list: elements whose u
- * did not fit on chip (their pass 2 re-reads m', v'), or -1 if none was built.
+ * is not held on chip (beyond a CTA's hold, or a per-window cover item; their
+ * pass 2 re-reads m', v'), or -1 if none was built.
  * Pass-level bytes at fp16 g: 30 per element + 8 per spilled element. */
 int64_t coconet_tlist_onchip_spilled(coconet_tlist_t tl);
 /* Shard index of flat position `pos` inside its owner's shard storage. */

@@ -80,7 +80,7 @@ class TensorList:
         return np.stack([np.frombuffer(b, dtype=np.int64)[:got] for b in bufs], axis=1)
 
     def onchip_spilled(self) -> int:
-        """Elements the last ONCHIP-LAMB launch could not hold on chip (-1: no plan)."""
+        """Elements the last ONCHIP-LAMB launch did not hold on chip (past the hold or cover items; -1: no plan)."""
         return int(self.lib.coconet_tlist_onchip_spilled(self.handle))
 
     def state_index_map(self, r: int):
